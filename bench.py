@@ -1,0 +1,489 @@
+"""Benchmark: LK trigger->done round trips on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lk|reference]
+
+Workload (BASELINE.json configs[1]): one persistent CTA on each of the 148
+SMs, empty task, round-robin single-worker dispatch ``mask = 1 << (k % 148)``.
+A *step* is ``--rounds`` (default 20,000) closed-loop trigger+wait round
+trips driven from C (lk_bench_roundtrip); the default 50 steps are the 1e6
+rounds the config names.  ``value`` = round trips (tasks) per second over the
+whole job (sum over ranks / max-over-ranks time).  Latency is host-observed
+by definition (trigger start -> FINISHED seen, native.py:256-259), so it is
+timed with CLOCK_MONOTONIC per round.  A device-wide synchronize cannot bracket
+the region: the persistent kernel stays resident, so cudaDeviceSynchronize (and
+torch.cuda.synchronize) would never return.  The C loop is itself synchronous
+(every round ends with the workers' NOP observed on the host), and ranks
+barrier (gloo, CPU-only) on both sides.
+
+Extra objects on the JSON line: latency percentiles and jitter, the
+cudaLaunchKernel+cudaStreamSynchronize baseline, the raw PCIe ping-pong
+floor, the full-148-worker variant, payload HBM GB/s (SAXPY / block reduce
+1-64 MiB, L2-cold by buffer rotation, device globaltimer spans), the roofline
+of the dominant payload kernel and the CPU baseline (oracle port of the
+reference executor, timed on this host).
+
+Multi-GPU (torchrun): one independent LK instance per GPU, host thread pinned
+to the GPU's NUMA-local cores; "replicas only", no collective on the path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MEASURED_PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0
+L2_BYTES = 126 * 1024 * 1024
+
+
+def pct(a, q):
+    return float(np.percentile(np.asarray(a, dtype=np.float64), q))
+
+
+def lat_summary(ns):
+    ns = np.asarray(ns, dtype=np.float64)
+    p50, p999 = pct(ns, 50), pct(ns, 99.9)
+    return {"p50_us": round(p50 / 1e3, 3), "p99_us": round(pct(ns, 99) / 1e3, 3),
+            "p99.9_us": round(p999 / 1e3, 3), "max_us": round(float(ns.max()) / 1e3, 3),
+            "mean_us": round(float(ns.mean()) / 1e3, 3), "jitter_us": round((p999 - p50) / 1e3, 3),
+            "n": int(ns.size)}
+
+
+def hbm_peak():
+    try:
+        j = json.loads(MEASURED_PEAKS.read_text())
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (getattr(self, "out", "") or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- dist
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")   # CPU collectives only: no kernels beside the resident LK
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def gather_max_sum(world, t_s, units):
+    if world == 1:
+        return t_s, units
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([t_s], dtype=torch.float64)
+    u = torch.tensor([units], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
+def aggregate(rank_times, rank_units):
+    """Whole-job throughput: total units / slowest rank's time."""
+    return sum(rank_units) / max(rank_times)
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+
+def cpu_baseline_port(num_workers=4, rounds=1000, warmup=50, n=65536, threshold=10_000, budget_s=30.0):
+    """The oracle port of the reference executor (oracle/cpu_session.py) on this
+    host: BASELINE config 0 (4 workers, int32 vector add of 64 Ki elements on
+    the worker thread, round-robin masks)."""
+    from oracle import work as W
+    from oracle.cpu_session import CpuSession
+    a = np.random.default_rng(0).integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    b = np.random.default_rng(1).integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    outs = [np.empty(n, np.int32) for _ in range(num_workers)]
+
+    def work_fn(i, slot):
+        np.copyto(outs[i], W.vector_add_i32(a, b))
+
+    s = CpuSession(num_workers=num_workers, spin_yield_threshold=threshold, work_fn=work_fn)
+    s.start()
+    lat = []
+    t_start = time.perf_counter()
+    for k in range(warmup + rounds):
+        m = 1 << (k % num_workers)
+        t0 = time.perf_counter_ns()
+        s.trigger(m, 0)
+        s.wait(m)
+        if k >= warmup:
+            lat.append(time.perf_counter_ns() - t0)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    s.dispose()
+    tot = sum(lat) / 1e9
+    return len(lat) / tot, lat
+
+
+def run_reference_arm(args, world, rank):
+    """--impl reference: the reference's CPU executor (oracle port) on our config."""
+    if rank != 0:
+        return
+    from oracle.cpu_session import CpuSession
+    workers = args.workers or 148
+    s = CpuSession(num_workers=workers, spin_yield_threshold=200)
+    s.start()
+    per_step = args.ref_rounds
+
+    def step(k0):
+        for k in range(k0, k0 + per_step):
+            m = 1 << (k % workers)
+            s.trigger(m, 0)
+            s.wait(m)
+
+    k = 0
+    for _ in range(args.warmup):
+        step(k)
+        k += per_step
+    lat = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for kk in range(k, k + per_step):
+            m = 1 << (kk % workers)
+            a = time.perf_counter_ns()
+            s.trigger(m, 0)
+            s.wait(m)
+            lat.append(time.perf_counter_ns() - a)
+        k += per_step
+    dt = time.perf_counter() - t0
+    s.dispose()
+    rounds = per_step * args.steps
+    value = rounds / dt
+    cores = len(os.sched_getaffinity(0))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tasks/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"empty-task round-robin dispatch, {workers} persistent workers",
+                   "rounds_per_step": per_step, "executor": "thread-per-worker CPU port of "
+                   "persistkern.native (oracle/cpu_session.py), spin_yield_threshold=200"},
+        "latency_us": lat_summary(lat),
+        "cpu_baseline": {"value": round(value, 3), "unit": "tasks/s", "cores": cores, "kind": "port",
+                         "sample": f"{rounds} round trips on {workers} Python worker threads (GIL-bound)"},
+        "e2e": {"value": round(value, 3), "unit": "tasks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "trigger->done round trips per second (empty task, 148 persistent workers)"
+
+
+# ----------------------------------------------------------------------------- LK arm
+
+def measure_payload(session, kind, sizes_mib, reps, rotate_bytes):
+    """GB/s of a payload kind dispatched to all workers, L2-cold by rotation."""
+    from paper_2310_01212_b200 import host
+    from paper_2310_01212_b200.device import BYTES_PER_ELEMENT, DeviceBuffer, WorkDescriptor
+    full = host.full_mask(session.num_workers)
+    out = {}
+    for mib in sizes_mib:
+        n = (mib << 20) // 4
+        per_set = (8 if kind == "saxpy_f32" else 4) * n
+        sets = max(2, min(64, -(-rotate_bytes // per_set)))
+        bufs, works = [], []
+        for k in range(sets):
+            if kind == "saxpy_f32":
+                x, y = DeviceBuffer(4 * n), DeviceBuffer(4 * n)
+                bufs += [x, y]
+                works.append(WorkDescriptor(slot=100 + k, kind=kind, data_in_ref=(x, y), data_out_ref=y, alpha=1.5))
+            else:
+                x, p, t = DeviceBuffer(4 * n), DeviceBuffer(4 * 160), DeviceBuffer(8)
+                bufs += [x, p, t]
+                works.append(WorkDescriptor(slot=100 + k, kind=kind, data_in_ref=x, data_out_ref=p, total_ref=t))
+        for w in works:
+            session.register(w, full)
+        spans, e2e = [], []
+        for r in range(reps + 2):
+            w = works[r % sets]
+            t0 = time.perf_counter_ns()
+            session.trigger(full, w)
+            session.wait(full)
+            t1 = time.perf_counter_ns()
+            b, e = session.last_spans()
+            if r >= 2:
+                spans.append(int(e.max()) - int(b.min()))
+                e2e.append(t1 - t0)
+        nbytes = BYTES_PER_ELEMENT[kind] * n
+        med_span = statistics.median(spans)
+        out[f"{mib}MiB"] = {"bytes": nbytes, "device_span_us": round(med_span / 1e3, 3),
+                            "gbs_device": round(nbytes / med_span, 1),
+                            "gbs_e2e": round(nbytes / statistics.median(e2e), 1),
+                            "rotation_sets": sets}
+        for bf in bufs:
+            bf.free()
+    return out
+
+
+def standalone_kernel_gbs(device, kind, mib, reps=20):
+    """Same work function as an ordinary kernel (148 CTAs), CUDA-event timed."""
+    from paper_2310_01212_b200 import native
+    from paper_2310_01212_b200.device import BYTES_PER_ELEMENT, DeviceBuffer, WorkDescriptor
+    n = (mib << 20) // 4
+    sets = 6
+    b = native.LaunchSyncBaseline(device=device)
+    bufs, works = [], []
+    for k in range(sets):
+        x, y = DeviceBuffer(4 * n, device), DeviceBuffer(4 * n, device)
+        bufs += [x, y]
+        works.append(WorkDescriptor(slot=0, kind=kind, data_in_ref=(x, y), data_out_ref=y, alpha=1.5))
+    ms = []
+    for r in range(reps):
+        ms.append(b.time_kernel(works[r % sets], 1))
+    b.close()
+    for bf in bufs:
+        bf.free()
+    med = statistics.median(ms[2:])
+    return {"ms": round(med, 4), "gbs": round(BYTES_PER_ELEMENT[kind] * n / (med * 1e6), 1)}
+
+
+def run_lk_arm(args, world, rank, local):
+    from paper_2310_01212_b200 import host, native
+    from paper_2310_01212_b200.device import WorkDescriptor
+
+    device = local
+    pinned = 0
+    try:
+        pinned = native.pin_host_thread(device)
+    except Exception:
+        pinned = 0
+    cfg = native.NativeConfig(num_workers=args.workers, device=device, spin_strategy=native.PURE_SPIN,
+                              poll_backoff_ns=args.backoff_ns, cell_stride=args.cell_stride)
+    session, init = native.NativeSession.start(cfg)
+    n = session.num_workers
+    empty = WorkDescriptor(slot=0, kind="empty")
+    session.register(empty)
+    rr_masks = [1 << i for i in range(n)]
+    R = args.rounds
+
+    for _ in range(args.warmup):
+        session.bench_roundtrip(rr_masks, 0, R)
+
+    barrier(world)
+    done_all, cyc_all = [], []
+    with ClockSampler(device) as clk:
+        t0 = time.perf_counter_ns()
+        for _ in range(args.steps):
+            _, done, cyc = session.bench_roundtrip(rr_masks, 0, R)
+            done_all.append(done)
+            cyc_all.append(cyc)
+        t1 = time.perf_counter_ns()
+    barrier(world)
+    elapsed = (t1 - t0) / 1e9
+    rounds = R * args.steps
+    t_max, units = gather_max_sum(world, elapsed, rounds)
+    value = units / t_max
+    done_all = np.concatenate(done_all)
+    cyc_all = np.concatenate(cyc_all)
+
+    extras = {}
+    # full-148-worker dispatch
+    full = host.full_mask(n)
+    _, fdone, fcyc = session.bench_roundtrip([full], 0, args.full_rounds)
+    extras["full_mask"] = {"trigger_to_done": lat_summary(fdone), "round_trip": lat_summary(fcyc),
+                           "tasks_per_s": round(args.full_rounds / (fcyc.sum() / 1e9), 1)}
+
+    # e2e through the Python API (reference-facing plugin), host buffers = mailbox words
+    e2e_rounds = args.e2e_rounds
+    t0 = time.perf_counter_ns()
+    for k in range(e2e_rounds):
+        m = rr_masks[k % n]
+        session.trigger(m, empty)
+        session.wait(m)
+    e2e_dt = (time.perf_counter_ns() - t0) / 1e9
+    e2e_value = e2e_rounds / e2e_dt
+
+    payload = {}
+    if not args.no_payload and rank == 0:
+        payload["saxpy_f32"] = measure_payload(session, "saxpy_f32", args.payload_mib, args.payload_reps,
+                                               4 * L2_BYTES)
+        payload["block_reduce_f32"] = measure_payload(session, "block_reduce_f32", args.payload_mib,
+                                                      args.payload_reps, 4 * L2_BYTES)
+    smids = session.smid_map
+    session.dispose()
+    session.close()
+
+    # conventional launch+sync baseline, same host thread
+    base = {}
+    b1 = native.LaunchSyncBaseline(device=device)
+    for name, grid in (("grid1", 1), ("grid148", n)):
+        b1.bench(empty, 200, grid)
+        launch, total = b1.bench(empty, args.base_rounds, grid)
+        base[name] = {"launch": lat_summary(launch), "launch_plus_sync": lat_summary(total)}
+    b1.close()
+    pp = native.pingpong(device, args.pp_rounds)
+    extras["pingpong_floor"] = lat_summary(pp[100:])
+
+    if rank != 0:
+        return
+    peak, peak_src = hbm_peak()
+    roof = None
+    if payload:
+        big = f"{max(args.payload_mib)}MiB"
+        ach = payload["saxpy_f32"][big]["gbs_device"]
+        traffic = None
+        tf = ROOT / "profiles" / "saxpy_traffic.json"
+        if tf.exists():
+            try:
+                traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": f"lk_persistent_kernel saxpy_f32 {big} (148 workers)",
+                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes": payload["saxpy_f32"][big]["bytes"],
+                "timing": "device %globaltimer span, first worker begin -> last worker end"}
+        try:
+            extras["standalone_saxpy_kernel"] = standalone_kernel_gbs(device, "saxpy_f32", max(args.payload_mib))
+        except Exception as exc:  # pragma: no cover
+            extras["standalone_saxpy_kernel"] = {"error": str(exc)}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cv, clat = cpu_baseline_port(budget_s=args.cpu_budget_s)
+        cpu = {"value": round(cv, 2), "unit": "tasks/s", "cores": 1, "kind": "port",
+               "sample": f"{len(clat)} round trips of BASELINE config 0 (4 Python worker threads, "
+                         "int32 vector add 64 Ki elements via numpy on the worker, spin_yield_threshold "
+                         "10000 = reference default); GIL-serialised so ~1 core; p50 "
+                         f"{lat_summary(clat)['p50_us']} us"}
+
+    base_p50 = base["grid1"]["launch_plus_sync"]["p50_us"]
+    lk = lat_summary(done_all)
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tasks/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * t_max / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "configs[1]: empty-task dispatch, 1 persistent CTA per SM on all SMs, "
+                               "round-robin single-worker masks", "workers": n, "rounds_per_step": R,
+                   "total_rounds": int(units), "threads_per_worker": cfg.threads_per_worker,
+                   "cell_stride": cfg.cell_stride, "poll_backoff_ns": cfg.poll_backoff_ns,
+                   "host_cores_pinned": pinned, "l2": "n/a for the empty task (no payload); payload "
+                   "GB/s rotate buffers over >= 4x L2",
+                   "timing": "host CLOCK_MONOTONIC per round; max over ranks"},
+        "latency_us": {"trigger_to_done": lk, "round_trip_with_ack": lat_summary(cyc_all),
+                       "init_ms": round(init.cycles / 1e6, 2)},
+        "launch_sync_baseline": base,
+        "speedup_vs_launch_sync_p50": round(base_p50 / lk["p50_us"], 2),
+        "speedup_vs_launch_sync_p999": round(base["grid1"]["launch_plus_sync"]["p99.9_us"] / lk["p99.9_us"], 2),
+        **extras,
+        "payload": payload,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_value, 1), "unit": "tasks/s",
+                "h2d_bytes_per_step": 8 * R, "d2h_bytes_per_step": 24 * R,
+                "note": "Python API session.trigger+session.wait per task (ctypes -> liblk.so); "
+                        "host<->device traffic is the mailbox words themselves (WORK+ack down, "
+                        "WORKING/FINISHED/NOP status cells up)"},
+        "gpu_launches": 1,
+        "gpu_launch_note": "one persistent kernel resident across the timed region; tasks are "
+                           "dispatched by mailbox words, not launches",
+        "smid_distinct": len(set(smids)),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["lk", "reference"], default="lk")
+    ap.add_argument("--rounds", type=int, default=20_000, help="round trips per step")
+    ap.add_argument("--workers", type=int, default=None)
+    ap.add_argument("--backoff-ns", type=int, default=0)
+    ap.add_argument("--cell-stride", type=int, default=8)
+    ap.add_argument("--full-rounds", type=int, default=100_000)
+    ap.add_argument("--e2e-rounds", type=int, default=100_000)
+    ap.add_argument("--base-rounds", type=int, default=100_000)
+    ap.add_argument("--pp-rounds", type=int, default=100_000)
+    ap.add_argument("--payload-mib", type=int, nargs="+", default=[1, 4, 16, 64])
+    ap.add_argument("--payload-reps", type=int, default=30)
+    ap.add_argument("--no-payload", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=30.0)
+    ap.add_argument("--ref-rounds", type=int, default=10, help="reference arm round trips per step")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+    else:
+        run_lk_arm(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,261 @@
+/*
+ * lk.h -- C ABI of the B200 LightKernel (LK) persistent-worker runtime.
+ *
+ * This is the drop-in boundary for the reference's `native` executor
+ * (persistkern.native.NativeSession, /root/reference/pkg/src/persistkern/native.py).
+ * Every entry point is extern "C", never throws, takes plain pointers and
+ * sizes, and returns an int status (LK_OK or a negative LK_E_* code).
+ * Worker = one CTA of one persistent sm_100a kernel, pinned to its own SM.
+ *
+ * Each function names the reference interface it replaces (file:line, paths
+ * relative to /root/reference/pkg/src/persistkern/).
+ */
+#ifndef LK_H_
+#define LK_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: 1:1 with persistkern.errors (errors.py:5-59) ---------- */
+#define LK_OK               0
+#define LK_E_USAGE         -1  /* UsageError            errors.py:58-59 */
+#define LK_E_BUSY          -2  /* BusyTriggerError      errors.py:31-32 */
+#define LK_E_DISPOSE_BUSY  -3  /* DisposeWhileBusyError errors.py:35-36 */
+#define LK_E_HANG          -4  /* HangDetected          errors.py:43-55 */
+#define LK_E_INIT          -5  /* InitError             errors.py:39-40 */
+#define LK_E_WORKER_DIED   -6  /* UsageError("worker i died") native.py:128-131 */
+#define LK_E_CUDA          -7  /* CUDA runtime failure (no reference analogue) */
+#define LK_E_CONFIG        -8  /* ConfigError           errors.py:23-24 */
+#define LK_E_PROTOCOL      -9  /* ProtocolViolation     errors.py:9-20 */
+#define LK_E_TRACE_LOST   -10  /* device trace ring overflowed */
+
+/* ---- wire words: protocol.py:31-45 ---------------------------------------- */
+#define LK_INIT       0u
+#define LK_FINISHED   1u
+#define LK_WORKING    2u
+#define LK_NOP        4u
+#define LK_EXIT       8u
+#define LK_WORK_BASE 16u
+
+/* ---- worker phases: protocol.py:104-109 ----------------------------------- */
+#define LK_PHASE_BOOTING   0u
+#define LK_PHASE_IDLE      1u
+#define LK_PHASE_WORKING   2u
+#define LK_PHASE_FINISHED  3u   /* FINISHED_PENDING_ACK */
+#define LK_PHASE_EXITED    4u
+
+/* ---- device-side error codes (lk_worker_error) ---------------------------- */
+#define LK_WERR_NONE          0u
+#define LK_WERR_ILLEGAL_WORD  1u  /* decode_to_gpu rejects: protocol.py:83-91 */
+#define LK_WERR_BUSY_SLOT     2u  /* other slot while WORKING: protocol.py:182-186 */
+#define LK_WERR_UNACKED_SLOT  3u  /* other slot while awaiting ack: protocol.py:192-197 */
+#define LK_WERR_AFTER_EXIT    4u  /* stepped after exit: protocol.py:163-164 */
+#define LK_WERR_BAD_SLOT      5u  /* slot outside the device descriptor table */
+#define LK_WERR_BAD_KIND      6u  /* UnsupportedWorkloadError analogue (device.py:114-118) */
+#define LK_WERR_BAD_COMPLETE  7u  /* completion outside WORKING: protocol.py:203-204 */
+
+/* ---- work kinds (device.py:16 has only "busy_loop") ------------------------ */
+#define LK_KIND_EMPTY             0u  /* iterations ignored: the 0-iteration task */
+#define LK_KIND_BUSY_LOOP         1u  /* native.py:63-67 */
+#define LK_KIND_VECTOR_ADD_I32    2u  /* out[i] = in0[i] + in1[i] mod 2^32 */
+#define LK_KIND_SAXPY_F32         3u  /* out[i] = fl(fl(alpha*in0[i]) + in1[i]) */
+#define LK_KIND_BLOCK_REDUCE_F32  4u  /* out[rank] = sum(chunk); *(double*)aux = total */
+#define LK_KIND_HBM_STREAM        5u  /* out[i] = in0[i], `iterations` passes (>=1) */
+#define LK_KIND_COUNT             6u
+
+/* descriptor flags */
+#define LK_DF_SCALAR   1u   /* pointers not 16-B aligned: scalar path */
+
+/*
+ * Work descriptor, 64 B POD, device-resident per slot.
+ * Replaces WorkDescriptor (device.py:48-66) + the `descriptors` dict
+ * (native.py:91, written 223, read 180).  Multi-worker kinds shard [0, n)
+ * over the workers of the trigger mask: worker of rank r (popcount of mask
+ * bits below it) takes the r-th 128-B-aligned chunk.
+ */
+typedef struct lk_desc {
+  uint32_t kind;
+  uint32_t flags;
+  uint64_t iterations;
+  uint64_t n;          /* elements */
+  uint64_t in0;        /* device pointers */
+  uint64_t in1;
+  uint64_t out;
+  uint64_t aux;        /* BLOCK_REDUCE: double* total (0 = no combine) */
+  float    alpha;
+  uint32_t reserved;
+} lk_desc;
+
+/* Session configuration; replaces NativeConfig (native.py:44-60). */
+typedef struct lk_config {
+  uint32_t num_workers;          /* 0 = one per SM (148 on B200) */
+  uint32_t threads_per_worker;   /* 0 = 512 */
+  int32_t  device;               /* CUDA ordinal */
+  uint32_t spin_strategy;        /* 0 pure_spin, 1 spin_then_yield (native.py:40-41) */
+  uint32_t spin_yield_threshold; /* host spins before sched_yield */
+  uint32_t record_trace;         /* native.py:51 */
+  uint32_t trace_capacity;       /* device records per worker; 0 = 65536 */
+  uint32_t poll_backoff_ns;      /* device __nanosleep between idle polls (0 = none) */
+  uint32_t cell_stride;          /* bytes between mailbox cells: 8, 64 or 128; 0 = 8 */
+  uint32_t num_slots;            /* descriptor table entries; 0 = 1024 */
+  uint64_t wait_timeout_ns;      /* wait_timeout_s (native.py:52) */
+  uint32_t flags;                /* LK_CF_* */
+  uint32_t reserved;
+} lk_config;
+
+#define LK_CF_ACQUIRE_POLL   1u  /* poll with ld.acquire.sys instead of ld.relaxed.sys */
+#define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
+
+/* One linearized protocol write; replaces TraceRecord (protocol.py:253-261). */
+typedef struct lk_trace_rec {
+  uint64_t step;     /* global order, consistent with per-worker causality */
+  uint32_t side;     /* 'H' or 'D' */
+  uint32_t worker;
+  uint32_t word;
+  uint32_t hseq;     /* host write index this record follows (per worker) */
+  uint64_t t_ns;     /* host: CLOCK_MONOTONIC; device: %globaltimer */
+} lk_trace_rec;
+
+typedef struct lk_session lk_session;
+typedef struct lk_baseline lk_baseline;
+
+/* ---- session lifecycle ---------------------------------------------------- */
+
+/* NativeSession.start (native.py:104-122): context, pinned mapped mailboxes,
+ * device descriptor table, cooperative launch of the persistent kernel, wait
+ * until every worker published INIT then NOP.  *init_ns = wall time. */
+int lk_create(const lk_config* cfg, lk_session** out, uint64_t* init_ns);
+
+/* NativeSession.dispose (native.py:277-295): EXIT to every worker, wait for the
+ * kernel to retire (timeout -> LK_E_HANG). */
+int lk_dispose(lk_session* s, uint64_t* elapsed_ns);
+
+/* Teardown ignoring the host rules (no reference analogue: the reference
+ * leaves dead sessions' daemon threads behind): EXIT to every worker, wait up
+ * to timeout_ns (0 = wait_timeout) for the kernel to retire. */
+int lk_abort(lk_session* s, uint64_t timeout_ns);
+
+/* Free host/device resources (after dispose, or to abandon a session). */
+int lk_destroy(lk_session* s);
+
+/* descriptors[slot] = work (native.py:223), staged device-resident ahead of
+ * the WORK word.  mask (nwords u64, little-endian bit i = worker i) is the
+ * worker set that will shard the payload.  Fails LK_E_USAGE while the slot is
+ * referenced by an un-waited dispatch (native.py:215-217). */
+int lk_register_desc(lk_session* s, uint32_t slot, const lk_desc* d,
+                     const uint64_t* mask, uint32_t nwords);
+
+/* NativeSession.trigger (native.py:208-231): validate (mask, busy workers,
+ * slot lock, idle cells -- in the reference's order), stage `d` into the slot
+ * when given and different from the staged copy (descriptors[slot] = work,
+ * "in place before the word lands"; NULL = use the registered descriptor),
+ * then write 16+slot to each masked worker in ascending order.
+ * *elapsed_ns = staging + word writes. */
+int lk_trigger(lk_session* s, const uint64_t* mask, uint32_t nwords,
+               uint32_t slot, const lk_desc* d, uint64_t* elapsed_ns);
+
+/* NativeSession.wait (native.py:250-275): spin until every masked worker
+ * published FINISHED (*finished_ns = call start -> that observation), write
+ * NOP acks ascending, spin until every masked worker republished NOP. */
+int lk_wait(lk_session* s, const uint64_t* mask, uint32_t nwords,
+            uint64_t* finished_ns);
+
+/* ---- introspection -------------------------------------------------------- */
+
+/* to_gpu / from_gpu cells and worker_phase (native.py:88-94), n entries. */
+int lk_read_cells(lk_session* s, uint32_t* to_gpu, uint32_t* from_gpu,
+                  uint32_t* phase, uint32_t n);
+/* worker_error (native.py:93, 196-199): device-side code + offending word. */
+int lk_worker_error(lk_session* s, uint32_t worker, uint32_t* code, uint32_t* word);
+/* %smid of each worker (check_block_mapping idea, device.py:102-111). */
+int lk_smid_map(lk_session* s, uint32_t* smid, uint32_t n);
+int lk_num_workers(lk_session* s, uint32_t* n);
+/* pending_mask (native.py:95); mask out, nwords u64. */
+int lk_pending(lk_session* s, uint64_t* mask, uint32_t nwords);
+/* 1 while the persistent kernel is resident (Thread.is_alive analogue). */
+int lk_kernel_alive(lk_session* s, uint32_t* alive);
+
+/* Fault injection: store a raw word into worker's to_gpu cell, bypassing every
+ * host rule (the reference tests inject illegal words into traces,
+ * T/test_acceptance.py:168-176; this injects them into the live device). */
+int lk_debug_poke(lk_session* s, uint32_t worker, uint32_t word);
+
+/* ---- tracing (native.py:135-147, 297-299) ---------------------------------- */
+/* Number of linearized records available (host + device). */
+int lk_trace_count(lk_session* s, uint64_t* n);
+/* Merge the host log and the per-worker device rings into one linearization
+ * (per-worker causal order; cross-worker order by host time). */
+int lk_trace_read(lk_session* s, lk_trace_rec* out, uint64_t cap, uint64_t* n);
+
+/* ---- protocol: shared host/device state machine ---------------------------- */
+/* worker_step (protocol.py:151-198) as compiled into the kernel, run on the
+ * host: phase/slot in-out, publish = word or 0xFFFFFFFF (none), action =
+ * 0 none, 1 begin work, 2 exit.  Returns LK_OK or LK_E_PROTOCOL (*werr set). */
+int lk_protocol_step(uint32_t* phase, uint32_t* slot, uint32_t observed,
+                     uint32_t* publish, uint32_t* action, uint32_t* werr);
+/* complete_work (protocol.py:201-206). */
+int lk_protocol_complete(uint32_t* phase, uint32_t* slot, uint32_t* publish,
+                         uint32_t* werr);
+/* replay_trace / validate_trace (protocol.py:372-398) over n writes given as
+ * parallel arrays (side 'H'/'D').  *bad_index = -1 when valid; reason gets a
+ * NUL-terminated message.  counts (optional, 3*max_workers u64: sm id, host
+ * work writes, begins) mirror ReplayState.dispatch_counts (protocol.py:287-295). */
+int lk_validate_trace(const uint32_t* side, const int64_t* sm_id, const uint32_t* word,
+                      uint64_t n, int64_t* bad_index, char* reason, uint32_t reason_cap,
+                      uint64_t* counts, uint32_t max_workers, uint32_t* n_workers);
+
+/* ---- measurement ------------------------------------------------------------ */
+/* Closed-loop trigger+wait rounds entirely in C (GIL-free).  Round k uses
+ * masks[k % nmasks] (nwords u64 each) and `slot`.  Per round (arrays may be
+ * NULL): trig_ns = trigger call, done_ns = trigger start -> last FINISHED
+ * observed, cycle_ns = trigger start -> ack consumed. */
+int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks,
+                       uint32_t nwords, uint32_t slot, uint64_t rounds,
+                       uint64_t* trig_ns, uint64_t* done_ns, uint64_t* cycle_ns);
+/* Device-side spans of the last dispatch per worker (globaltimer ns):
+ * begin (WORK observed) and end (work done, before FINISHED). */
+int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n);
+
+/* Raw host<->GPU ping-pong floor: one thread polls a mapped host word and
+ * echoes it back; rounds samples of the round trip. */
+int lk_pingpong(int device, uint64_t rounds, uint64_t* rt_ns);
+
+/* ---- conventional baseline: cudaLaunchKernel + cudaStreamSynchronize --------
+ * Replaces ThreadSpawnBaseline (native.py:304-331).  The same device work
+ * functions as the persistent kernel, one CTA per worker of `grid`. */
+int lk_baseline_create(int device, uint32_t threads, lk_baseline** out);
+int lk_baseline_launch(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t* launch_ns);
+int lk_baseline_wait(lk_baseline* b, uint64_t* wait_ns);
+/* rounds of launch+sync; launch_ns / total_ns per round (may be NULL). */
+int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t rounds,
+                      uint64_t* launch_ns, uint64_t* total_ns);
+/* Device time of one launch via CUDA events on the launching stream: reps
+ * launches, avg ms per launch. */
+int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_t grid,
+                            uint32_t reps, float* avg_ms);
+int lk_baseline_destroy(lk_baseline* b);
+
+/* ---- host helpers ----------------------------------------------------------- */
+/* Pin the calling thread to the CPU cores local to the GPU's NUMA node
+ * (/sys/bus/pci/devices/<bdf>/local_cpulist).  *ncores = cores in the set. */
+int lk_pin_thread_near(int device, uint32_t* ncores);
+int lk_device_count(int* n);
+int lk_sm_count(int device, int* n);
+/* device memory helpers (payload buffers when the caller has no allocator) */
+int lk_dev_alloc(int device, uint64_t bytes, uint64_t* ptr);
+int lk_dev_free(uint64_t ptr);
+int lk_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes);
+int lk_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes);
+const char* lk_strerror(int code);
+/* message of the last failing call on this thread (may be empty) */
+const char* lk_last_error(void);
+uint32_t lk_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LK_H_ */

@@ -1,0 +1,1039 @@
+// lk_host.cu -- host side of the LK runtime behind the C ABI in include/lk.h.
+//
+// Owns the CUDA context use, the pinned mapped mailboxes, the device
+// descriptor table and the persistent kernel's stream.  All spinning happens
+// here, outside Python (ctypes releases the GIL for every call).
+//
+// Host rules follow persistkern.native.NativeSession
+// (/root/reference/pkg/src/persistkern/native.py:82-299): trigger validates
+// mask / busy / slot lock / idle (208-231), writes 16+slot ascending; wait spins
+// to FINISHED, acks with NOP ascending and spins to NOP (250-275); dispose
+// refuses while pending, writes EXIT, joins (277-295).
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <pthread.h>
+#include <sched.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#if defined(__x86_64__)
+#include <immintrin.h>
+#define LK_PAUSE() _mm_pause()
+#else
+#define LK_PAUSE() asm volatile("" ::: "memory")
+#endif
+
+#include "lk_internal.h"
+#include "lk_protocol.cuh"
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define LK_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(LK_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                               \
+  } while (0)
+
+static inline uint64_t now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return uint64_t(ts.tv_sec) * 1000000000ull + uint64_t(ts.tv_nsec);
+}
+
+// ------------------------------------------------------------------ service stream
+// Allocation, frees and staging copies never touch the legacy stream and never
+// synchronize the device: a resident persistent kernel never "completes", so a
+// device-wide sync (cudaDeviceSynchronize, cudaFree, cudaMemset) would block
+// forever.  Stream-ordered allocation on a private non-blocking stream does not.
+static std::mutex g_svc_mu;
+static cudaStream_t g_svc[64];
+
+static cudaStream_t svc_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_svc_mu);
+  if (!g_svc[dev]) {
+    cudaStreamCreateWithFlags(&g_svc[dev], cudaStreamNonBlocking);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;  // keep freed memory mapped: no unmap on sync
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  return g_svc[dev];
+}
+
+static cudaError_t dev_alloc(void** p, size_t bytes) {
+  cudaStream_t st = svc_stream();
+  cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, st);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(st);
+}
+
+static cudaError_t dev_free(void* p) {
+  if (!p) return cudaSuccess;
+  cudaStream_t st = svc_stream();
+  cudaError_t e = cudaFreeAsync(p, st);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(st);
+}
+
+// ------------------------------------------------------------------ session
+struct HostRec {
+  uint32_t hseq;
+  uint32_t word;
+  uint64_t t_ns;
+};
+
+struct lk_session {
+  lk_config cfg;
+  uint32_t nw = 0, nwords = 0, threads = 0;
+  int device = 0;
+  size_t smem = 0;
+  cudaStream_t stream = nullptr;   // persistent kernel
+  cudaStream_t copy_stream = nullptr;
+
+  // pinned mapped host block
+  uint8_t* host_block = nullptr;
+  uint32_t* to_gpu = nullptr;                 // stride cell_words
+  volatile unsigned long long* status = nullptr;  // stride cell_u64
+  uint32_t* hseq = nullptr;                   // stride cell_words
+  volatile unsigned long long* err = nullptr;
+  volatile uint32_t* smid = nullptr;
+  uint32_t cell_words = 2, cell_u64 = 1;
+
+  // device block
+  uint8_t* dev_block = nullptr;
+  lk_desc* d_desc = nullptr;
+  unsigned long long* d_mask = nullptr;
+  uint32_t* d_ctr = nullptr;
+  unsigned long long* d_spans = nullptr;
+  lk_dev_trace* d_trace = nullptr;
+  uint32_t* d_tcnt = nullptr;
+
+  // host bookkeeping (guarded by mu)
+  std::mutex mu;
+  std::vector<uint64_t> pending;                          // nwords
+  std::unordered_map<uint32_t, std::vector<uint64_t>> pending_by_slot;
+  std::vector<uint8_t> registered;                        // per slot
+  std::vector<lk_desc> reg_desc;                          // host copy per slot
+  std::vector<std::vector<uint64_t>> reg_mask;            // per slot (nwords)
+  bool disposed = false;
+  bool kernel_done = false;
+  uint64_t t_create = 0;
+
+  // tracing
+  std::vector<uint32_t> host_seq;                         // per worker
+  std::vector<std::vector<HostRec>> host_log;             // per worker
+
+  // scratch
+  std::vector<uint32_t> ids;
+
+  inline uint32_t word(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64]); }
+  inline uint32_t phase(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64] >> 32); }
+  inline void host_write(uint32_t i, uint32_t w) {
+    if (cfg.record_trace) {
+      const uint32_t s = ++host_seq[i];
+      __atomic_store_n(hseq + uint64_t(i) * cell_words, s, __ATOMIC_RELEASE);
+      host_log[i].push_back(HostRec{s, w, now_ns()});
+    }
+    __atomic_store_n(to_gpu + uint64_t(i) * cell_words, w, __ATOMIC_RELEASE);
+  }
+};
+
+static bool mask_ids(const lk_session* s, const uint64_t* mask, uint32_t nwords, std::vector<uint32_t>& ids,
+                     int* rc) {
+  ids.clear();
+  for (uint32_t k = 0; k < nwords; ++k) {
+    uint64_t m = mask[k];
+    while (m) {
+      const uint32_t b = uint32_t(__builtin_ctzll(m));
+      m &= m - 1;
+      const uint64_t id = uint64_t(k) * 64 + b;
+      if (id >= s->nw) {
+        *rc = fail(LK_E_USAGE, "sm mask wider than %u clusters", s->nw);
+        return false;
+      }
+      ids.push_back(uint32_t(id));
+    }
+  }
+  if (ids.empty()) {
+    *rc = fail(LK_E_USAGE, "sm mask must select at least one cluster");
+    return false;
+  }
+  return true;
+}
+
+static std::string ids_str(const std::vector<uint32_t>& v) {
+  std::string out = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i) out += ", ";
+    out += std::to_string(v[i]);
+  }
+  return out + "]";
+}
+
+// Worker errors surface on the next host call (native.py:128-131).
+static int check_workers(lk_session* s) {
+  for (uint32_t i = 0; i < s->nw; ++i) {
+    const unsigned long long e = s->err[i];
+    if (e) return fail(LK_E_WORKER_DIED, "worker %u died: device error %u on word %u", i, uint32_t(e),
+                       uint32_t(e >> 32));
+  }
+  return LK_OK;
+}
+
+static int require_live(lk_session* s) {
+  if (!s) return fail(LK_E_USAGE, "null session");
+  if (s->disposed) return fail(LK_E_USAGE, "session already disposed");
+  return check_workers(s);
+}
+
+static int kernel_status(lk_session* s) {
+  if (s->kernel_done) return 1;
+  cudaError_t q = cudaStreamQuery(s->stream);
+  if (q == cudaErrorNotReady) return 0;
+  s->kernel_done = true;
+  if (q != cudaSuccess) {
+    fail(LK_E_CUDA, "persistent kernel failed: %s", cudaGetErrorString(q));
+    return -1;
+  }
+  return 1;
+}
+
+struct Spinner {
+  const lk_session* s;
+  uint64_t deadline;
+  uint32_t spins = 0;
+  uint32_t checks = 0;
+  explicit Spinner(const lk_session* ss) : s(ss) { deadline = now_ns() + ss->cfg.wait_timeout_ns; }
+  // returns false on timeout
+  inline bool step() {
+    LK_PAUSE();
+    if (s->cfg.spin_strategy == 1 && ++spins >= s->cfg.spin_yield_threshold) {
+      spins = 0;
+      sched_yield();
+    }
+    if ((++checks & 1023u) == 0) return now_ns() <= deadline;
+    return true;
+  }
+};
+
+// Spin until word(i) == want for every id; checks worker errors and the
+// kernel on the slow path.  Returns LK_OK, LK_E_HANG or LK_E_WORKER_DIED.
+static int spin_words(lk_session* s, const std::vector<uint32_t>& ids, uint32_t want, const char* what) {
+  Spinner sp(s);
+  size_t j = 0;
+  while (j < ids.size()) {
+    if (s->word(ids[j]) == want) {
+      ++j;
+      continue;
+    }
+    if (!sp.step()) {
+      int rc = check_workers(s);
+      if (rc) return rc;
+      return fail(LK_E_HANG, "%s made no progress within %.3fs (workers %s)", what,
+                  double(s->cfg.wait_timeout_ns) / 1e9, ids_str(ids).c_str());
+    }
+    if ((sp.checks & 0xFFFFu) == 0) {
+      int rc = check_workers(s);
+      if (rc) return rc;
+      if (kernel_status(s) != 0) return fail(LK_E_WORKER_DIED, "persistent kernel is no longer running");
+    }
+  }
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ create
+extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* init_ns) {
+  if (!cfg_in || !out) return fail(LK_E_USAGE, "null argument");
+  *out = nullptr;
+  const uint64_t t0 = now_ns();
+  lk_config cfg = *cfg_in;
+  if (cfg.spin_strategy > 1) return fail(LK_E_USAGE, "unknown spin strategy %u", cfg.spin_strategy);
+  if (cfg.spin_strategy == 1 && cfg.spin_yield_threshold == 0)
+    return fail(LK_E_USAGE, "spin_yield_threshold must be positive");
+  if (cfg.cell_stride == 0) cfg.cell_stride = 8;
+  if (cfg.cell_stride != 8 && cfg.cell_stride != 16 && cfg.cell_stride != 32 && cfg.cell_stride != 64 &&
+      cfg.cell_stride != 128)
+    return fail(LK_E_CONFIG, "cell_stride must be 8, 16, 32, 64 or 128");
+  if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 512;
+  if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 1024)
+    return fail(LK_E_CONFIG, "threads_per_worker must be a multiple of 32 and <= 1024");
+  if (cfg.num_slots == 0) cfg.num_slots = 1024;
+  if (cfg.trace_capacity == 0) cfg.trace_capacity = 65536;
+  if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
+
+  int ndev = 0;
+  LK_CUDA(cudaGetDeviceCount(&ndev));
+  if (cfg.device < 0 || cfg.device >= ndev) return fail(LK_E_CONFIG, "no CUDA device %d", cfg.device);
+  LK_CUDA(cudaSetDevice(cfg.device));
+  cudaDeviceProp prop;
+  LK_CUDA(cudaGetDeviceProperties(&prop, cfg.device));
+  if (!prop.cooperativeLaunch) return fail(LK_E_INIT, "device lacks cooperative launch");
+  if (!prop.canMapHostMemory) return fail(LK_E_INIT, "device cannot map host memory");
+  const uint32_t nsm = uint32_t(prop.multiProcessorCount);
+  if (cfg.num_workers == 0) cfg.num_workers = nsm;
+  if (cfg.num_workers > nsm)
+    return fail(LK_E_CONFIG, "num_workers %u exceeds the %u SMs (one worker per SM)", cfg.num_workers, nsm);
+
+  auto* s = new lk_session();
+  s->cfg = cfg;
+  s->nw = cfg.num_workers;
+  s->nwords = (s->nw + 63) / 64;
+  s->threads = cfg.threads_per_worker;
+  s->device = cfg.device;
+  s->cell_words = cfg.cell_stride / 4;
+  s->cell_u64 = cfg.cell_stride / 8;
+  s->pending.assign(s->nwords, 0);
+  s->registered.assign(cfg.num_slots, 0);
+  s->reg_desc.resize(cfg.num_slots);
+  s->reg_mask.resize(cfg.num_slots);
+  s->host_seq.assign(s->nw, 0);
+  s->host_log.resize(s->nw);
+  s->t_create = t0;
+
+  auto cleanup = [&](int rc) {
+    if (s->host_block) cudaFreeHost(s->host_block);
+    if (s->dev_block) dev_free(s->dev_block);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    delete s;
+    return rc;
+  };
+
+  // --- pinned mapped mailboxes: to_gpu | status | hseq | err | smid, 4 KiB aligned
+  auto al = [](size_t x) { return (x + 4095) & ~size_t(4095); };
+  const size_t cells = al(size_t(s->nw) * cfg.cell_stride);
+  const size_t errb = al(size_t(s->nw) * 8), smidb = al(size_t(s->nw) * 4);
+  const size_t host_bytes = 3 * cells + errb + smidb;
+  cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&s->host_block), host_bytes,
+                                 cudaHostAllocMapped | cudaHostAllocPortable);
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(ce)));
+  memset(s->host_block, 0, host_bytes);
+  s->to_gpu = reinterpret_cast<uint32_t*>(s->host_block);
+  s->status = reinterpret_cast<volatile unsigned long long*>(s->host_block + cells);
+  s->hseq = reinterpret_cast<uint32_t*>(s->host_block + 2 * cells);
+  s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + 3 * cells);
+  s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + 3 * cells + errb);
+  for (uint32_t i = 0; i < s->nw; ++i) {
+    s->to_gpu[uint64_t(i) * s->cell_words] = LK_NOP;
+    s->status[uint64_t(i) * s->cell_u64] = uint64_t(LK_NOP) | (uint64_t(LK_PHASE_BOOTING) << 32);
+    s->smid[i] = 0xFFFFFFFFu;
+  }
+
+  // --- device block: desc | masks | ctr | spans | trace | tcnt
+  const size_t descb = al(size_t(cfg.num_slots) * sizeof(lk_desc));
+  const size_t maskb = al(size_t(cfg.num_slots) * s->nwords * 8);
+  const size_t ctrb = al(size_t(cfg.num_slots) * 4);
+  const size_t spanb = al(size_t(s->nw) * 16);
+  const size_t traceb = cfg.record_trace ? al(size_t(s->nw) * cfg.trace_capacity * sizeof(lk_dev_trace)) : 0;
+  const size_t tcntb = al(size_t(s->nw) * 4);
+  const size_t dev_bytes = descb + maskb + ctrb + spanb + traceb + tcntb;
+  ce = dev_alloc(reinterpret_cast<void**>(&s->dev_block), dev_bytes);
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "device alloc: %s", cudaGetErrorString(ce)));
+  ce = cudaMemsetAsync(s->dev_block, 0, dev_bytes, svc_stream());
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(svc_stream());  // zeroed before the kernel reads it
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "memset: %s", cudaGetErrorString(ce)));
+  uint8_t* p = s->dev_block;
+  s->d_desc = reinterpret_cast<lk_desc*>(p); p += descb;
+  s->d_mask = reinterpret_cast<unsigned long long*>(p); p += maskb;
+  s->d_ctr = reinterpret_cast<uint32_t*>(p); p += ctrb;
+  s->d_spans = reinterpret_cast<unsigned long long*>(p); p += spanb;
+  s->d_trace = traceb ? reinterpret_cast<lk_dev_trace*>(p) : nullptr; p += traceb;
+  s->d_tcnt = reinterpret_cast<uint32_t*>(p);
+
+  ce = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "stream: %s", cudaGetErrorString(ce)));
+  ce = cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "stream: %s", cudaGetErrorString(ce)));
+
+  // --- one CTA per SM: dynamic smem above half the SM's capacity
+  s->smem = size_t(prop.sharedMemPerMultiprocessor) / 2 + 8192;
+  if (s->smem > size_t(prop.sharedMemPerBlockOptin) - 1024) s->smem = size_t(prop.sharedMemPerBlockOptin) - 1024;
+  ce = lk_persistent_configure(s->smem);
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "smem attr: %s", cudaGetErrorString(ce)));
+  int bps = 0;
+  ce = lk_persistent_occupancy(s->threads, s->smem, &bps);
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "occupancy: %s", cudaGetErrorString(ce)));
+  if (bps != 1) return cleanup(fail(LK_E_INIT, "expected exactly 1 resident worker per SM, got %d", bps));
+
+  lk_dev_args a;
+  memset(&a, 0, sizeof a);
+  a.to_gpu = s->to_gpu;
+  a.status = const_cast<unsigned long long*>(s->status);
+  a.hseq = s->hseq;
+  a.err = const_cast<unsigned long long*>(s->err);
+  a.smid = const_cast<uint32_t*>(s->smid);
+  a.desc = s->d_desc;
+  a.slot_mask = s->d_mask;
+  a.reduce_ctr = s->d_ctr;
+  a.spans = s->d_spans;
+  a.trace = s->d_trace;
+  a.trace_cnt = s->d_tcnt;
+  a.cell_words = s->cell_words;
+  a.cell_u64 = s->cell_u64;
+  a.num_slots = cfg.num_slots;
+  a.nwords = s->nwords;
+  a.trace_cap = cfg.trace_capacity;
+  a.record_trace = cfg.record_trace ? 1 : 0;
+  a.backoff_ns = cfg.poll_backoff_ns;
+  a.flags = cfg.flags;
+  ce = lk_launch_persistent(a, s->nw, s->threads, s->smem, s->stream);
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(ce)));
+
+  // --- boot: every worker publishes INIT then NOP (native.py:113-118)
+  const uint64_t deadline = now_ns() + cfg.wait_timeout_ns;
+  for (uint32_t i = 0; i < s->nw;) {
+    if (s->word(i) == LK_NOP && s->phase(i) == LK_PHASE_IDLE) { ++i; continue; }
+    if (s->err[i]) return cleanup(fail(LK_E_INIT, "worker %u failed during boot", i));
+    if (now_ns() > deadline) {
+      // the kernel may still run: leak rather than free memory it can touch
+      const int ks = kernel_status(s);
+      if (ks == 0) return fail(LK_E_INIT, "workers failed to reach idle (worker %u)", i);
+      return cleanup(fail(LK_E_INIT, "workers failed to reach idle (worker %u)", i));
+    }
+    LK_PAUSE();
+  }
+  *out = s;
+  if (init_ns) *init_ns = now_ns() - t0;
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ descriptors
+static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* d, const uint64_t* mask, uint32_t nwords);
+
+extern "C" int lk_register_desc(lk_session* s, uint32_t slot, const lk_desc* d, const uint64_t* mask,
+                                uint32_t nwords) {
+  int rc = require_live(s);
+  if (rc) return rc;
+  if (!d) return fail(LK_E_USAGE, "null descriptor");
+  if (slot >= s->cfg.num_slots)
+    return fail(LK_E_USAGE, "slot %u outside the %u-entry descriptor table", slot, s->cfg.num_slots);
+  if (d->kind >= LK_KIND_COUNT) return fail(LK_E_USAGE, "unknown work kind %u", d->kind);
+  std::lock_guard<std::mutex> g(s->mu);
+  if (s->pending_by_slot.count(slot))
+    return fail(LK_E_USAGE, "descriptor slot %u still referenced by an un-waited dispatch", slot);
+  return stage_locked(s, slot, d, mask, nwords);
+}
+
+// ------------------------------------------------------------------ trigger / wait
+static inline bool multi_worker_kind(uint32_t kind) {
+  return kind != LK_KIND_EMPTY && kind != LK_KIND_BUSY_LOOP;
+}
+
+// Stage desc (+ the worker set that shards it) in the slot; a no-op when the
+// device copy is already identical.  Caller holds s->mu.
+static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* d, const uint64_t* mask, uint32_t nwords) {
+  std::vector<uint64_t> m(s->nwords, 0);
+  if (mask && multi_worker_kind(d->kind))
+    for (uint32_t k = 0; k < nwords && k < s->nwords; ++k) m[k] = mask[k];
+  if (s->registered[slot] && memcmp(&s->reg_desc[slot], d, sizeof(lk_desc)) == 0 && s->reg_mask[slot] == m)
+    return LK_OK;
+  LK_CUDA(cudaMemcpyAsync(s->d_desc + slot, d, sizeof(lk_desc), cudaMemcpyHostToDevice, s->copy_stream));
+  LK_CUDA(cudaMemcpyAsync(s->d_mask + uint64_t(slot) * s->nwords, m.data(), 8 * s->nwords,
+                          cudaMemcpyHostToDevice, s->copy_stream));
+  LK_CUDA(cudaStreamSynchronize(s->copy_stream));  // in place before any WORK word names it
+  s->registered[slot] = 1;
+  s->reg_desc[slot] = *d;
+  s->reg_mask[slot] = std::move(m);
+  return LK_OK;
+}
+
+// Checks in the reference's order (native.py:210-220): live, mask, busy
+// workers, slot lock, idle cells; then stage the descriptor (when given) and
+// write the WORK word to every masked worker, ascending.
+static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, uint32_t slot,
+                          const lk_desc* d, std::vector<uint32_t>& ids, uint64_t* elapsed_ns) {
+  int rc = require_live(s);
+  if (rc) return rc;
+  if (!mask_ids(s, mask, nwords, ids, &rc)) return rc;
+  std::vector<uint32_t> busy;
+  for (uint32_t i : ids)
+    if (s->pending[i >> 6] >> (i & 63) & 1) busy.push_back(i);
+  if (!busy.empty()) return fail(LK_E_BUSY, "worker(s) %s still busy", ids_str(busy).c_str());
+  if (s->pending_by_slot.count(slot))
+    return fail(LK_E_USAGE, "descriptor slot %u still referenced by an un-waited dispatch", slot);
+  if (slot >= s->cfg.num_slots)
+    return fail(LK_E_USAGE, "slot %u outside the %u-entry descriptor table", slot, s->cfg.num_slots);
+  for (uint32_t i : ids) {
+    const uint32_t w = s->word(i);
+    if (w != LK_NOP) return fail(LK_E_BUSY, "worker %u not idle (from_gpu=%u)", i, w);
+  }
+  const uint64_t t0 = now_ns();
+  if (d) {
+    if (d->kind >= LK_KIND_COUNT) return fail(LK_E_USAGE, "unknown work kind %u", d->kind);
+    rc = stage_locked(s, slot, d, mask, nwords);
+    if (rc) return rc;
+  } else if (!s->registered[slot]) {
+    return fail(LK_E_USAGE, "descriptor slot %u not registered", slot);
+  }
+  const uint32_t word = LK_WORK_BASE + slot;
+  for (uint32_t i : ids) s->host_write(i, word);
+  const uint64_t t1 = now_ns();
+  std::vector<uint64_t> m(s->nwords, 0);
+  for (uint32_t i : ids) {
+    s->pending[i >> 6] |= 1ull << (i & 63);
+    m[i >> 6] |= 1ull << (i & 63);
+  }
+  s->pending_by_slot[slot] = std::move(m);
+  if (elapsed_ns) *elapsed_ns = t1 - t0;
+  return LK_OK;
+}
+
+extern "C" int lk_trigger(lk_session* s, const uint64_t* mask, uint32_t nwords, uint32_t slot,
+                          const lk_desc* d, uint64_t* elapsed_ns) {
+  if (!s || !mask) return fail(LK_E_USAGE, "null argument");
+  std::lock_guard<std::mutex> g(s->mu);
+  std::vector<uint32_t> ids;
+  return trigger_locked(s, mask, nwords, slot, d, ids, elapsed_ns);
+}
+
+static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::vector<uint32_t>& ids,
+                     uint64_t* finished_ns, uint64_t t_trigger, uint64_t* done_abs) {
+  {
+    std::lock_guard<std::mutex> g(s->mu);
+    int rc = require_live(s);
+    if (rc) return rc;
+    if (!mask_ids(s, mask, nwords, ids, &rc)) return rc;
+    for (uint32_t i : ids)
+      if (!(s->pending[i >> 6] >> (i & 63) & 1)) return fail(LK_E_USAGE, "wait on worker(s) that were never triggered");
+  }
+  const uint64_t t0 = t_trigger ? t_trigger : now_ns();
+  int rc = spin_words(s, ids, LK_FINISHED, "wait for FINISHED");
+  if (rc) return rc;
+  const uint64_t finished_at = now_ns();
+  for (uint32_t i : ids) s->host_write(i, LK_NOP);
+  rc = spin_words(s, ids, LK_NOP, "wait for ack consumption");
+  if (rc) return rc;
+  {
+    std::lock_guard<std::mutex> g(s->mu);
+    std::vector<uint64_t> m(s->nwords, 0);
+    for (uint32_t i : ids) m[i >> 6] |= 1ull << (i & 63);
+    for (uint32_t k = 0; k < s->nwords; ++k) s->pending[k] &= ~m[k];
+    for (auto it = s->pending_by_slot.begin(); it != s->pending_by_slot.end();) {
+      bool any = false;
+      for (uint32_t k = 0; k < s->nwords; ++k) {
+        it->second[k] &= ~m[k];
+        any |= it->second[k] != 0;
+      }
+      if (any) ++it; else it = s->pending_by_slot.erase(it);
+    }
+  }
+  if (finished_ns) *finished_ns = finished_at - t0;
+  if (done_abs) *done_abs = finished_at;
+  return LK_OK;
+}
+
+extern "C" int lk_wait(lk_session* s, const uint64_t* mask, uint32_t nwords, uint64_t* finished_ns) {
+  if (!s || !mask) return fail(LK_E_USAGE, "null argument");
+  std::vector<uint32_t> ids;
+  return wait_impl(s, mask, nwords, ids, finished_ns, 0, nullptr);
+}
+
+extern "C" int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks, uint32_t nwords,
+                                  uint32_t slot, uint64_t rounds, uint64_t* trig_ns, uint64_t* done_ns,
+                                  uint64_t* cycle_ns) {
+  if (!s || !masks || nmasks == 0) return fail(LK_E_USAGE, "null argument");
+  std::vector<uint32_t> ids;
+  ids.reserve(s->nw);
+  for (uint64_t k = 0; k < rounds; ++k) {
+    const uint64_t* m = masks + (k % nmasks) * uint64_t(nwords);
+    const uint64_t t0 = now_ns();
+    uint64_t el = 0;
+    int rc;
+    {
+      std::lock_guard<std::mutex> g(s->mu);
+      rc = trigger_locked(s, m, nwords, slot, nullptr, ids, &el);
+    }
+    if (rc) return rc;
+    uint64_t done_abs = 0;
+    rc = wait_impl(s, m, nwords, ids, nullptr, t0, &done_abs);
+    if (rc) return rc;
+    const uint64_t t2 = now_ns();
+    if (trig_ns) trig_ns[k] = el;
+    if (done_ns) done_ns[k] = done_abs - t0;
+    if (cycle_ns) cycle_ns[k] = t2 - t0;
+  }
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ dispose
+extern "C" int lk_dispose(lk_session* s, uint64_t* elapsed_ns) {
+  if (!s) return fail(LK_E_USAGE, "null session");
+  std::lock_guard<std::mutex> g(s->mu);
+  int rc = require_live(s);
+  if (rc) return rc;
+  std::vector<uint32_t> busy;
+  for (uint32_t i = 0; i < s->nw; ++i)
+    if (s->pending[i >> 6] >> (i & 63) & 1) busy.push_back(i);
+  if (!busy.empty()) return fail(LK_E_DISPOSE_BUSY, "worker(s) %s still working", ids_str(busy).c_str());
+  const uint64_t t0 = now_ns();
+  for (uint32_t i = 0; i < s->nw; ++i) s->host_write(i, LK_EXIT);
+  const uint64_t deadline = t0 + s->cfg.wait_timeout_ns;
+  for (;;) {
+    const int ks = kernel_status(s);
+    if (ks < 0) return LK_E_CUDA;
+    if (ks == 1) break;
+    if (now_ns() > deadline) return fail(LK_E_HANG, "persistent kernel did not exit");
+    usleep(20);
+  }
+  s->disposed = true;
+  if (elapsed_ns) *elapsed_ns = now_ns() - t0;
+  return LK_OK;
+}
+
+// Teardown that ignores the host rules: EXIT to every worker whatever its
+// state (a WORKING worker finishes its item first), then wait for the kernel.
+// Used to reclaim the GPU after a worker died or a caller bailed out.
+extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
+  if (!s) return fail(LK_E_USAGE, "null session");
+  std::lock_guard<std::mutex> g(s->mu);
+  if (s->kernel_done) {
+    s->disposed = true;
+    return LK_OK;
+  }
+  for (uint32_t i = 0; i < s->nw; ++i)
+    __atomic_store_n(s->to_gpu + uint64_t(i) * s->cell_words, LK_EXIT, __ATOMIC_RELEASE);
+  const uint64_t deadline = now_ns() + (timeout_ns ? timeout_ns : s->cfg.wait_timeout_ns);
+  for (;;) {
+    const int ks = kernel_status(s);
+    if (ks != 0) break;
+    if (now_ns() > deadline) return fail(LK_E_HANG, "persistent kernel did not exit after abort");
+    usleep(50);
+  }
+  s->disposed = true;
+  return LK_OK;
+}
+
+extern "C" int lk_destroy(lk_session* s) {
+  if (!s) return LK_OK;
+  if (!s->kernel_done) {
+    if (kernel_status(s) == 0) {
+      // Still resident (never disposed, or hung): the kernel can touch the
+      // mailboxes, so the memory is deliberately leaked.
+      return fail(LK_E_HANG, "persistent kernel still resident; resources leaked");
+    }
+  }
+  cudaFreeHost(s->host_block);
+  dev_free(s->dev_block);
+  cudaStreamDestroy(s->stream);
+  cudaStreamDestroy(s->copy_stream);
+  delete s;
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ introspection
+extern "C" int lk_read_cells(lk_session* s, uint32_t* to_gpu, uint32_t* from_gpu, uint32_t* phase, uint32_t n) {
+  if (!s) return fail(LK_E_USAGE, "null session");
+  const uint32_t m = std::min(n, s->nw);
+  for (uint32_t i = 0; i < m; ++i) {
+    const unsigned long long st = s->status[uint64_t(i) * s->cell_u64];
+    if (to_gpu) to_gpu[i] = __atomic_load_n(s->to_gpu + uint64_t(i) * s->cell_words, __ATOMIC_ACQUIRE);
+    if (from_gpu) from_gpu[i] = uint32_t(st);
+    if (phase) phase[i] = uint32_t(st >> 32);
+  }
+  return LK_OK;
+}
+
+extern "C" int lk_debug_poke(lk_session* s, uint32_t worker, uint32_t word) {
+  if (!s || worker >= s->nw) return fail(LK_E_USAGE, "bad worker");
+  __atomic_store_n(s->to_gpu + uint64_t(worker) * s->cell_words, word, __ATOMIC_RELEASE);
+  return LK_OK;
+}
+
+extern "C" int lk_worker_error(lk_session* s, uint32_t worker, uint32_t* code, uint32_t* word) {
+  if (!s || worker >= s->nw) return fail(LK_E_USAGE, "bad worker");
+  const unsigned long long e = s->err[worker];
+  if (code) *code = uint32_t(e);
+  if (word) *word = uint32_t(e >> 32);
+  return LK_OK;
+}
+
+extern "C" int lk_smid_map(lk_session* s, uint32_t* smid, uint32_t n) {
+  if (!s || !smid) return fail(LK_E_USAGE, "null argument");
+  for (uint32_t i = 0; i < std::min(n, s->nw); ++i) smid[i] = s->smid[i];
+  return LK_OK;
+}
+
+extern "C" int lk_num_workers(lk_session* s, uint32_t* n) {
+  if (!s || !n) return fail(LK_E_USAGE, "null argument");
+  *n = s->nw;
+  return LK_OK;
+}
+
+extern "C" int lk_pending(lk_session* s, uint64_t* mask, uint32_t nwords) {
+  if (!s || !mask) return fail(LK_E_USAGE, "null argument");
+  std::lock_guard<std::mutex> g(s->mu);
+  for (uint32_t k = 0; k < nwords; ++k) mask[k] = k < s->nwords ? s->pending[k] : 0;
+  return LK_OK;
+}
+
+extern "C" int lk_kernel_alive(lk_session* s, uint32_t* alive) {
+  if (!s || !alive) return fail(LK_E_USAGE, "null argument");
+  const int ks = kernel_status(s);
+  *alive = ks == 0 ? 1u : 0u;
+  return LK_OK;
+}
+
+extern "C" int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n) {
+  if (!s) return fail(LK_E_USAGE, "null session");
+  std::vector<unsigned long long> sp(2 * size_t(s->nw));
+  LK_CUDA(cudaMemcpyAsync(sp.data(), s->d_spans, sp.size() * 8, cudaMemcpyDeviceToHost, s->copy_stream));
+  LK_CUDA(cudaStreamSynchronize(s->copy_stream));
+  for (uint32_t i = 0; i < std::min(n, s->nw); ++i) {
+    if (begin_ns) begin_ns[i] = sp[2 * i];
+    if (end_ns) end_ns[i] = sp[2 * i + 1];
+  }
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ tracing
+struct MergedRec {
+  uint64_t anchor;  // host time of the host write this record follows
+  uint32_t worker;
+  uint32_t local;   // position in the worker's merged stream
+  lk_trace_rec r;
+};
+
+static int build_trace(lk_session* s, std::vector<MergedRec>& outv) {
+  if (!s->cfg.record_trace) return fail(LK_E_USAGE, "session was started without record_trace");
+  std::vector<uint32_t> cnt(s->nw);
+  LK_CUDA(cudaMemcpyAsync(cnt.data(), s->d_tcnt, 4 * size_t(s->nw), cudaMemcpyDeviceToHost, s->copy_stream));
+  LK_CUDA(cudaStreamSynchronize(s->copy_stream));
+  for (uint32_t i = 0; i < s->nw; ++i)
+    if (cnt[i] > s->cfg.trace_capacity)
+      return fail(LK_E_TRACE_LOST, "worker %u wrote %u trace records into a %u-record ring", i, cnt[i],
+                  s->cfg.trace_capacity);
+  std::vector<lk_dev_trace> ring(s->cfg.trace_capacity);
+  outv.clear();
+  for (uint32_t i = 0; i < s->nw; ++i) {
+    if (cnt[i]) {
+      LK_CUDA(cudaMemcpyAsync(ring.data(), s->d_trace + uint64_t(i) * s->cfg.trace_capacity,
+                              size_t(cnt[i]) * sizeof(lk_dev_trace), cudaMemcpyDeviceToHost, s->copy_stream));
+      LK_CUDA(cudaStreamSynchronize(s->copy_stream));
+    }
+    const auto& hl = s->host_log[i];
+    size_t h = 0, d = 0;
+    uint32_t local = 0;
+    uint64_t anchor = s->t_create;
+    // device record tagged hseq=k follows host write k and precedes write k+1
+    while (h < hl.size() || d < cnt[i]) {
+      const bool take_dev = d < cnt[i] && (h >= hl.size() || ring[d].hseq < hl[h].hseq);
+      MergedRec m;
+      m.worker = i;
+      m.local = local++;
+      if (take_dev) {
+        m.anchor = anchor;
+        m.r = lk_trace_rec{0, 'D', i, ring[d].word, ring[d].hseq, ring[d].t_ns};
+        ++d;
+      } else {
+        anchor = hl[h].t_ns;
+        m.anchor = anchor;
+        m.r = lk_trace_rec{0, 'H', i, hl[h].word, hl[h].hseq, hl[h].t_ns};
+        ++h;
+      }
+      outv.push_back(m);
+    }
+  }
+  std::stable_sort(outv.begin(), outv.end(), [](const MergedRec& a, const MergedRec& b) {
+    if (a.anchor != b.anchor) return a.anchor < b.anchor;
+    if (a.worker != b.worker) return a.worker < b.worker;
+    return a.local < b.local;
+  });
+  for (size_t k = 0; k < outv.size(); ++k) outv[k].r.step = k;
+  return LK_OK;
+}
+
+extern "C" int lk_trace_count(lk_session* s, uint64_t* n) {
+  if (!s || !n) return fail(LK_E_USAGE, "null argument");
+  std::vector<MergedRec> v;
+  int rc = build_trace(s, v);
+  if (rc) return rc;
+  *n = v.size();
+  return LK_OK;
+}
+
+extern "C" int lk_trace_read(lk_session* s, lk_trace_rec* out, uint64_t cap, uint64_t* n) {
+  if (!s || !n) return fail(LK_E_USAGE, "null argument");
+  std::vector<MergedRec> v;
+  int rc = build_trace(s, v);
+  if (rc) return rc;
+  const uint64_t m = std::min<uint64_t>(cap, v.size());
+  for (uint64_t k = 0; k < m; ++k) out[k] = v[k].r;
+  *n = m;
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ protocol (host build)
+extern "C" int lk_protocol_step(uint32_t* phase, uint32_t* slot, uint32_t observed, uint32_t* publish,
+                                uint32_t* action, uint32_t* werr) {
+  if (!phase || !slot) return fail(LK_E_USAGE, "null argument");
+  lk_wstate st{*phase, *slot};
+  const lk_step_out o = lk_worker_step(st, observed);
+  if (werr) *werr = o.werr;
+  if (o.werr) return LK_E_PROTOCOL;
+  *phase = st.phase;
+  *slot = st.slot;
+  if (publish) *publish = o.publish;
+  if (action) *action = o.action;
+  return LK_OK;
+}
+
+extern "C" int lk_protocol_complete(uint32_t* phase, uint32_t* slot, uint32_t* publish, uint32_t* werr) {
+  if (!phase || !slot) return fail(LK_E_USAGE, "null argument");
+  lk_wstate st{*phase, *slot};
+  const lk_step_out o = lk_complete_work(st);
+  if (werr) *werr = o.werr;
+  if (o.werr) return LK_E_PROTOCOL;
+  *phase = st.phase;
+  *slot = st.slot;
+  if (publish) *publish = o.publish;
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ ping-pong floor
+extern "C" int lk_pingpong(int device, uint64_t rounds, uint64_t* rt_ns) {
+  if (!rt_ns) return fail(LK_E_USAGE, "null argument");
+  LK_CUDA(cudaSetDevice(device));
+  uint32_t* cells = nullptr;
+  LK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cells), 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(cells, 0, 4096);
+  uint32_t* flag = cells;
+  uint32_t* echo = cells + 32;  // separate 128-B line
+  cudaStream_t st;
+  LK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaError_t ce = lk_launch_pingpong(flag, echo, rounds, st);
+  if (ce != cudaSuccess) return fail(LK_E_CUDA, "pingpong launch: %s", cudaGetErrorString(ce));
+  int rc = LK_OK;
+  for (uint64_t r = 1; r <= rounds; ++r) {
+    const uint32_t want = uint32_t(r);
+    const uint64_t t0 = now_ns();
+    __atomic_store_n(flag, want, __ATOMIC_RELEASE);
+    const uint64_t deadline = t0 + 5000000000ull;
+    while (__atomic_load_n(echo, __ATOMIC_ACQUIRE) != want) {
+      LK_PAUSE();
+      if (now_ns() > deadline) { rc = fail(LK_E_HANG, "pingpong stalled at round %llu", (unsigned long long)r); break; }
+    }
+    if (rc) break;
+    rt_ns[r - 1] = now_ns() - t0;
+  }
+  if (rc == LK_OK) {
+    LK_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    cudaFreeHost(cells);
+  }
+  return rc;
+}
+
+// ------------------------------------------------------------------ baseline
+struct lk_baseline {
+  int device;
+  uint32_t threads;
+  cudaStream_t stream;
+  uint32_t* d_ctr;
+  bool in_flight;
+  cudaEvent_t e0, e1;
+};
+
+extern "C" int lk_baseline_create(int device, uint32_t threads, lk_baseline** out) {
+  if (!out) return fail(LK_E_USAGE, "null argument");
+  if (threads == 0) threads = 512;
+  if (threads % 32 || threads > 1024) return fail(LK_E_CONFIG, "threads must be a multiple of 32 <= 1024");
+  LK_CUDA(cudaSetDevice(device));
+  auto* b = new lk_baseline();
+  b->device = device;
+  b->threads = threads;
+  b->in_flight = false;
+  LK_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  LK_CUDA(dev_alloc(reinterpret_cast<void**>(&b->d_ctr), 4));
+  LK_CUDA(cudaMemsetAsync(b->d_ctr, 0, 4, svc_stream()));
+  LK_CUDA(cudaStreamSynchronize(svc_stream()));
+  LK_CUDA(cudaEventCreate(&b->e0));
+  LK_CUDA(cudaEventCreate(&b->e1));
+  *out = b;
+  return LK_OK;
+}
+
+extern "C" int lk_baseline_launch(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t* launch_ns) {
+  if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
+  if (b->in_flight) return fail(LK_E_USAGE, "previous task not yet joined");
+  const uint64_t t0 = now_ns();
+  cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream);
+  const uint64_t t1 = now_ns();
+  if (ce != cudaSuccess) return fail(LK_E_CUDA, "launch: %s", cudaGetErrorString(ce));
+  b->in_flight = true;
+  if (launch_ns) *launch_ns = t1 - t0;
+  return LK_OK;
+}
+
+extern "C" int lk_baseline_wait(lk_baseline* b, uint64_t* wait_ns) {
+  if (!b) return fail(LK_E_USAGE, "null argument");
+  if (!b->in_flight) return fail(LK_E_USAGE, "no task in flight");
+  const uint64_t t0 = now_ns();
+  LK_CUDA(cudaStreamSynchronize(b->stream));
+  b->in_flight = false;
+  if (wait_ns) *wait_ns = now_ns() - t0;
+  return LK_OK;
+}
+
+extern "C" int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t rounds,
+                                 uint64_t* launch_ns, uint64_t* total_ns) {
+  if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
+  for (uint64_t k = 0; k < rounds; ++k) {
+    const uint64_t t0 = now_ns();
+    cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream);
+    const uint64_t t1 = now_ns();
+    if (ce != cudaSuccess) return fail(LK_E_CUDA, "launch: %s", cudaGetErrorString(ce));
+    LK_CUDA(cudaStreamSynchronize(b->stream));
+    const uint64_t t2 = now_ns();
+    if (launch_ns) launch_ns[k] = t1 - t0;
+    if (total_ns) total_ns[k] = t2 - t0;
+  }
+  return LK_OK;
+}
+
+extern "C" int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_t grid, uint32_t reps,
+                                       float* avg_ms) {
+  if (!b || !d || !avg_ms || reps == 0) return fail(LK_E_USAGE, "bad argument");
+  LK_CUDA(cudaEventRecord(b->e0, b->stream));
+  for (uint32_t k = 0; k < reps; ++k) {
+    cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream);
+    if (ce != cudaSuccess) return fail(LK_E_CUDA, "launch: %s", cudaGetErrorString(ce));
+  }
+  LK_CUDA(cudaEventRecord(b->e1, b->stream));
+  LK_CUDA(cudaEventSynchronize(b->e1));
+  float ms = 0.f;
+  LK_CUDA(cudaEventElapsedTime(&ms, b->e0, b->e1));
+  *avg_ms = ms / float(reps);
+  return LK_OK;
+}
+
+extern "C" int lk_baseline_destroy(lk_baseline* b) {
+  if (!b) return LK_OK;
+  cudaStreamSynchronize(b->stream);
+  cudaStreamDestroy(b->stream);
+  dev_free(b->d_ctr);
+  cudaEventDestroy(b->e0);
+  cudaEventDestroy(b->e1);
+  delete b;
+  return LK_OK;
+}
+
+// ------------------------------------------------------------------ helpers
+extern "C" int lk_pin_thread_near(int device, uint32_t* ncores) {
+  char bdf[64] = {0};
+  LK_CUDA(cudaDeviceGetPCIBusId(bdf, sizeof bdf, device));
+  for (char* c = bdf; *c; ++c) *c = char(tolower(*c));
+  char path[160];
+  snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/local_cpulist", bdf);
+  FILE* f = fopen(path, "r");
+  if (!f) return fail(LK_E_USAGE, "cannot read %s", path);
+  char line[4096] = {0};
+  if (!fgets(line, sizeof line, f)) line[0] = 0;
+  fclose(f);
+  cpu_set_t allowed, want;
+  CPU_ZERO(&want);
+  if (sched_getaffinity(0, sizeof allowed, &allowed) != 0) return fail(LK_E_USAGE, "sched_getaffinity failed");
+  uint32_t n = 0;
+  for (char* tok = strtok(line, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+    int a = 0, b = 0;
+    if (sscanf(tok, "%d-%d", &a, &b) == 2) {
+    } else if (sscanf(tok, "%d", &a) == 1) {
+      b = a;
+    } else {
+      continue;
+    }
+    for (int c = a; c <= b && c < CPU_SETSIZE; ++c)
+      if (CPU_ISSET(c, &allowed)) { CPU_SET(c, &want); ++n; }
+  }
+  if (n == 0) return fail(LK_E_USAGE, "no allowed cores local to device %d (%s)", device, path);
+  if (pthread_setaffinity_np(pthread_self(), sizeof want, &want) != 0)
+    return fail(LK_E_USAGE, "pthread_setaffinity_np failed: %s", strerror(errno));
+  if (ncores) *ncores = n;
+  return LK_OK;
+}
+
+extern "C" int lk_device_count(int* n) {
+  if (!n) return fail(LK_E_USAGE, "null argument");
+  LK_CUDA(cudaGetDeviceCount(n));
+  return LK_OK;
+}
+
+extern "C" int lk_sm_count(int device, int* n) {
+  if (!n) return fail(LK_E_USAGE, "null argument");
+  LK_CUDA(cudaDeviceGetAttribute(n, cudaDevAttrMultiProcessorCount, device));
+  return LK_OK;
+}
+
+extern "C" int lk_dev_alloc(int device, uint64_t bytes, uint64_t* ptr) {
+  if (!ptr) return fail(LK_E_USAGE, "null argument");
+  LK_CUDA(cudaSetDevice(device));
+  void* p = nullptr;
+  LK_CUDA(dev_alloc(&p, bytes));
+  *ptr = reinterpret_cast<uint64_t>(p);
+  return LK_OK;
+}
+
+extern "C" int lk_dev_free(uint64_t ptr) {
+  LK_CUDA(dev_free(reinterpret_cast<void*>(ptr)));
+  return LK_OK;
+}
+
+extern "C" int lk_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes) {
+  cudaStream_t st = svc_stream();
+  LK_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice, st));
+  LK_CUDA(cudaStreamSynchronize(st));
+  return LK_OK;
+}
+
+extern "C" int lk_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes) {
+  cudaStream_t st = svc_stream();
+  LK_CUDA(cudaMemcpyAsync(dst, reinterpret_cast<const void*>(src), bytes, cudaMemcpyDeviceToHost, st));
+  LK_CUDA(cudaStreamSynchronize(st));
+  return LK_OK;
+}
+
+extern "C" const char* lk_strerror(int code) {
+  switch (code) {
+    case LK_OK: return "ok";
+    case LK_E_USAGE: return "usage error";
+    case LK_E_BUSY: return "worker busy";
+    case LK_E_DISPOSE_BUSY: return "dispose while busy";
+    case LK_E_HANG: return "hang detected";
+    case LK_E_INIT: return "init failed";
+    case LK_E_WORKER_DIED: return "worker died";
+    case LK_E_CUDA: return "CUDA error";
+    case LK_E_CONFIG: return "configuration error";
+    case LK_E_PROTOCOL: return "protocol violation";
+    case LK_E_TRACE_LOST: return "trace ring overflow";
+    default: return "unknown error";
+  }
+}
+
+extern "C" const char* lk_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" uint32_t lk_abi_version(void) { return 1u; }

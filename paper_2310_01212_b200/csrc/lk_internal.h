@@ -1,0 +1,48 @@
+// lk_internal.h -- structures shared by the host runtime (lk_host.cu) and the
+// sm_100a kernels (lk_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <stdint.h>
+#include <cuda_runtime.h>
+#include "../../include/lk.h"
+
+// One device trace record (16 B): a value-changing from_gpu write.
+struct lk_dev_trace {
+  uint32_t word;
+  uint32_t hseq;   // host write index (per worker) last observed by the worker
+  uint64_t t_ns;   // %globaltimer
+};
+
+// Kernel arguments of the persistent kernel.  Mailbox cells live in pinned
+// mapped host memory (to_gpu, status, hseq, err, smid); everything else is
+// device-resident.
+struct lk_dev_args {
+  const uint32_t* to_gpu;          // host-mapped, cell i at to_gpu[i*cell_words]
+  unsigned long long* status;      // host-mapped, cell i at status[i*cell_u64]: word | phase<<32
+  const uint32_t* hseq;            // host-mapped, same stride as to_gpu (trace mode)
+  unsigned long long* err;         // host-mapped, err[i] = code | word<<32
+  uint32_t* smid;                  // host-mapped, smid[i]
+  const lk_desc* desc;             // device, num_slots entries
+  const unsigned long long* slot_mask;  // device, num_slots * nwords
+  uint32_t* reduce_ctr;            // device, num_slots
+  unsigned long long* spans;       // device, 2 per worker: begin, end (globaltimer)
+  lk_dev_trace* trace;             // device, num_workers * trace_cap
+  uint32_t* trace_cnt;             // device, num_workers
+  uint32_t cell_words;             // to_gpu / hseq stride in u32
+  uint32_t cell_u64;               // status stride in u64
+  uint32_t num_slots;
+  uint32_t nwords;
+  uint32_t trace_cap;
+  uint32_t record_trace;
+  uint32_t backoff_ns;
+  uint32_t flags;                  // LK_CF_*
+};
+
+// Launch wrappers (lk_kernels.cu).
+cudaError_t lk_launch_persistent(const lk_dev_args& a, uint32_t grid, uint32_t threads,
+                                 size_t smem, cudaStream_t st);
+cudaError_t lk_persistent_configure(size_t smem);
+cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_per_sm);
+cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads,
+                           uint32_t* reduce_ctr, cudaStream_t st);
+cudaError_t lk_launch_pingpong(volatile uint32_t* flag, volatile uint32_t* echo,
+                               uint64_t rounds, cudaStream_t st);

@@ -1,0 +1,434 @@
+// lk_kernels.cu -- the sm_100a device side of the LK runtime.
+//
+//  * lk_persistent_kernel: one CTA per SM for the whole session (the paper's
+//    persistent worker; reference loop native.py:149-199).
+//    Thread 0 of each CTA is the elected poller: it spins on its to_gpu cell
+//    in pinned host memory (ld.*.sys over PCIe), runs the shared state machine
+//    (lk_protocol.cuh) and publishes its from_gpu/status cell with sys-scope
+//    stores.  The other threads park on a CTA barrier (no issue slots used)
+//    and only wake for payload work items.
+//  * lk_work_kernel: the same work functions as an ordinary kernel, for the
+//    cudaLaunchKernel+cudaStreamSynchronize baseline (ThreadSpawnBaseline
+//    analogue, native.py:304-331).
+//  * lk_pingpong_kernel: the raw host<->GPU round-trip floor.
+//
+// Work items are HBM-streaming element-wise maps / reductions: no tensor
+// cores.  Payload loads use ld.global.cg (L2-coherent, no L1 allocation) since
+// the persistent kernel re-reads buffers that DMA or other SMs rewrote between
+// dispatches; 128-bit vectors, U independent loads per thread before use.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "lk_internal.h"
+#include "lk_protocol.cuh"
+
+namespace {
+
+constexpr uint32_t kMaxThreads = 1024;
+constexpr uint32_t kCmdWork = 1;
+constexpr uint32_t kCmdExit = 2;
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+__device__ __forceinline__ uint4 ld_cg4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_cg1(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_cg64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4(uint4* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
+// ---------------------------------------------------------------- work items
+// Shard [0, n) over `count` workers in 128-B (32-element) aligned chunks.
+struct Part { uint64_t b, e; };
+__device__ __forceinline__ Part partition(uint64_t n, uint32_t rank, uint32_t count) {
+  uint64_t chunk = (n + count - 1) / count;
+  chunk = (chunk + 31) & ~uint64_t(31);
+  uint64_t b = min(n, uint64_t(rank) * chunk);
+  return Part{b, min(n, b + chunk)};
+}
+
+struct OpAddI32 {  // int32 add with two's-complement wraparound
+  __device__ __forceinline__ uint32_t s(uint32_t x, uint32_t y) const { return x + y; }
+};
+struct OpSaxpy {   // numpy float32: fl(fl(alpha*x) + y), no FMA contraction
+  float alpha;
+  __device__ __forceinline__ uint32_t s(uint32_t x, uint32_t y) const {
+    return __float_as_uint(__fadd_rn(__fmul_rn(alpha, __uint_as_float(x)), __uint_as_float(y)));
+  }
+};
+struct OpCopy {
+  __device__ __forceinline__ uint32_t s(uint32_t x, uint32_t) const { return x; }
+};
+
+template <class Op>
+__device__ __forceinline__ uint4 vop(const Op& op, uint4 x, uint4 y) {
+  return make_uint4(op.s(x.x, y.x), op.s(x.y, y.y), op.s(x.z, y.z), op.s(x.w, y.w));
+}
+
+// out[i] = op(in0[i], in1[i]) over [p.b, p.e), all threads of the CTA.
+template <int U, bool kTwo, class Op>
+__device__ __forceinline__ void map_chunk(const lk_desc& d, Part p, const Op& op) {
+  const uint32_t T = blockDim.x, t = threadIdx.x;
+  const uint32_t* a = reinterpret_cast<const uint32_t*>(d.in0);
+  const uint32_t* c = reinterpret_cast<const uint32_t*>(d.in1);
+  uint32_t* o = reinterpret_cast<uint32_t*>(d.out);
+  if (d.flags & LK_DF_SCALAR) {
+    for (uint64_t i = p.b + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
+    return;
+  }
+  const uint4* a4 = reinterpret_cast<const uint4*>(a);
+  const uint4* c4 = reinterpret_cast<const uint4*>(c);
+  uint4* o4 = reinterpret_cast<uint4*>(o);
+  const uint64_t vb = p.b >> 2, ve = p.e >> 2;
+  uint64_t v = vb + t;
+  for (; v + uint64_t(U - 1) * T < ve; v += uint64_t(U) * T) {
+    uint4 x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x[u] = ld_cg4(a4 + v + u * T);
+      if (kTwo) y[u] = ld_cg4(c4 + v + u * T);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) st4(o4 + v + u * T, vop(op, x[u], kTwo ? y[u] : x[u]));
+  }
+  for (; v < ve; v += T) st4(o4 + v, vop(op, ld_cg4(a4 + v), kTwo ? ld_cg4(c4 + v) : make_uint4(0, 0, 0, 0)));
+  for (uint64_t i = (ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct ReduceSmem {
+  float part[kMaxThreads / 32];
+  uint32_t last;
+};
+
+// out[rank] = fp32 sum of the chunk (per-thread sequential, then a fixed
+// shuffle tree); the last worker to finish sums the partials in rank order in
+// fp64 into *(double*)aux.
+template <int U>
+__device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t rank, uint32_t count,
+                                             uint32_t* ctr, ReduceSmem& sm) {
+  const uint32_t T = blockDim.x, t = threadIdx.x;
+  const float* x = reinterpret_cast<const float*>(d.in0);
+  float acc = 0.f;
+  if (d.flags & LK_DF_SCALAR) {
+    for (uint64_t i = p.b + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
+  } else {
+    const uint4* x4 = reinterpret_cast<const uint4*>(x);
+    const uint64_t vb = p.b >> 2, ve = p.e >> 2;
+    uint64_t v = vb + t;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (; v + uint64_t(U - 1) * T < ve; v += uint64_t(U) * T) {
+      uint4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) r[u] = ld_cg4(x4 + v + u * T);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        s.x += __uint_as_float(r[u].x); s.y += __uint_as_float(r[u].y);
+        s.z += __uint_as_float(r[u].z); s.w += __uint_as_float(r[u].w);
+      }
+    }
+    for (; v < ve; v += T) {
+      uint4 r = ld_cg4(x4 + v);
+      s.x += __uint_as_float(r.x); s.y += __uint_as_float(r.y);
+      s.z += __uint_as_float(r.z); s.w += __uint_as_float(r.w);
+    }
+    acc = (s.x + s.y) + (s.z + s.w);
+    for (uint64_t i = (ve << 2) + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
+  }
+  acc = warp_sum(acc);
+  const uint32_t warp = t >> 5, lane = t & 31, nwarps = (T + 31) >> 5;
+  if (lane == 0) sm.part[warp] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    float v = lane < nwarps ? sm.part[lane] : 0.f;
+    v = warp_sum(v);
+    if (lane == 0) {
+      reinterpret_cast<float*>(d.out)[rank] = v;
+      uint32_t last = 0;
+      if (d.aux) {
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == count - 1;
+      }
+      sm.last = last;
+    }
+  }
+  __syncthreads();
+  if (sm.last && warp == 0) {
+    __threadfence();
+    const uint32_t* partials = reinterpret_cast<const uint32_t*>(d.out);
+    double tot = 0.0;
+    for (uint32_t r = lane; r < count; r += 32) tot += double(__uint_as_float(ld_cg1(partials + r)));
+    tot = warp_sum(tot);
+    if (lane == 0) {
+      *reinterpret_cast<double*>(d.aux) = tot;
+      *ctr = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ void busy_loop(uint64_t iterations) {
+  for (uint64_t i = 0; i < iterations; ++i) asm volatile("" : "+l"(i));
+}
+
+__device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
+  return kind == LK_KIND_EMPTY || kind == LK_KIND_BUSY_LOOP;
+}
+
+// Payload work shared by both kernels; every thread of the CTA calls it.
+__device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
+                                          uint32_t* ctr, ReduceSmem& rs) {
+  const Part p = partition(d.n, rank, count);
+  switch (d.kind) {
+    case LK_KIND_VECTOR_ADD_I32: map_chunk<4, true>(d, p, OpAddI32{}); break;
+    case LK_KIND_SAXPY_F32: map_chunk<4, true>(d, p, OpSaxpy{d.alpha}); break;
+    case LK_KIND_HBM_STREAM: {
+      const uint64_t passes = d.iterations ? d.iterations : 1;
+      for (uint64_t k = 0; k < passes; ++k) map_chunk<8, false>(d, p, OpCopy{});
+      break;
+    }
+    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs); break;
+    default: break;
+  }
+}
+
+// ---------------------------------------------------------------- persistent
+struct Elected {           // thread 0's private protocol state
+  lk_wstate st;
+  uint32_t pub;            // word currently in our from_gpu cell
+  uint32_t hseq_seen;
+  uint32_t tcnt;
+  uint32_t settled;
+  bool settled_valid;
+};
+
+__device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t word,
+                                        bool release) {
+  if (a.record_trace && word != e.pub) {
+    lk_dev_trace* r = a.trace + uint64_t(wid) * a.trace_cap + (e.tcnt % a.trace_cap);
+    r->word = word;
+    r->hseq = e.hseq_seen;
+    r->t_ns = globaltimer();
+    ++e.tcnt;
+    a.trace_cnt[wid] = e.tcnt;
+    __threadfence();
+  }
+  const unsigned long long v = uint64_t(word) | (uint64_t(e.st.phase) << 32);
+  unsigned long long* cell = a.status + uint64_t(wid) * a.cell_u64;
+  if (release) st_release_sys(cell, v); else st_relaxed_sys(cell, v);
+  e.pub = word;
+}
+
+__device__ __forceinline__ void report_error(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t werr,
+                                             uint32_t word) {
+  st_relaxed_sys(a.err + wid, uint64_t(werr) | (uint64_t(word) << 32));
+  e.st.phase = LK_PHASE_EXITED;
+  publish(a, wid, e, e.pub, true);
+}
+
+// Spin on to_gpu[wid] until the state machine begins work or exits.
+__device__ __noinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  const uint32_t* cell = a.to_gpu + uint64_t(wid) * a.cell_words;
+  const bool acquire = (a.flags & LK_CF_ACQUIRE_POLL) || a.record_trace;
+  for (;;) {
+    const uint32_t w = acquire ? ld_acquire_sys(cell) : ld_relaxed_sys(cell);
+    if (e.settled_valid && w == e.settled) {
+      if (a.backoff_ns) __nanosleep(a.backoff_ns);
+      continue;
+    }
+    if (a.record_trace) e.hseq_seen = ld_relaxed_sys(a.hseq + uint64_t(wid) * a.cell_words);
+    const uint32_t before = e.st.phase;
+    const lk_step_out o = lk_worker_step(e.st, w);
+    if (o.werr) {
+      report_error(a, wid, e, o.werr, w);
+      return LK_ACT_EXIT;
+    }
+    bool progressed = e.st.phase != before;
+    if (o.publish != LK_NO_PUBLISH && o.publish != e.pub) {
+      publish(a, wid, e, o.publish, false);
+      progressed = true;
+    } else if (e.st.phase != before) {
+      publish(a, wid, e, e.pub, false);  // phase-only update (EXIT): word unchanged
+    }
+    if (o.action != LK_ACT_NONE) {
+      e.settled_valid = false;
+      return o.action;
+    }
+    e.settled_valid = !progressed;
+    e.settled = w;
+  }
+}
+
+struct PersistSmem {
+  lk_desc desc;
+  uint32_t cmd, rank, count, slot;
+  ReduceSmem red;
+};
+
+__global__ void __launch_bounds__(kMaxThreads, 1) lk_persistent_kernel(const lk_dev_args a) {
+  __shared__ PersistSmem sm;
+  const uint32_t wid = blockIdx.x;
+  Elected e;
+  e.st = lk_wstate{LK_PHASE_BOOTING, 0};
+  e.pub = LK_NOP;  // cells start at the NOP sentinel (protocol.py:217-218)
+  e.hseq_seen = 0;
+  e.tcnt = 0;
+  e.settled = 0;
+  e.settled_valid = false;
+  uint64_t t_begin = 0;
+  if (threadIdx.x == 0) st_relaxed_sys_u32(a.smid + wid, smid());
+
+  for (;;) {
+    if (threadIdx.x == 0) {
+      for (;;) {
+        const uint32_t act = poll(a, wid, e);
+        if (act == LK_ACT_EXIT) { sm.cmd = kCmdExit; break; }
+        t_begin = globaltimer();
+        const uint32_t slot = e.st.slot;
+        if (slot >= a.num_slots) { report_error(a, wid, e, LK_WERR_BAD_SLOT, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
+        lk_desc d;
+        {
+          const uint4* src = reinterpret_cast<const uint4*>(a.desc + slot);
+          uint4* dst = reinterpret_cast<uint4*>(&d);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dst[k] = ld_cg4(src + k);
+        }
+        if (d.kind >= LK_KIND_COUNT) { report_error(a, wid, e, LK_WERR_BAD_KIND, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
+        if (single_thread_kind(d.kind)) {
+          if (d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
+          a.spans[2 * wid] = t_begin;
+          a.spans[2 * wid + 1] = globaltimer();
+          const lk_step_out o = lk_complete_work(e.st);
+          publish(a, wid, e, o.publish, (a.flags & LK_CF_FENCE_ALWAYS) != 0);
+          continue;
+        }
+        // payload item: rank/count from the slot's trigger mask
+        const unsigned long long* m = a.slot_mask + uint64_t(slot) * a.nwords;
+        uint32_t count = 0, rank = 0;
+        const uint32_t mw = wid >> 6;
+        for (uint32_t k = 0; k < a.nwords; ++k) {
+          const unsigned long long bits = ld_cg64(m + k);
+          count += __popcll(bits);
+          if (k < mw) rank += __popcll(bits);
+          else if (k == mw) rank += __popcll(bits & ((1ull << (wid & 63)) - 1ull));
+        }
+        sm.desc = d;
+        sm.rank = rank;
+        sm.count = count ? count : 1;
+        sm.slot = slot;
+        sm.cmd = kCmdWork;
+        break;
+      }
+    }
+    __syncthreads();
+    if (sm.cmd == kCmdExit) return;
+    const lk_desc d = sm.desc;
+    run_multi(d, sm.rank, sm.count, a.reduce_ctr + sm.slot, sm.red);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.spans[2 * wid] = t_begin;
+      a.spans[2 * wid + 1] = globaltimer();
+      const lk_step_out o = lk_complete_work(e.st);
+      publish(a, wid, e, o.publish, true);  // payload visible before FINISHED
+    }
+  }
+}
+
+// ---------------------------------------------------------------- baseline
+__global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, uint32_t* ctr) {
+  __shared__ ReduceSmem rs;
+  if (single_thread_kind(d.kind)) {
+    if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
+    return;
+  }
+  run_multi(d, blockIdx.x, gridDim.x, ctr, rs);
+}
+
+// ---------------------------------------------------------------- ping-pong
+__global__ void lk_pingpong_kernel(volatile uint32_t* flag, volatile uint32_t* echo, uint64_t rounds) {
+  for (uint64_t r = 1; r <= rounds; ++r) {
+    const uint32_t want = uint32_t(r);
+    while (ld_relaxed_sys(const_cast<const uint32_t*>(flag)) != want) {
+    }
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(echo), "r"(want) : "memory");
+  }
+}
+
+}  // namespace
+
+cudaError_t lk_persistent_configure(size_t smem) {
+  return cudaFuncSetAttribute(lk_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+}
+
+cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, lk_persistent_kernel, int(threads), smem);
+}
+
+cudaError_t lk_launch_persistent(const lk_dev_args& a, uint32_t grid, uint32_t threads, size_t smem,
+                                 cudaStream_t st) {
+  void* args[] = {const_cast<lk_dev_args*>(&a)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lk_persistent_kernel), dim3(grid),
+                                     dim3(threads), args, smem, st);
+}
+
+cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads, uint32_t* reduce_ctr,
+                           cudaStream_t st) {
+  lk_work_kernel<<<grid, threads, 0, st>>>(d, reduce_ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t lk_launch_pingpong(volatile uint32_t* flag, volatile uint32_t* echo, uint64_t rounds,
+                               cudaStream_t st) {
+  lk_pingpong_kernel<<<1, 1, 0, st>>>(flag, echo, rounds);
+  return cudaGetLastError();
+}

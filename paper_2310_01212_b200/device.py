@@ -1,0 +1,195 @@
+"""Work descriptors and device payload buffers.
+
+``WorkDescriptor`` keeps the reference's constructor
+(/root/reference/pkg/src/persistkern/device.py:48-66: slot, iterations, kind,
+data_in_ref, data_out_ref) and adds the payload kinds the B200 worker
+executes.  The reference's only kind is ``busy_loop``; its native worker
+ignores ``kind`` and the data refs (native.py:179-181).  Here the kind picks
+a device work function and the refs are device buffers:
+
+=================== ============================= ===========================
+kind                data_in_ref                   data_out_ref
+=================== ============================= ===========================
+empty               --                            --
+busy_loop           --                            --
+vector_add_i32      (a, b) int32                  out int32 (may alias a/b)
+saxpy_f32           (x, y) float32                out float32 (y for in-place)
+block_reduce_f32    x float32                     partials float32[count];
+                                                  ``total_ref`` float64[1]
+hbm_stream          src (any, 4-B elements)       dst
+=================== ============================= ===========================
+
+A buffer is a torch CUDA tensor, a :class:`DeviceBuffer`, or a raw device
+address (int).  ``n`` defaults to the element count of the first input.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, UnsupportedWorkloadError, UsageError
+
+EMPTY = "empty"
+BUSY_LOOP = "busy_loop"
+VECTOR_ADD_I32 = "vector_add_i32"
+SAXPY_F32 = "saxpy_f32"
+BLOCK_REDUCE_F32 = "block_reduce_f32"
+HBM_STREAM = "hbm_stream"
+KINDS = tuple(_lib.KIND_IDS)
+SINGLE_THREAD_KINDS = (EMPTY, BUSY_LOOP)
+
+# algorithmic HBM bytes per element
+BYTES_PER_ELEMENT = {VECTOR_ADD_I32: 12, SAXPY_F32: 12, BLOCK_REDUCE_F32: 4, HBM_STREAM: 8}
+
+
+class DeviceBuffer:
+    """A cudaMalloc'd payload buffer owned by the runtime (no torch needed)."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        lib = _lib.load()
+        ptr = C.c_uint64()
+        _lib.check(lib.lk_dev_alloc(device, nbytes, C.byref(ptr)))
+        self.ptr = ptr.value
+        self.nbytes = nbytes
+        self.device = device
+
+    @classmethod
+    def from_array(cls, arr: np.ndarray, device: int = 0) -> "DeviceBuffer":
+        buf = cls(arr.nbytes, device)
+        buf.upload(arr)
+        return buf
+
+    def upload(self, arr: np.ndarray) -> None:
+        a = np.ascontiguousarray(arr)
+        if a.nbytes > self.nbytes:
+            raise UsageError("array larger than the device buffer")
+        _lib.check(_lib.load().lk_memcpy_h2d(self.ptr, a.ctypes.data, a.nbytes))
+
+    def download(self, dtype, count: Optional[int] = None) -> np.ndarray:
+        dt = np.dtype(dtype)
+        count = self.nbytes // dt.itemsize if count is None else count
+        out = np.empty(count, dtype=dt)
+        _lib.check(_lib.load().lk_memcpy_d2h(out.ctypes.data, self.ptr, out.nbytes))
+        return out
+
+    def free(self) -> None:
+        if self.ptr:
+            _lib.load().lk_dev_free(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _addr(ref) -> int:
+    if ref is None:
+        return 0
+    if isinstance(ref, int):
+        return ref
+    if isinstance(ref, DeviceBuffer):
+        return ref.ptr
+    if hasattr(ref, "data_ptr"):
+        if hasattr(ref, "is_cuda") and not ref.is_cuda:
+            raise UsageError("payload tensors must live on the GPU")
+        return int(ref.data_ptr())
+    cai = getattr(ref, "__cuda_array_interface__", None)
+    if cai is not None:
+        return int(cai["data"][0])
+    raise UsageError(f"cannot take a device address of {type(ref).__name__}")
+
+
+def _numel(ref) -> Optional[int]:
+    if isinstance(ref, DeviceBuffer):
+        return ref.nbytes // 4
+    if hasattr(ref, "numel"):
+        return int(ref.numel())
+    return None
+
+
+def _dtype_name(ref) -> Optional[str]:
+    dt = getattr(ref, "dtype", None)
+    return None if dt is None else str(dt).replace("torch.", "")
+
+
+@dataclass(frozen=True)
+class WorkDescriptor:
+    """One offloadable unit: what the worker runs when ``16+slot`` lands."""
+
+    slot: int
+    iterations: int = 0
+    kind: str = BUSY_LOOP
+    data_in_ref: Optional[object] = field(default=None, compare=False)
+    data_out_ref: Optional[object] = field(default=None, compare=False)
+    alpha: float = 1.0
+    n: Optional[int] = None
+    total_ref: Optional[object] = field(default=None, compare=False)
+
+    def __post_init__(self) -> None:
+        if self.slot < 0:
+            raise ConfigError(f"slot must be nonnegative, got {self.slot}")
+        if self.iterations < 0:
+            raise ConfigError(f"iterations must be nonnegative, got {self.iterations}")
+        if self.kind not in _lib.KIND_IDS:
+            raise UnsupportedWorkloadError(f"unknown workload kind {self.kind!r}")
+        if self.kind in SINGLE_THREAD_KINDS and (self.data_in_ref is not None
+                                                 or self.data_out_ref is not None):
+            raise ConfigError(f"{self.kind} work must not carry data references")
+        if self.kind not in SINGLE_THREAD_KINDS and (self.data_in_ref is None
+                                                     or self.data_out_ref is None):
+            raise ConfigError(f"{self.kind} work needs data_in_ref and data_out_ref")
+
+    @property
+    def multi_worker(self) -> bool:
+        """True when the masked workers shard a payload (the trigger mask matters)."""
+        return self.kind not in SINGLE_THREAD_KINDS
+
+    def inputs(self) -> tuple:
+        ins = self.data_in_ref
+        return tuple(ins) if isinstance(ins, (tuple, list)) else (ins,)
+
+    def elements(self) -> int:
+        if self.n is not None:
+            return int(self.n)
+        if not self.multi_worker:
+            return 0
+        counts = [c for c in (_numel(r) for r in self.inputs()) if c is not None]
+        if not counts:
+            raise ConfigError(f"{self.kind}: pass n= for raw device addresses")
+        return min(counts)
+
+    def payload_bytes(self) -> int:
+        return BYTES_PER_ELEMENT.get(self.kind, 0) * self.elements() * max(1, self.iterations
+                                                                           if self.kind == HBM_STREAM else 1)
+
+    def to_c(self) -> "_lib.lk_desc":
+        d = _lib.lk_desc()
+        d.kind = _lib.KIND_IDS[self.kind]
+        d.iterations = self.iterations
+        d.alpha = float(self.alpha)
+        if not self.multi_worker:
+            return d
+        ins = self.inputs()
+        want = {VECTOR_ADD_I32: ("int32", 2), SAXPY_F32: ("float32", 2),
+                BLOCK_REDUCE_F32: ("float32", 1), HBM_STREAM: (None, 1)}[self.kind]
+        if len(ins) != want[1]:
+            raise ConfigError(f"{self.kind} takes {want[1]} input buffer(s), got {len(ins)}")
+        for r in ins + (self.data_out_ref,):
+            dn = _dtype_name(r)
+            if want[0] and dn is not None and dn != want[0]:
+                raise ConfigError(f"{self.kind} expects {want[0]} buffers, got {dn}")
+        d.n = self.elements()
+        d.in0 = _addr(ins[0])
+        d.in1 = _addr(ins[1]) if len(ins) > 1 else 0
+        d.out = _addr(self.data_out_ref)
+        if self.kind == BLOCK_REDUCE_F32:
+            d.aux = _addr(self.total_ref)
+        if any(p % 16 for p in (d.in0, d.in1, d.out)):
+            d.flags |= _lib.DF_SCALAR
+        return d

@@ -1,0 +1,82 @@
+"""Phase timings and worker-mask helpers shared by the session classes.
+
+Mirror of the helper half of persistkern.host
+(/root/reference/pkg/src/persistkern/host.py:28-99).  On this runtime every
+``cycles`` value is nanoseconds of host wall clock (as on the reference's
+native backend, host.py:44).  Masks are Python ints, bit i = worker i; on
+B200 a full mask is 148 bits wide and crosses the C ABI as little-endian
+u64 words.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, Optional
+
+from .errors import UsageError
+
+PHASE_INIT = "Init"
+PHASE_ALLOC = "Alloc"
+PHASE_COPYIN = "Copyin"
+PHASE_TRIGGER = "Trigger"
+PHASE_LAUNCH = "Launch"
+PHASE_WAIT = "Wait"
+PHASE_COPYOUT = "Copyout"
+PHASE_DISPOSE = "Dispose"
+
+MODEL_LK = "LK"
+MODEL_BASELINE = "BASE"
+
+_MASKED_PHASES = (PHASE_TRIGGER, PHASE_WAIT, PHASE_LAUNCH)
+
+
+@dataclass(frozen=True)
+class PhaseTiming:
+    phase: str
+    cycles: int        # nanoseconds on this runtime
+    sm_mask: int = 0
+
+    def __post_init__(self) -> None:
+        if self.cycles < 0:
+            raise ValueError("cycles must be nonnegative")
+        if self.phase in _MASKED_PHASES and self.sm_mask == 0:
+            raise ValueError(f"{self.phase} timing needs a nonempty sm mask")
+
+
+def full_mask(num_sms: int) -> int:
+    return (1 << num_sms) - 1
+
+
+def mask_of(sm_ids: Iterable[int]) -> int:
+    m = 0
+    for i in sm_ids:
+        m |= 1 << i
+    return m
+
+
+def sms_in_mask(mask: int) -> list[int]:
+    ids = []
+    while mask:
+        low = (mask & -mask).bit_length() - 1
+        ids.append(low)
+        mask &= mask - 1
+    return ids
+
+
+def _check_mask(mask: int, num_sms: int) -> list[int]:
+    if mask <= 0:
+        raise UsageError("sm mask must select at least one cluster")
+    if mask >> num_sms:
+        raise UsageError(f"sm mask {mask:#x} wider than {num_sms} clusters")
+    return sms_in_mask(mask)
+
+
+def timings_csv(rows, backend: Optional[str] = None) -> str:
+    """``run_id,model,phase,sm_mask,cycles[,backend]`` rows (host.py:84-99)."""
+    head = "run_id,model,phase,sm_mask,cycles" + (",backend" if backend is not None else "")
+    lines = [head]
+    for run_id, model, t in rows:
+        cols = [str(run_id), model, t.phase, str(t.sm_mask), str(t.cycles)]
+        if backend is not None:
+            cols.append(backend)
+        lines.append(",".join(cols))
+    return "\n".join(lines) + "\n"

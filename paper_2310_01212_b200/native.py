@@ -1,0 +1,445 @@
+"""The B200 persistent-worker session: drop-in for persistkern.native.
+
+``NativeSession`` keeps the reference's API
+(/root/reference/pkg/src/persistkern/native.py:82-299: ``start`` / ``trigger`` /
+``wait`` / ``dispose`` / ``recorded_trace``, the ``to_gpu`` / ``from_gpu`` /
+``worker_phase`` views, ``_spin_until``) but its workers are the CTAs of one
+resident sm_100a kernel, one per SM, and its mailboxes are pinned mapped host
+words.  Every call goes straight to liblk.so (include/lk.h) with the GIL
+released; there is no Python or CPU execution path behind it.
+
+``LaunchSyncBaseline`` is the conventional flow the paper compares against
+(``ThreadSpawnBaseline``, native.py:304-331): one cudaLaunchKernel of the same
+work function per task, then cudaStreamSynchronize.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import logging
+import time
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib, protocol
+from .device import WorkDescriptor
+from .errors import HangDetected, UsageError
+from .host import (PHASE_COPYIN, PHASE_COPYOUT, PHASE_DISPOSE, PHASE_INIT, PHASE_LAUNCH,
+                   PHASE_TRIGGER, PHASE_WAIT, PhaseTiming, _check_mask, full_mask)
+
+log = logging.getLogger(__name__)
+
+PURE_SPIN = "pure_spin"
+SPIN_THEN_YIELD = "spin_then_yield"
+BACKEND = "b200"
+
+
+@dataclass(frozen=True)
+class NativeConfig:
+    """Session configuration (reference fields first, native.py:44-60).
+
+    ``num_workers=None`` means one worker per SM (148 on B200).  The spin
+    settings govern the *host* spin in lk_wait; device workers always spin in
+    hardware, optionally backing off with ``poll_backoff_ns`` of __nanosleep.
+    """
+
+    num_workers: Optional[int] = None
+    pin_to_cores: bool = False
+    spin_strategy: str = SPIN_THEN_YIELD
+    spin_yield_threshold: int = 10_000
+    busy_loop_ns_per_iteration: float = 25.0
+    record_trace: bool = False
+    wait_timeout_s: float = 10.0
+    # B200 knobs
+    device: int = 0
+    threads_per_worker: int = 512
+    poll_backoff_ns: int = 0
+    cell_stride: int = 8
+    num_slots: int = 1024
+    trace_capacity: int = 65536
+    acquire_poll: bool = False
+    fence_always: bool = False
+
+    def __post_init__(self) -> None:
+        if self.num_workers is not None and self.num_workers < 1:
+            raise UsageError("num_workers must be >= 1")
+        if self.spin_strategy not in (PURE_SPIN, SPIN_THEN_YIELD):
+            raise UsageError(f"unknown spin strategy {self.spin_strategy!r}")
+        if self.spin_strategy == SPIN_THEN_YIELD and self.spin_yield_threshold <= 0:
+            raise UsageError("spin_yield_threshold must be positive")
+        if self.wait_timeout_s <= 0:
+            raise UsageError("wait_timeout_s must be positive")
+
+    def to_c(self) -> "_lib.lk_config":
+        c = _lib.lk_config()
+        c.num_workers = self.num_workers or 0
+        c.threads_per_worker = self.threads_per_worker
+        c.device = self.device
+        c.spin_strategy = 0 if self.spin_strategy == PURE_SPIN else 1
+        c.spin_yield_threshold = self.spin_yield_threshold
+        c.record_trace = 1 if self.record_trace else 0
+        c.trace_capacity = self.trace_capacity
+        c.poll_backoff_ns = self.poll_backoff_ns
+        c.cell_stride = self.cell_stride
+        c.num_slots = self.num_slots
+        c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
+        c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
+                   | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0))
+        return c
+
+
+def pin_host_thread(device: int) -> int:
+    """Pin the calling thread to the GPU's NUMA-local cores; returns core count."""
+    n = C.c_uint32()
+    _lib.check(_lib.load().lk_pin_thread_near(device, C.byref(n)))
+    return n.value
+
+
+class _WorkerHandle:
+    """Stands in for the reference's per-worker threading.Thread."""
+
+    def __init__(self, session: "NativeSession", wid: int):
+        self._s, self.wid = session, wid
+        self.name = f"lk-worker-{wid}"
+
+    def is_alive(self) -> bool:
+        return self._s._kernel_alive() and self._s.worker_phase[self.wid] is not protocol.Phase.EXITED
+
+
+class NativeSession:
+    """A booted persistent kernel (one CTA per SM) plus its mailboard."""
+
+    def __init__(self, cfg: NativeConfig, handle: C.c_void_p, num_workers: int):
+        self.cfg = cfg
+        self._lib = _lib.load()
+        self._h = handle
+        self.num_workers = num_workers
+        self.nwords = (num_workers + 63) // 64
+        self.disposed = False
+        self.timings: list[PhaseTiming] = []
+        self.descriptors: dict[int, WorkDescriptor] = {}
+        self._staged: dict[int, tuple] = {}
+        self._threads = [_WorkerHandle(self, i) for i in range(num_workers)]
+        self._u64 = C.c_uint64()
+        self._cells = (C.c_uint32 * num_workers)()
+        self._cells2 = (C.c_uint32 * num_workers)()
+        self._cells3 = (C.c_uint32 * num_workers)()
+
+    # -- bring-up ----------------------------------------------------------
+
+    @classmethod
+    def start(cls, cfg: Optional[NativeConfig] = None) -> tuple["NativeSession", PhaseTiming]:
+        cfg = cfg or NativeConfig()
+        lib = _lib.load()
+        t0 = time.perf_counter_ns()
+        if cfg.pin_to_cores:
+            try:
+                pin_host_thread(cfg.device)
+            except Exception as exc:   # downgrade like _maybe_pin (native.py:70-79)
+                log.warning("host core pinning failed (%s); running unpinned", exc)
+        h = C.c_void_p()
+        init_ns = C.c_uint64()
+        _lib.check(lib.lk_create(C.byref(cfg.to_c()), C.byref(h), C.byref(init_ns)))
+        n = C.c_uint32()
+        _lib.check(lib.lk_num_workers(h, C.byref(n)))
+        if cfg.num_workers is None:
+            cfg = dataclasses.replace(cfg, num_workers=n.value)
+        session = cls(cfg, h, n.value)
+        timing = PhaseTiming(PHASE_INIT, time.perf_counter_ns() - t0, full_mask(n.value))
+        session.timings.append(timing)
+        return session, timing
+
+    # -- views of the mailboard (native.py:88-94) --------------------------
+
+    def _read_cells(self):
+        _lib.check(self._lib.lk_read_cells(self._h, self._cells, self._cells2, self._cells3,
+                                           self.num_workers))
+        return list(self._cells), list(self._cells2), list(self._cells3)
+
+    @property
+    def to_gpu(self) -> list[int]:
+        return self._read_cells()[0]
+
+    @property
+    def from_gpu(self) -> list[int]:
+        return self._read_cells()[1]
+
+    @property
+    def worker_phase(self) -> list[protocol.Phase]:
+        return [protocol.PHASE_OF_CODE[c] for c in self._read_cells()[2]]
+
+    @property
+    def worker_error(self) -> list[Optional[BaseException]]:
+        out: list[Optional[BaseException]] = []
+        code, word = C.c_uint32(), C.c_uint32()
+        for i in range(self.num_workers):
+            _lib.check(self._lib.lk_worker_error(self._h, i, C.byref(code), C.byref(word)))
+            out.append(None if code.value == 0 else protocol.ProtocolViolation(
+                f"{_lib.WERR_NAMES.get(code.value, 'device error')} (word {word.value})",
+                word=word.value))
+        return out
+
+    @property
+    def pending_mask(self) -> int:
+        buf = (C.c_uint64 * self.nwords)()
+        _lib.check(self._lib.lk_pending(self._h, buf, self.nwords))
+        return int.from_bytes(bytes(buf), "little")
+
+    @property
+    def smid_map(self) -> list[int]:
+        """%smid of each worker's CTA: the B200 form of check_block_mapping."""
+        buf = (C.c_uint32 * self.num_workers)()
+        _lib.check(self._lib.lk_smid_map(self._h, buf, self.num_workers))
+        return list(buf)
+
+    def _kernel_alive(self) -> bool:
+        a = C.c_uint32()
+        _lib.check(self._lib.lk_kernel_alive(self._h, C.byref(a)))
+        return bool(a.value)
+
+    # -- host side -----------------------------------------------------------
+
+    def _require_live(self) -> None:
+        if self.disposed:
+            raise UsageError("session already disposed")
+
+    def _mask(self, mask: int) -> bytes:
+        return mask.to_bytes(8 * self.nwords, "little")
+
+    def register(self, work: WorkDescriptor, mask: int = 0) -> int:
+        """Stage ``work`` in its device slot (a no-op when already staged).
+
+        Returns the ns spent.  Payload kinds record the worker set that will
+        shard them, so a new mask for the same descriptor re-stages it.
+        """
+        t0 = time.perf_counter_ns()
+        key = mask if work.multi_worker else 0
+        if self._staged.get(work.slot) == (work, key) and self.descriptors.get(work.slot) is work:
+            return 0   # same descriptor object already staged with this mask
+        d = work.to_c()
+        rc = self._lib.lk_register_desc(self._h, work.slot, C.byref(d), self._mask(key), self.nwords)
+        _lib.check(rc)
+        self.descriptors[work.slot] = work
+        self._staged[work.slot] = (work, key)
+        return time.perf_counter_ns() - t0
+
+    def trigger(self, mask: int, work: WorkDescriptor) -> PhaseTiming:
+        """Dispatch: one word write per masked worker, no kernel launch."""
+        self._require_live()
+        _check_mask(mask, self.num_workers)
+        key = mask if work.multi_worker else 0
+        if self._staged.get(work.slot) == (work, key) and self.descriptors.get(work.slot) is work:
+            d = None   # this descriptor object is already staged for this worker set
+        else:
+            d = C.byref(work.to_c())
+        rc = self._lib.lk_trigger(self._h, self._mask(mask), self.nwords, work.slot, d, C.byref(self._u64))
+        _lib.check(rc)
+        if d is not None:
+            self.descriptors[work.slot] = work
+            self._staged[work.slot] = (work, key)
+        timing = PhaseTiming(PHASE_TRIGGER, self._u64.value, mask)
+        self.timings.append(timing)
+        return timing
+
+    def wait(self, mask: int) -> PhaseTiming:
+        """Spin (in C) until every masked worker published FINISHED, then ack."""
+        self._require_live()
+        sm_ids = _check_mask(mask, self.num_workers)
+        rc = self._lib.lk_wait(self._h, self._mask(mask), self.nwords, C.byref(self._u64))
+        _lib.check(rc, sm_ids=sm_ids)
+        timing = PhaseTiming(PHASE_WAIT, self._u64.value, mask)
+        self.timings.append(timing)
+        return timing
+
+    def _spin_until(self, cond, what: str, sm_ids) -> int:
+        """Python-level poll helper with the reference's timeout contract."""
+        deadline = time.monotonic() + self.cfg.wait_timeout_s
+        while True:
+            if cond():
+                return time.perf_counter_ns()
+            if time.monotonic() > deadline:
+                raise HangDetected(f"{what} made no progress within {self.cfg.wait_timeout_s}s",
+                                   sm_ids=tuple(sm_ids))
+            time.sleep(0)
+
+    def copyin(self, buf, host_array: np.ndarray) -> PhaseTiming:
+        """Stage a payload host->device (Copyin phase, host.py:212-213)."""
+        t0 = time.perf_counter_ns()
+        a = np.ascontiguousarray(host_array)
+        _lib.check(self._lib.lk_memcpy_h2d(_dev_addr(buf), a.ctypes.data, a.nbytes))
+        timing = PhaseTiming(PHASE_COPYIN, time.perf_counter_ns() - t0)
+        self.timings.append(timing)
+        return timing
+
+    def copyout(self, host_array: np.ndarray, buf) -> PhaseTiming:
+        """Read a result device->host (Copyout phase, host.py:215-216)."""
+        t0 = time.perf_counter_ns()
+        _lib.check(self._lib.lk_memcpy_d2h(host_array.ctypes.data, _dev_addr(buf), host_array.nbytes))
+        timing = PhaseTiming(PHASE_COPYOUT, time.perf_counter_ns() - t0)
+        self.timings.append(timing)
+        return timing
+
+    def dispose(self) -> PhaseTiming:
+        """EXIT to every worker; the persistent kernel retires."""
+        self._require_live()
+        rc = self._lib.lk_dispose(self._h, C.byref(self._u64))
+        _lib.check(rc, sm_ids=tuple(range(self.num_workers)))
+        self.disposed = True
+        timing = PhaseTiming(PHASE_DISPOSE, self._u64.value, full_mask(self.num_workers))
+        self.timings.append(timing)
+        return timing
+
+    def abort(self, timeout_s: float = 10.0) -> None:
+        """Retire the kernel whatever the host state (dead worker, pending work)."""
+        if self._h:
+            _lib.check(self._lib.lk_abort(self._h, int(timeout_s * 1e9)))
+            self.disposed = True
+
+    def close(self) -> None:
+        """Dispose (or abort) if needed and free the runtime's memory."""
+        if self._h:
+            if not self.disposed:
+                try:
+                    self.dispose()
+                except Exception:
+                    self.abort()
+            self._lib.lk_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            if self._h and self.disposed:
+                self._lib.lk_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    # -- tracing ----------------------------------------------------------------
+
+    def trace_arrays(self):
+        """The linearized trace as numpy arrays (step, side, worker, word, hseq, t_ns)."""
+        n = C.c_uint64()
+        _lib.check(self._lib.lk_trace_count(self._h, C.byref(n)))
+        buf = (_lib.lk_trace_rec * max(1, n.value))()
+        _lib.check(self._lib.lk_trace_read(self._h, buf, n.value, C.byref(n)))
+        dt = np.dtype([("step", "<u8"), ("side", "<u4"), ("worker", "<u4"), ("word", "<u4"),
+                       ("hseq", "<u4"), ("t_ns", "<u8")])
+        return np.frombuffer(bytes(buf), dtype=dt, count=n.value).copy()
+
+    def recorded_trace(self) -> list[protocol.TraceRecord]:
+        """Records in linearized order (per-worker causal order is exact)."""
+        a = self.trace_arrays()
+        return [protocol.TraceRecord(int(r["step"]), chr(r["side"]), int(r["worker"]), int(r["word"]))
+                for r in a]
+
+    # -- measurement ------------------------------------------------------------
+
+    def bench_roundtrip(self, masks: list[int], slot: int, rounds: int):
+        """Closed-loop trigger+wait rounds run entirely in C.
+
+        Returns (trigger_ns, done_ns, cycle_ns) numpy arrays: trigger call,
+        trigger start -> last FINISHED seen, trigger start -> ack consumed.
+        """
+        packed = b"".join(self._mask(m) for m in masks)
+        trig = np.zeros(rounds, dtype=np.uint64)
+        done = np.zeros(rounds, dtype=np.uint64)
+        cyc = np.zeros(rounds, dtype=np.uint64)
+        rc = self._lib.lk_bench_roundtrip(self._h, packed, len(masks), self.nwords, slot, rounds,
+                                          trig.ctypes.data, done.ctypes.data, cyc.ctypes.data)
+        _lib.check(rc)
+        return trig, done, cyc
+
+    def last_spans(self):
+        """Device globaltimer (begin, end) of each worker's last dispatch."""
+        b = np.zeros(self.num_workers, dtype=np.uint64)
+        e = np.zeros(self.num_workers, dtype=np.uint64)
+        _lib.check(self._lib.lk_last_spans(self._h, b.ctypes.data, e.ctypes.data, self.num_workers))
+        return b, e
+
+
+def _dev_addr(buf) -> int:
+    from .device import _addr
+    return _addr(buf)
+
+
+class LaunchSyncBaseline:
+    """cudaLaunchKernel + cudaStreamSynchronize per task (the CUDA "spawn")."""
+
+    def __init__(self, device: int = 0, threads_per_worker: int = 512, grid: Optional[int] = None):
+        self._lib = _lib.load()
+        self._h = C.c_void_p()
+        _lib.check(self._lib.lk_baseline_create(device, threads_per_worker, C.byref(self._h)))
+        if grid is None:
+            n = C.c_int()
+            _lib.check(self._lib.lk_sm_count(device, C.byref(n)))
+            grid = n.value
+        self.grid = grid
+        self.timings: list[PhaseTiming] = []
+        self._u64 = C.c_uint64()
+        self._inflight = False
+
+    def launch(self, work: WorkDescriptor, grid: Optional[int] = None) -> PhaseTiming:
+        if self._inflight:
+            raise UsageError("previous task not yet joined")
+        d = work.to_c()
+        g = grid or self.grid
+        _lib.check(self._lib.lk_baseline_launch(self._h, C.byref(d), g, C.byref(self._u64)))
+        self._inflight = True
+        timing = PhaseTiming(PHASE_LAUNCH, self._u64.value, full_mask(g))
+        self.timings.append(timing)
+        return timing
+
+    def wait(self) -> PhaseTiming:
+        if not self._inflight:
+            raise UsageError("no task in flight")
+        _lib.check(self._lib.lk_baseline_wait(self._h, C.byref(self._u64)))
+        self._inflight = False
+        timing = PhaseTiming(PHASE_WAIT, self._u64.value, full_mask(self.grid))
+        self.timings.append(timing)
+        return timing
+
+    def bench(self, work: WorkDescriptor, rounds: int, grid: Optional[int] = None):
+        d = work.to_c()
+        launch = np.zeros(rounds, dtype=np.uint64)
+        total = np.zeros(rounds, dtype=np.uint64)
+        _lib.check(self._lib.lk_baseline_bench(self._h, C.byref(d), grid or self.grid, rounds,
+                                               launch.ctypes.data, total.ctypes.data))
+        return launch, total
+
+    def time_kernel(self, work: WorkDescriptor, reps: int, grid: Optional[int] = None) -> float:
+        """Average device ms per launch (CUDA events on the launching stream)."""
+        d = work.to_c()
+        ms = C.c_float()
+        _lib.check(self._lib.lk_baseline_time_kernel(self._h, C.byref(d), grid or self.grid, reps,
+                                                     C.byref(ms)))
+        return float(ms.value)
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.lk_baseline_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# The reference's spawn-per-task baseline name, for drop-in call sites.
+ThreadSpawnBaseline = LaunchSyncBaseline
+
+
+def pingpong(device: int, rounds: int) -> np.ndarray:
+    """Raw host->GPU->host word round trips (ns): the link floor under LK."""
+    out = np.zeros(rounds, dtype=np.uint64)
+    _lib.check(_lib.load().lk_pingpong(device, rounds, out.ctypes.data))
+    return out

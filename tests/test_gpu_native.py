@@ -1,0 +1,375 @@
+"""The reference's native-executor suite (/root/reference/pkg/tests/test_native.py)
+run against the B200 session, plus GPU-only protocol parity checks.
+
+Every trace is validated by the ORACLE replay (oracle/protocol.py, pinned to
+the reference's golden vectors) and by the product's native validator, and
+each worker's projection must equal the reference's golden form
+D0 D4 (H[16+slot] D2 D1 H4 D4)* H8.
+"""
+from __future__ import annotations
+
+import random
+import statistics
+
+import pytest
+
+from oracle import projection
+from oracle import protocol as O
+from paper_2310_01212_b200 import _lib, host, native, protocol
+from paper_2310_01212_b200.device import WorkDescriptor
+from paper_2310_01212_b200.errors import (BusyTriggerError, DisposeWhileBusyError, HangDetected,
+                                          UsageError)
+
+pytestmark = pytest.mark.gpu
+
+FAST = dict(spin_yield_threshold=200, record_trace=True)
+TINY_WORK = WorkDescriptor(slot=0, iterations=32)
+
+
+_LIVE: list = []
+
+
+@pytest.fixture(autouse=True)
+def _reclaim_gpu():
+    """A test that leaves a session resident (dead worker, failed assert) must
+    not starve the next one of SMs: abort whatever is still running."""
+    yield
+    while _LIVE:
+        s = _LIVE.pop()
+        s.close()
+
+
+def start(num_workers=4, **kw):
+    cfg = native.NativeConfig(num_workers=num_workers, **{**FAST, **kw})
+    session, _ = native.NativeSession.start(cfg)
+    _LIVE.append(session)
+    return session
+
+
+def writes_of(session):
+    return [(r.side, r.sm_id, r.word) for r in session.recorded_trace()]
+
+
+def assert_trace_ok(session, program=None, num_workers=None):
+    w = writes_of(session)
+    r = O.replay(w)
+    assert r.violation is None, r.violation
+    v = protocol.validate_trace(w)
+    assert v is None, v
+    assert all(a == b for a, b in r.dispatch_counts().values())   # exactly once
+    if program is not None:
+        per = projection.program_slots(program, num_workers)
+        proj = projection.projections(w, num_workers)
+        for i in range(num_workers):
+            assert proj[i] == projection.expected_projection(per[i]), i
+    return r
+
+
+# ------------------------------------------------ reference test_native.py, one for one
+
+def test_start_brings_workers_to_idle():
+    session = start(4)
+    assert session.from_gpu == [protocol.NOP] * 4
+    assert all(p is protocol.Phase.IDLE for p in session.worker_phase)
+    session.dispose()
+
+
+def test_minimal_single_worker_session():
+    session = start(1)
+    assert session.from_gpu == [protocol.NOP]
+    session.trigger(1, TINY_WORK)
+    session.wait(1)
+    session.dispose()
+
+
+def test_boot_is_announced_in_the_trace():
+    session = start(2)
+    session.dispose()
+    for worker in (0, 1):
+        words = [r.word for r in session.recorded_trace()
+                 if r.side == protocol.DEVICE_SIDE and r.sm_id == worker]
+        assert words[:2] == [protocol.INIT, protocol.NOP]
+
+
+def test_zero_iteration_roundtrip_validates():
+    session = start(2)
+    session.trigger(0b01, WorkDescriptor(slot=0, iterations=0))
+    session.wait(0b01)
+    session.dispose()
+    assert_trace_ok(session, [(0b01, 0)], 2)
+
+
+def test_multi_worker_stress_smoke():
+    session = start(4)
+    cycles = 400
+    for k in range(cycles):
+        mask = 1 << (k % 4)
+        session.trigger(mask, TINY_WORK)
+        session.wait(mask)
+    session.dispose()
+    r = assert_trace_ok(session, [(1 << (k % 4), 0) for k in range(cycles)], 4)
+    assert sum(w for w, _ in r.dispatch_counts().values()) == cycles
+
+
+def test_full_mask_dispatch():
+    session = start(4)
+    session.trigger(0b1111, TINY_WORK)
+    session.wait(0b1111)
+    session.dispose()
+    assert_trace_ok(session, [(0b1111, 0)], 4)
+
+
+def test_single_writer_word_sets():
+    session = start(2)
+    session.trigger(0b11, TINY_WORK)
+    session.wait(0b11)
+    session.dispose()
+    for rec in session.recorded_trace():
+        if rec.side == protocol.HOST_SIDE:
+            assert rec.word in (protocol.NOP, protocol.EXIT) or rec.word >= protocol.WORK_BASE
+        else:
+            assert rec.word in protocol.FROM_GPU_WORDS
+
+
+def test_retrigger_busy_worker_rejected():
+    session = start(2)
+    session.trigger(0b01, WorkDescriptor(slot=0, iterations=200_000))
+    with pytest.raises(BusyTriggerError):
+        session.trigger(0b01, TINY_WORK)
+    session.wait(0b01)
+    session.dispose()
+
+
+def test_dispose_joins_every_thread():
+    session = start(4)
+    session.trigger(0b1111, TINY_WORK)
+    session.wait(0b1111)
+    session.dispose()
+    assert all(not th.is_alive() for th in session._threads)
+    with pytest.raises(UsageError):
+        session.trigger(1, TINY_WORK)
+
+
+def test_dispose_while_pending_rejected():
+    session = start(2)
+    session.trigger(0b10, TINY_WORK)
+    with pytest.raises(DisposeWhileBusyError):
+        session.dispose()
+    session.wait(0b10)
+    session.dispose()
+
+
+def test_spin_until_times_out():
+    session = start(1, wait_timeout_s=0.05)
+    with pytest.raises(HangDetected):
+        session._spin_until(lambda: False, "test condition", [0])
+    session.dispose()
+
+
+def test_trigger_latency_beats_kernel_launch():
+    session = start(4)
+    work = WorkDescriptor(slot=0, iterations=64)
+    trigger_ns = []
+    for k in range(300):
+        mask = 1 << (k % 4)
+        trigger_ns.append(session.trigger(mask, work).cycles)
+        session.wait(mask)
+    session.dispose()
+    baseline = native.LaunchSyncBaseline(grid=1)
+    spawn_ns = []
+    for _ in range(300):
+        spawn_ns.append(baseline.launch(work).cycles)
+        baseline.wait()
+    baseline.close()
+    assert statistics.median(trigger_ns) < statistics.median(spawn_ns)
+
+
+def test_descriptor_slot_locked_while_in_flight():
+    session = start(2)
+    session.trigger(0b01, WorkDescriptor(slot=0, iterations=100_000))
+    with pytest.raises(UsageError):
+        session.trigger(0b10, WorkDescriptor(slot=0, iterations=10))
+    session.trigger(0b10, WorkDescriptor(slot=1, iterations=10))
+    session.wait(0b11)
+    session.trigger(0b01, TINY_WORK)
+    session.wait(0b01)
+    session.dispose()
+    assert_trace_ok(session)
+
+
+def test_timing_rows_carry_backend_column():
+    session = start(1)
+    t = session.trigger(1, TINY_WORK)
+    session.wait(1)
+    session.dispose()
+    text = host.timings_csv([("r0", host.MODEL_LK, t)], backend=native.BACKEND)
+    assert text.splitlines()[1] == f"r0,LK,Trigger,1,{t.cycles},b200"
+
+
+def test_pinning_request_downgrades_gracefully():
+    session = start(2, pin_to_cores=True)
+    session.trigger(0b11, TINY_WORK)
+    session.wait(0b11)
+    session.dispose()
+
+
+def test_config_validation():
+    with pytest.raises(UsageError):
+        native.NativeConfig(num_workers=0)
+    with pytest.raises(UsageError):
+        native.NativeConfig(spin_strategy="nap")
+    with pytest.raises(UsageError):
+        native.NativeConfig(spin_strategy=native.SPIN_THEN_YIELD, spin_yield_threshold=0)
+
+
+def test_pure_spin_roundtrip():
+    session = start(1, spin_strategy=native.PURE_SPIN)
+    session.trigger(1, TINY_WORK)
+    session.wait(1)
+    session.dispose()
+    assert_trace_ok(session, [(1, 0)], 1)
+
+
+# ------------------------------------------------ B200-specific
+
+def test_all_sms_one_worker_each():
+    session = start(None, record_trace=False)
+    n = session.num_workers
+    assert n == 148
+    smids = session.smid_map
+    assert len(set(smids)) == n                 # one CTA per SM, all distinct
+    full = host.full_mask(n)
+    session.trigger(full, WorkDescriptor(slot=0, kind="empty"))
+    session.wait(full)
+    session.dispose()
+
+
+def test_full_gpu_trace_and_wide_masks():
+    session = start(None, trace_capacity=4096)
+    n = session.num_workers
+    full = host.full_mask(n)
+    prog = [(full, 0), (1 << (n - 1), 1), ((1 << 64) | (1 << 128) | 1, 2), (full, 3)]
+    for mask, slot in prog:
+        session.trigger(mask, WorkDescriptor(slot=slot, kind="empty"))
+        session.wait(mask)
+    with pytest.raises(UsageError):
+        session.trigger(1 << n, TINY_WORK)        # wider than the board
+    with pytest.raises(UsageError):
+        session.trigger(0, TINY_WORK)
+    session.dispose()
+    assert_trace_ok(session, prog, n)
+
+
+def test_wait_on_untriggered_worker_rejected():
+    session = start(2)
+    with pytest.raises(UsageError):
+        session.wait(0b01)
+    session.trigger(0b01, TINY_WORK)
+    with pytest.raises(UsageError):
+        session.wait(0b11)
+    session.wait(0b01)
+    session.dispose()
+
+
+def test_partial_wait_frees_slot_only_when_all_bits_waited():
+    session = start(4)
+    session.trigger(0b0011, WorkDescriptor(slot=3, iterations=10))
+    session.wait(0b0001)
+    with pytest.raises(UsageError):
+        session.trigger(0b0100, WorkDescriptor(slot=3, iterations=10))
+    session.wait(0b0010)
+    session.trigger(0b0100, WorkDescriptor(slot=3, iterations=10))
+    session.wait(0b0100)
+    session.dispose()
+    assert_trace_ok(session)
+
+
+def test_criterion_7_random_programs_on_gpu():
+    """Random split-mask programs (T/test_acceptance.py:122-145 shape) on the device."""
+    rng = random.Random(20250808)
+    session = start(8, trace_capacity=4096)
+    program = []
+    slot = 0
+    for _ in range(60):
+        sms = rng.sample(range(8), rng.randint(1, 8))
+        split = rng.randrange(len(sms)) if len(sms) > 1 and rng.random() < 0.3 else 0
+        covered = 0
+        for group in [g for g in (sms[:split], sms[split:]) if g]:
+            m = host.mask_of(group)
+            session.trigger(m, WorkDescriptor(slot=slot % 64, iterations=rng.randrange(400)))
+            program.append((m, slot % 64))
+            slot += 1
+            covered |= m
+        session.wait(covered)
+    session.dispose()
+    assert_trace_ok(session, program, 8)
+
+
+@pytest.mark.slow
+def test_criterion_8_gpu_stress():
+    """10,000 round-robin cycles, zero violations, exactly-once (T/test_acceptance.py:187-223)."""
+    session = start(4, trace_capacity=32768)
+    work = WorkDescriptor(slot=0, iterations=32)
+    trig = []
+    for k in range(10_000):
+        mask = 1 << (k % 4)
+        trig.append(session.trigger(mask, work).cycles)
+        session.wait(mask)
+    session.dispose()
+    r = assert_trace_ok(session, [(1 << (k % 4), 0) for k in range(10_000)], 4)
+    assert sum(w for w, _ in r.dispatch_counts().values()) == 10_000
+
+
+def test_c_side_roundtrip_loop_traces_validate():
+    session = start(None, trace_capacity=8192)
+    n = session.num_workers
+    session.register(WorkDescriptor(slot=0, kind="empty"))
+    masks = [1 << i for i in range(n)]
+    trig, done, cyc = session.bench_roundtrip(masks, 0, 5 * n)
+    assert (done > 0).all() and (cyc >= done).all()
+    session.dispose()
+    assert_trace_ok(session, [(masks[k % n], 0) for k in range(5 * n)], n)
+
+
+def test_unregistered_slot_refused():
+    session = start(1)
+    rc = session._lib.lk_trigger(session._h, session._mask(1), session.nwords, 9, None, None)
+    assert rc == _lib.LK_E_USAGE
+    session.dispose()
+
+
+@pytest.mark.parametrize("word,code", [(9, 1), (3, 1)])
+def test_device_violation_surfaces_as_worker_died(word, code):
+    """Fault injection: an illegal to_gpu word makes the worker record the
+    violation and leave its loop; the host's next call raises (native.py:128-131)."""
+    session = start(2)
+    _lib.check(session._lib.lk_debug_poke(session._h, 1, word))
+    session._spin_until(lambda: session.worker_phase[1] is protocol.Phase.EXITED, "device exit", [1])
+    err = session.worker_error[1]
+    assert err is not None and err.word == word
+    with pytest.raises(UsageError, match="worker 1 died"):
+        session.trigger(0b01, TINY_WORK)
+
+
+def test_conflicting_slot_while_working_is_a_device_violation():
+    session = start(1)
+    session.trigger(1, WorkDescriptor(slot=0, iterations=2_000_000))
+    _lib.check(session._lib.lk_debug_poke(session._h, 0, protocol.WORK_BASE + 5))
+    session._spin_until(lambda: session.worker_phase[0] is protocol.Phase.EXITED, "device exit", [0])
+    assert session.worker_error[0].word == protocol.WORK_BASE + 5
+
+
+def test_baseline_launch_wait_contract():
+    b = native.LaunchSyncBaseline()
+    with pytest.raises(UsageError):
+        b.wait()
+    b.launch(WorkDescriptor(slot=0, kind="empty"))
+    with pytest.raises(UsageError):
+        b.launch(WorkDescriptor(slot=0, kind="empty"))
+    b.wait()
+    b.close()
+
+
+def test_pingpong_floor_runs():
+    rt = native.pingpong(0, 200)
+    assert (rt > 0).all()
