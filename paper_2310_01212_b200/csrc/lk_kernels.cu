@@ -133,7 +133,7 @@ __device__ __forceinline__ void map_chunk(const lk_desc& d, Part p, const Op& op
     for (int u = 0; u < U; ++u) st4(o4 + v + u * T, vop(op, x[u], kTwo ? y[u] : x[u]));
   }
   for (; v < ve; v += T) st4(o4 + v, vop(op, ld_cg4(a4 + v), kTwo ? ld_cg4(c4 + v) : make_uint4(0, 0, 0, 0)));
-  for (uint64_t i = (ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
+  for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -184,7 +184,7 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
       s.z += __uint_as_float(r.z); s.w += __uint_as_float(r.w);
     }
     acc = (s.x + s.y) + (s.z + s.w);
-    for (uint64_t i = (ve << 2) + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
+    for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
   }
   acc = warp_sum(acc);
   const uint32_t warp = t >> 5, lane = t & 31, nwarps = (T + 31) >> 5;
