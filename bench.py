@@ -319,7 +319,8 @@ def run_lk_arm(args, world, rank, local):
     except Exception:
         pinned = 0
     cfg = native.NativeConfig(num_workers=args.workers, device=device, spin_strategy=native.PURE_SPIN,
-                              poll_backoff_ns=args.backoff_ns, cell_stride=args.cell_stride)
+                              poll_backoff_ns=args.backoff_ns, cell_stride=args.cell_stride,
+                              poll_replicas=args.replicas, poll_spacing_ns=args.spacing_ns)
     session, init = native.NativeSession.start(cfg)
     n = session.num_workers
     empty = WorkDescriptor(slot=0, kind="empty")
@@ -428,6 +429,7 @@ def run_lk_arm(args, world, rank, local):
                                "round-robin single-worker masks", "workers": n, "rounds_per_step": R,
                    "total_rounds": int(units), "threads_per_worker": cfg.threads_per_worker,
                    "cell_stride": cfg.cell_stride, "poll_backoff_ns": cfg.poll_backoff_ns,
+                   "poll_replicas": cfg.poll_replicas, "poll_spacing_ns": cfg.poll_spacing_ns,
                    "host_cores_pinned": pinned, "l2": "n/a for the empty task (no payload); payload "
                    "GB/s rotate buffers over >= 4x L2",
                    "timing": "host CLOCK_MONOTONIC per round; max over ranks"},
@@ -463,7 +465,9 @@ def main():
     ap.add_argument("--rounds", type=int, default=20_000, help="round trips per step")
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--backoff-ns", type=int, default=0)
-    ap.add_argument("--cell-stride", type=int, default=8)
+    ap.add_argument("--cell-stride", type=int, default=128)
+    ap.add_argument("--replicas", type=int, default=4)
+    ap.add_argument("--spacing-ns", type=int, default=200)
     ap.add_argument("--full-rounds", type=int, default=100_000)
     ap.add_argument("--e2e-rounds", type=int, default=100_000)
     ap.add_argument("--base-rounds", type=int, default=100_000)

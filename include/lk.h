@@ -100,10 +100,12 @@ typedef struct lk_config {
   uint32_t record_trace;         /* native.py:51 */
   uint32_t trace_capacity;       /* device records per worker; 0 = 65536 */
   uint32_t poll_backoff_ns;      /* device __nanosleep between idle polls (0 = none) */
-  uint32_t cell_stride;          /* bytes between mailbox cells: 8, 64 or 128; 0 = 8 */
+  uint32_t cell_stride;          /* bytes between mailbox cells: 8..128 (power of 2); 0 = 128 */
   uint32_t num_slots;            /* descriptor table entries; 0 = 1024 */
   uint64_t wait_timeout_ns;      /* wait_timeout_s (native.py:52) */
   uint32_t flags;                /* LK_CF_* */
+  uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 4 */
+  uint32_t poll_spacing_ns;      /* stagger between replica loads; 0 = 200 */
   uint32_t reserved;
 } lk_config;
 

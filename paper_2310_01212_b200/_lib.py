@@ -80,6 +80,8 @@ class lk_config(C.Structure):
         ("num_slots", C.c_uint32),
         ("wait_timeout_ns", C.c_uint64),
         ("flags", C.c_uint32),
+        ("poll_replicas", C.c_uint32),
+        ("poll_spacing_ns", C.c_uint32),
         ("reserved", C.c_uint32),
     ]
 

@@ -118,12 +118,11 @@ struct lk_session {
 
   // pinned mapped host block
   uint8_t* host_block = nullptr;
-  uint32_t* to_gpu = nullptr;                 // stride cell_words
+  unsigned long long* to_gpu = nullptr;       // worker i replica k at [(i*replicas+k)*cell_u64]
   volatile unsigned long long* status = nullptr;  // stride cell_u64
-  uint32_t* hseq = nullptr;                   // stride cell_words
   volatile unsigned long long* err = nullptr;
   volatile uint32_t* smid = nullptr;
-  uint32_t cell_words = 2, cell_u64 = 1;
+  uint32_t cell_u64 = 16, replicas = 4;
 
   // device block
   uint8_t* dev_block = nullptr;
@@ -154,13 +153,16 @@ struct lk_session {
 
   inline uint32_t word(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64]); }
   inline uint32_t phase(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64] >> 32); }
+  // One logical to_gpu write: {word, seq} into every replica line.
   inline void host_write(uint32_t i, uint32_t w) {
-    if (cfg.record_trace) {
-      const uint32_t s = ++host_seq[i];
-      __atomic_store_n(hseq + uint64_t(i) * cell_words, s, __ATOMIC_RELEASE);
-      host_log[i].push_back(HostRec{s, w, now_ns()});
-    }
-    __atomic_store_n(to_gpu + uint64_t(i) * cell_words, w, __ATOMIC_RELEASE);
+    const uint32_t sq = ++host_seq[i];
+    if (cfg.record_trace) host_log[i].push_back(HostRec{sq, w, now_ns()});
+    const unsigned long long v = uint64_t(w) | (uint64_t(sq) << 32);
+    unsigned long long* c = to_gpu + uint64_t(i) * replicas * cell_u64;
+    for (uint32_t k = 0; k < replicas; ++k) __atomic_store_n(c + k * cell_u64, v, __ATOMIC_RELEASE);
+  }
+  inline uint32_t to_gpu_word(uint32_t i) const {
+    return uint32_t(__atomic_load_n(to_gpu + uint64_t(i) * replicas * cell_u64, __ATOMIC_ACQUIRE));
   }
 };
 
@@ -276,10 +278,14 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.spin_strategy > 1) return fail(LK_E_USAGE, "unknown spin strategy %u", cfg.spin_strategy);
   if (cfg.spin_strategy == 1 && cfg.spin_yield_threshold == 0)
     return fail(LK_E_USAGE, "spin_yield_threshold must be positive");
-  if (cfg.cell_stride == 0) cfg.cell_stride = 8;
+  if (cfg.cell_stride == 0) cfg.cell_stride = 128;
   if (cfg.cell_stride != 8 && cfg.cell_stride != 16 && cfg.cell_stride != 32 && cfg.cell_stride != 64 &&
       cfg.cell_stride != 128)
     return fail(LK_E_CONFIG, "cell_stride must be 8, 16, 32, 64 or 128");
+  if (cfg.poll_replicas == 0) cfg.poll_replicas = 4;
+  if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)
+    return fail(LK_E_CONFIG, "poll_replicas must be 1, 2, 4 or 8");
+  if (cfg.poll_spacing_ns == 0) cfg.poll_spacing_ns = 200;
   if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 512;
   if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 1024)
     return fail(LK_E_CONFIG, "threads_per_worker must be a multiple of 32 and <= 1024");
@@ -306,8 +312,8 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->nwords = (s->nw + 63) / 64;
   s->threads = cfg.threads_per_worker;
   s->device = cfg.device;
-  s->cell_words = cfg.cell_stride / 4;
   s->cell_u64 = cfg.cell_stride / 8;
+  s->replicas = cfg.poll_replicas;
   s->pending.assign(s->nwords, 0);
   s->registered.assign(cfg.num_slots, 0);
   s->reg_desc.resize(cfg.num_slots);
@@ -325,22 +331,23 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     return rc;
   };
 
-  // --- pinned mapped mailboxes: to_gpu | status | hseq | err | smid, 4 KiB aligned
+  // --- pinned mapped mailboxes: to_gpu replicas | status | err | smid, 4 KiB aligned
   auto al = [](size_t x) { return (x + 4095) & ~size_t(4095); };
+  const size_t tob = al(size_t(s->nw) * s->replicas * cfg.cell_stride);
   const size_t cells = al(size_t(s->nw) * cfg.cell_stride);
   const size_t errb = al(size_t(s->nw) * 8), smidb = al(size_t(s->nw) * 4);
-  const size_t host_bytes = 3 * cells + errb + smidb;
+  const size_t host_bytes = tob + cells + errb + smidb;
   cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&s->host_block), host_bytes,
                                  cudaHostAllocMapped | cudaHostAllocPortable);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(ce)));
   memset(s->host_block, 0, host_bytes);
-  s->to_gpu = reinterpret_cast<uint32_t*>(s->host_block);
-  s->status = reinterpret_cast<volatile unsigned long long*>(s->host_block + cells);
-  s->hseq = reinterpret_cast<uint32_t*>(s->host_block + 2 * cells);
-  s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + 3 * cells);
-  s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + 3 * cells + errb);
+  s->to_gpu = reinterpret_cast<unsigned long long*>(s->host_block);
+  s->status = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob);
+  s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob + cells);
+  s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + tob + cells + errb);
   for (uint32_t i = 0; i < s->nw; ++i) {
-    s->to_gpu[uint64_t(i) * s->cell_words] = LK_NOP;
+    for (uint32_t k = 0; k < s->replicas; ++k)
+      s->to_gpu[(uint64_t(i) * s->replicas + k) * s->cell_u64] = LK_NOP;  // {NOP, seq 0}
     s->status[uint64_t(i) * s->cell_u64] = uint64_t(LK_NOP) | (uint64_t(LK_PHASE_BOOTING) << 32);
     s->smid[i] = 0xFFFFFFFFu;
   }
@@ -385,7 +392,6 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   memset(&a, 0, sizeof a);
   a.to_gpu = s->to_gpu;
   a.status = const_cast<unsigned long long*>(s->status);
-  a.hseq = s->hseq;
   a.err = const_cast<unsigned long long*>(s->err);
   a.smid = const_cast<uint32_t*>(s->smid);
   a.desc = s->d_desc;
@@ -394,8 +400,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.spans = s->d_spans;
   a.trace = s->d_trace;
   a.trace_cnt = s->d_tcnt;
-  a.cell_words = s->cell_words;
   a.cell_u64 = s->cell_u64;
+  a.replicas = s->replicas;
+  a.spacing_ns = cfg.poll_spacing_ns;
   a.num_slots = cfg.num_slots;
   a.nwords = s->nwords;
   a.trace_cap = cfg.trace_capacity;
@@ -616,8 +623,7 @@ extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
     s->disposed = true;
     return LK_OK;
   }
-  for (uint32_t i = 0; i < s->nw; ++i)
-    __atomic_store_n(s->to_gpu + uint64_t(i) * s->cell_words, LK_EXIT, __ATOMIC_RELEASE);
+  for (uint32_t i = 0; i < s->nw; ++i) s->host_write(i, LK_EXIT);
   const uint64_t deadline = now_ns() + (timeout_ns ? timeout_ns : s->cfg.wait_timeout_ns);
   for (;;) {
     const int ks = kernel_status(s);
@@ -652,7 +658,7 @@ extern "C" int lk_read_cells(lk_session* s, uint32_t* to_gpu, uint32_t* from_gpu
   const uint32_t m = std::min(n, s->nw);
   for (uint32_t i = 0; i < m; ++i) {
     const unsigned long long st = s->status[uint64_t(i) * s->cell_u64];
-    if (to_gpu) to_gpu[i] = __atomic_load_n(s->to_gpu + uint64_t(i) * s->cell_words, __ATOMIC_ACQUIRE);
+    if (to_gpu) to_gpu[i] = s->to_gpu_word(i);
     if (from_gpu) from_gpu[i] = uint32_t(st);
     if (phase) phase[i] = uint32_t(st >> 32);
   }
@@ -661,7 +667,8 @@ extern "C" int lk_read_cells(lk_session* s, uint32_t* to_gpu, uint32_t* from_gpu
 
 extern "C" int lk_debug_poke(lk_session* s, uint32_t worker, uint32_t word) {
   if (!s || worker >= s->nw) return fail(LK_E_USAGE, "bad worker");
-  __atomic_store_n(s->to_gpu + uint64_t(worker) * s->cell_words, word, __ATOMIC_RELEASE);
+  std::lock_guard<std::mutex> g(s->mu);
+  s->host_write(worker, word);
   return LK_OK;
 }
 

@@ -16,9 +16,9 @@ struct lk_dev_trace {
 // mapped host memory (to_gpu, status, hseq, err, smid); everything else is
 // device-resident.
 struct lk_dev_args {
-  const uint32_t* to_gpu;          // host-mapped, cell i at to_gpu[i*cell_words]
+  const unsigned long long* to_gpu;  // host-mapped; worker i replica k at to_gpu[(i*replicas + k)*cell_u64]:
+                                     // word | seq<<32 (seq = host write index, monotone per worker)
   unsigned long long* status;      // host-mapped, cell i at status[i*cell_u64]: word | phase<<32
-  const uint32_t* hseq;            // host-mapped, same stride as to_gpu (trace mode)
   unsigned long long* err;         // host-mapped, err[i] = code | word<<32
   uint32_t* smid;                  // host-mapped, smid[i]
   const lk_desc* desc;             // device, num_slots entries
@@ -27,8 +27,9 @@ struct lk_dev_args {
   unsigned long long* spans;       // device, 2 per worker: begin, end (globaltimer)
   lk_dev_trace* trace;             // device, num_workers * trace_cap
   uint32_t* trace_cnt;             // device, num_workers
-  uint32_t cell_words;             // to_gpu / hseq stride in u32
-  uint32_t cell_u64;               // status stride in u64
+  uint32_t cell_u64;               // cell stride in u64 (to_gpu replicas and status)
+  uint32_t replicas;               // to_gpu replicas per worker: 1, 2, 4 or 8
+  uint32_t spacing_ns;             // stagger between replica loads
   uint32_t num_slots;
   uint32_t nwords;
   uint32_t trace_cap;

@@ -246,10 +246,10 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
 struct Elected {           // thread 0's private protocol state
   lk_wstate st;
   uint32_t pub;            // word currently in our from_gpu cell
-  uint32_t hseq_seen;
+  uint32_t seq;            // host write index of the current to_gpu word
+  uint32_t cur;            // current to_gpu word
   uint32_t tcnt;
-  uint32_t settled;
-  bool settled_valid;
+  bool dirty;              // cur not yet stepped to a fixed point
 };
 
 __device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t word,
@@ -257,7 +257,7 @@ __device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elec
   if (a.record_trace && word != e.pub) {
     lk_dev_trace* r = a.trace + uint64_t(wid) * a.trace_cap + (e.tcnt % a.trace_cap);
     r->word = word;
-    r->hseq = e.hseq_seen;
+    r->hseq = e.seq;
     r->t_ns = globaltimer();
     ++e.tcnt;
     a.trace_cnt[wid] = e.tcnt;
@@ -276,21 +276,22 @@ __device__ __forceinline__ void report_error(const lk_dev_args& a, uint32_t wid,
   publish(a, wid, e, e.pub, true);
 }
 
-// Spin on to_gpu[wid] until the state machine begins work or exits.
-__device__ __noinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e) {
-  const uint32_t* cell = a.to_gpu + uint64_t(wid) * a.cell_words;
-  const bool acquire = (a.flags & LK_CF_ACQUIRE_POLL) || a.record_trace;
-  for (;;) {
-    const uint32_t w = acquire ? ld_acquire_sys(cell) : ld_relaxed_sys(cell);
-    if (e.settled_valid && w == e.settled) {
-      if (a.backoff_ns) __nanosleep(a.backoff_ns);
-      continue;
-    }
-    if (a.record_trace) e.hseq_seen = ld_relaxed_sys(a.hseq + uint64_t(wid) * a.cell_words);
+__device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* p, bool acquire) {
+  unsigned long long v;
+  if (acquire) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Step the current word to a fixed point, exactly as the reference worker
+// re-reads a level-triggered cell until it stops making progress
+// (native.py:158-195).  Returns an action, or LK_ACT_NONE once settled.
+__device__ __forceinline__ uint32_t settle(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  while (e.dirty) {
     const uint32_t before = e.st.phase;
-    const lk_step_out o = lk_worker_step(e.st, w);
+    const lk_step_out o = lk_worker_step(e.st, e.cur);
     if (o.werr) {
-      report_error(a, wid, e, o.werr, w);
+      report_error(a, wid, e, o.werr, e.cur);
       return LK_ACT_EXIT;
     }
     bool progressed = e.st.phase != before;
@@ -300,12 +301,58 @@ __device__ __noinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Electe
     } else if (e.st.phase != before) {
       publish(a, wid, e, e.pub, false);  // phase-only update (EXIT): word unchanged
     }
-    if (o.action != LK_ACT_NONE) {
-      e.settled_valid = false;
-      return o.action;
+    if (o.action != LK_ACT_NONE) return o.action;  // cur stays dirty: re-stepped after the work
+    e.dirty = progressed;
+  }
+  return LK_ACT_NONE;
+}
+
+// Spin until the state machine begins work or exits.  The to_gpu cell is K
+// replicas {word, seq} on separate 128-B lines; one ld.relaxed.sys per replica
+// is kept in flight, staggered by spacing_ns, so the host's write is sampled K
+// times per PCIe round trip (same-line loads would merge in L1).  A value is
+// accepted only when its seq is newer, so replicas written one after another
+// never make the state machine go backwards.
+template <int K>
+__device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  const unsigned long long* base = a.to_gpu + uint64_t(wid) * K * a.cell_u64;
+  const uint32_t step = a.cell_u64;
+  const bool acquire = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
+  for (;;) {
+    const uint32_t act = settle(a, wid, e);
+    if (act != LK_ACT_NONE) return act;
+    unsigned long long v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v[k] = ld_cell(base + k * step, acquire);
+      if (K > 1) __nanosleep(a.spacing_ns);
     }
-    e.settled_valid = !progressed;
-    e.settled = w;
+    for (bool fresh = false; !fresh;) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const unsigned long long c = v[k];
+        if (uint32_t(c >> 32) > e.seq) {
+          e.seq = uint32_t(c >> 32);
+          e.cur = uint32_t(c);
+          e.dirty = true;
+          fresh = true;
+          break;
+        }
+        v[k] = ld_cell(base + k * step, acquire);
+        if (K > 1) __nanosleep(a.spacing_ns);
+        else if (a.backoff_ns) __nanosleep(a.backoff_ns);
+      }
+      if (!fresh && K > 1 && a.backoff_ns) __nanosleep(a.backoff_ns);
+    }
+  }
+}
+
+__device__ __noinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  switch (a.replicas) {
+    case 1: return poll_k<1>(a, wid, e);
+    case 2: return poll_k<2>(a, wid, e);
+    case 8: return poll_k<8>(a, wid, e);
+    default: return poll_k<4>(a, wid, e);
   }
 }
 
@@ -321,10 +368,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) lk_persistent_kernel(const lk_
   Elected e;
   e.st = lk_wstate{LK_PHASE_BOOTING, 0};
   e.pub = LK_NOP;  // cells start at the NOP sentinel (protocol.py:217-218)
-  e.hseq_seen = 0;
+  e.seq = 0;       // the host's initial {NOP, seq 0} value
+  e.cur = LK_NOP;
   e.tcnt = 0;
-  e.settled = 0;
-  e.settled_valid = false;
+  e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   uint64_t t_begin = 0;
   if (threadIdx.x == 0) st_relaxed_sys_u32(a.smid + wid, smid());
 

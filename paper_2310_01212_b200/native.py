@@ -56,7 +56,9 @@ class NativeConfig:
     device: int = 0
     threads_per_worker: int = 512
     poll_backoff_ns: int = 0
-    cell_stride: int = 8
+    cell_stride: int = 128
+    poll_replicas: int = 4
+    poll_spacing_ns: int = 200
     num_slots: int = 1024
     trace_capacity: int = 65536
     acquire_poll: bool = False
@@ -84,6 +86,8 @@ class NativeConfig:
         c.poll_backoff_ns = self.poll_backoff_ns
         c.cell_stride = self.cell_stride
         c.num_slots = self.num_slots
+        c.poll_replicas = self.poll_replicas
+        c.poll_spacing_ns = self.poll_spacing_ns
         c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0))
