@@ -154,21 +154,51 @@ def aggregate(rank_times, rank_units):
 
 # ----------------------------------------------------------------------------- CPU baseline
 
-def cpu_baseline_port(num_workers=4, rounds=1000, warmup=50, n=65536, threshold=10_000, budget_s=30.0):
-    """The oracle port of the reference executor (oracle/cpu_session.py) on this
-    host: BASELINE config 0 (4 workers, int32 vector add of 64 Ki elements on
-    the worker thread, round-robin masks)."""
+def cpu_baseline_config0(num_workers=4, rounds=1000, warmup=50, n=65536, threshold=10_000, budget_s=30.0):
+    """BASELINE config 0 on this host's cores: 4 workers, int32 vector add of
+    64 Ki elements run on the worker thread, round-robin masks, reference
+    default spin_yield_threshold.  Runs the unmodified reference executor
+    (baseline/_ref) with its descriptor table swapped for a dict whose lookup
+    (native.py:180, on the worker thread) performs the vector add -- a harness
+    shim, no reference edit; else the oracle port.  Returns (tasks/s, ns
+    latencies, kind)."""
     from oracle import work as W
-    from oracle.cpu_session import CpuSession
     a = np.random.default_rng(0).integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
     b = np.random.default_rng(1).integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
-    outs = [np.empty(n, np.int32) for _ in range(num_workers)]
+    out = np.empty(n, np.int32)
 
-    def work_fn(i, slot):
-        np.copyto(outs[i], W.vector_add_i32(a, b))
+    Exe = reference_executor()
+    if Exe.kind == "reference":
+        from persistkern import native as ref_native
+        from persistkern.device import WorkDescriptor as RefWork
 
-    s = CpuSession(num_workers=num_workers, spin_yield_threshold=threshold, work_fn=work_fn)
-    s.start()
+        class _PayloadTable(dict):
+            def __getitem__(self, slot):
+                np.copyto(out, W.vector_add_i32(a, b))
+                return dict.__getitem__(self, slot)
+
+        rs, _ = ref_native.NativeSession.start(
+            ref_native.NativeConfig(num_workers=num_workers, spin_yield_threshold=threshold))
+        rs.descriptors = _PayloadTable()
+        rw = RefWork(slot=0, iterations=0)
+
+        class _S:
+            def trigger(self, m, _slot):
+                rs.trigger(m, rw)
+
+            def wait(self, m):
+                rs.wait(m)
+
+            def dispose(self):
+                rs.dispose()
+        s = _S()
+    else:
+        from oracle.cpu_session import CpuSession
+
+        def work_fn(i, slot):
+            np.copyto(out, W.vector_add_i32(a, b))
+        s = CpuSession(num_workers=num_workers, spin_yield_threshold=threshold, work_fn=work_fn)
+        s.start()
     lat = []
     t_start = time.perf_counter()
     for k in range(warmup + rounds):
@@ -182,41 +212,84 @@ def cpu_baseline_port(num_workers=4, rounds=1000, warmup=50, n=65536, threshold=
             break
     s.dispose()
     tot = sum(lat) / 1e9
-    return len(lat) / tot, lat
+    return len(lat) / tot, lat, Exe.kind
+
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_executor():
+    """The unmodified reference executor: persistkern.native from baseline/_ref
+    (pip-installed from /root/reference, travels to the GPU box) -> kind
+    "reference"; else the oracle port (oracle/cpu_session.py) -> kind "port"."""
+    if (REF_DIR / "persistkern" / "native.py").exists():
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        from persistkern import native as ref_native
+        from persistkern.device import WorkDescriptor as RefWork
+
+        class _Ref:
+            kind = "reference"
+            name = "persistkern.native.NativeSession (baseline/_ref, unmodified)"
+
+            def __init__(self, workers, threshold):
+                self.s, _ = ref_native.NativeSession.start(
+                    ref_native.NativeConfig(num_workers=workers, spin_yield_threshold=threshold))
+                self.w = RefWork(slot=0, iterations=0)
+
+            def roundtrip(self, m):
+                self.s.trigger(m, self.w)
+                self.s.wait(m)
+
+            def close(self):
+                self.s.dispose()
+        return _Ref
+    from oracle.cpu_session import CpuSession
+
+    class _Port:
+        kind = "port"
+        name = "oracle/cpu_session.py (thread-per-worker port of persistkern.native)"
+
+        def __init__(self, workers, threshold):
+            self.s = CpuSession(num_workers=workers, spin_yield_threshold=threshold)
+            self.s.start()
+
+        def roundtrip(self, m):
+            self.s.trigger(m, 0)
+            self.s.wait(m)
+
+        def close(self):
+            self.s.dispose()
+    return _Port
 
 
 def run_reference_arm(args, world, rank):
-    """--impl reference: the reference's CPU executor (oracle port) on our config."""
+    """--impl reference: the reference's own CPU executor on our arm's config
+    (148 workers, empty task, round-robin single-worker masks)."""
     if rank != 0:
         return
-    from oracle.cpu_session import CpuSession
     workers = args.workers or 148
-    s = CpuSession(num_workers=workers, spin_yield_threshold=200)
-    s.start()
+    threshold = 200   # the reference test suite's setting (T/test_native.py:13); 10k default is ~20x slower here
+    Exe = reference_executor()
+    t_init = time.perf_counter()
+    s = Exe(workers, threshold)
+    init_s = time.perf_counter() - t_init
     per_step = args.ref_rounds
-
-    def step(k0):
-        for k in range(k0, k0 + per_step):
-            m = 1 << (k % workers)
-            s.trigger(m, 0)
-            s.wait(m)
-
     k = 0
     for _ in range(args.warmup):
-        step(k)
+        for kk in range(k, k + per_step):
+            s.roundtrip(1 << (kk % workers))
         k += per_step
     lat = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
         for kk in range(k, k + per_step):
-            m = 1 << (kk % workers)
             a = time.perf_counter_ns()
-            s.trigger(m, 0)
-            s.wait(m)
+            s.roundtrip(1 << (kk % workers))
             lat.append(time.perf_counter_ns() - a)
         k += per_step
     dt = time.perf_counter() - t0
-    s.dispose()
+    s.close()
     rounds = per_step * args.steps
     value = rounds / dt
     cores = len(os.sched_getaffinity(0))
@@ -225,12 +298,14 @@ def run_reference_arm(args, world, rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"empty-task round-robin dispatch, {workers} persistent workers",
-                   "rounds_per_step": per_step, "executor": "thread-per-worker CPU port of "
-                   "persistkern.native (oracle/cpu_session.py), spin_yield_threshold=200"},
+        "config": {"workload": f"configs[1] shape on the CPU executor: empty-task round-robin dispatch, "
+                               f"{workers} persistent workers", "rounds_per_step": per_step,
+                   "executor": Exe.name, "spin_yield_threshold": threshold,
+                   "init_s": round(init_s, 3)},
         "latency_us": lat_summary(lat),
-        "cpu_baseline": {"value": round(value, 3), "unit": "tasks/s", "cores": cores, "kind": "port",
-                         "sample": f"{rounds} round trips on {workers} Python worker threads (GIL-bound)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "tasks/s", "cores": cores, "kind": Exe.kind,
+                         "sample": f"{rounds} round trips on {workers} Python worker threads "
+                                   f"(GIL-bound; {cores} host threads available)"},
         "e2e": {"value": round(value, 3), "unit": "tasks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -412,8 +487,8 @@ def run_lk_arm(args, world, rank, local):
 
     cpu = None
     if not args.no_cpu_baseline:
-        cv, clat = cpu_baseline_port(budget_s=args.cpu_budget_s)
-        cpu = {"value": round(cv, 2), "unit": "tasks/s", "cores": 1, "kind": "port",
+        cv, clat, ckind = cpu_baseline_config0(budget_s=args.cpu_budget_s)
+        cpu = {"value": round(cv, 2), "unit": "tasks/s", "cores": 1, "kind": ckind,
                "sample": f"{len(clat)} round trips of BASELINE config 0 (4 Python worker threads, "
                          "int32 vector add 64 Ki elements via numpy on the worker, spin_yield_threshold "
                          "10000 = reference default); GIL-serialised so ~1 core; p50 "
@@ -477,7 +552,7 @@ def main():
     ap.add_argument("--no-payload", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=30.0)
-    ap.add_argument("--ref-rounds", type=int, default=10, help="reference arm round trips per step")
+    ap.add_argument("--ref-rounds", type=int, default=8, help="reference arm round trips per step")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

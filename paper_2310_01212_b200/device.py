@@ -193,3 +193,32 @@ class WorkDescriptor:
         if any(p % 16 for p in (d.in0, d.in1, d.out)):
             d.flags |= _lib.DF_SCALAR
         return d
+
+
+_FOREIGN: dict = {}
+
+
+def as_work(work) -> WorkDescriptor:
+    """Accept the reference's own ``persistkern.device.WorkDescriptor`` (or any
+    object with its fields: slot, iterations, kind, data_in_ref, data_out_ref;
+    P/device.py:48-66) so existing call sites pass their descriptors unchanged.
+    The converted descriptor is cached per source object, so re-triggering the
+    same foreign descriptor stays a words-only dispatch."""
+    if isinstance(work, WorkDescriptor):
+        return work
+    hit = _FOREIGN.get(id(work))
+    if hit is not None and hit[0] is work:
+        return hit[1]
+    try:
+        conv = WorkDescriptor(slot=work.slot, iterations=getattr(work, "iterations", 0),
+                              kind=getattr(work, "kind", BUSY_LOOP),
+                              data_in_ref=getattr(work, "data_in_ref", None),
+                              data_out_ref=getattr(work, "data_out_ref", None),
+                              alpha=getattr(work, "alpha", 1.0), n=getattr(work, "n", None),
+                              total_ref=getattr(work, "total_ref", None))
+    except AttributeError as exc:
+        raise UsageError(f"not a work descriptor: {type(work).__name__}") from exc
+    if len(_FOREIGN) > 4096:
+        _FOREIGN.clear()
+    _FOREIGN[id(work)] = (work, conv)
+    return conv

@@ -24,7 +24,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib, protocol
-from .device import WorkDescriptor
+from .device import WorkDescriptor, as_work
 from .errors import HangDetected, UsageError
 from .host import (PHASE_COPYIN, PHASE_COPYOUT, PHASE_DISPOSE, PHASE_INIT, PHASE_LAUNCH,
                    PHASE_TRIGGER, PHASE_WAIT, PhaseTiming, _check_mask, full_mask)
@@ -219,6 +219,7 @@ class NativeSession:
         shard them, so a new mask for the same descriptor re-stages it.
         """
         t0 = time.perf_counter_ns()
+        work = as_work(work)
         key = mask if work.multi_worker else 0
         if self._staged.get(work.slot) == (work, key) and self.descriptors.get(work.slot) is work:
             return 0   # same descriptor object already staged with this mask
@@ -233,6 +234,7 @@ class NativeSession:
         """Dispatch: one word write per masked worker, no kernel launch."""
         self._require_live()
         _check_mask(mask, self.num_workers)
+        work = as_work(work)
         key = mask if work.multi_worker else 0
         if self._staged.get(work.slot) == (work, key) and self.descriptors.get(work.slot) is work:
             d = None   # this descriptor object is already staged for this worker set
@@ -393,7 +395,7 @@ class LaunchSyncBaseline:
     def launch(self, work: WorkDescriptor, grid: Optional[int] = None) -> PhaseTiming:
         if self._inflight:
             raise UsageError("previous task not yet joined")
-        d = work.to_c()
+        d = as_work(work).to_c()
         g = grid or self.grid
         _lib.check(self._lib.lk_baseline_launch(self._h, C.byref(d), g, C.byref(self._u64)))
         self._inflight = True
@@ -411,7 +413,7 @@ class LaunchSyncBaseline:
         return timing
 
     def bench(self, work: WorkDescriptor, rounds: int, grid: Optional[int] = None):
-        d = work.to_c()
+        d = as_work(work).to_c()
         launch = np.zeros(rounds, dtype=np.uint64)
         total = np.zeros(rounds, dtype=np.uint64)
         _lib.check(self._lib.lk_baseline_bench(self._h, C.byref(d), grid or self.grid, rounds,

@@ -1,0 +1,157 @@
+"""CPU tests of the boundary and host logic (no GPU): the C-ABI library loads
+and exports every symbol include/lk.h declares, struct layouts match the
+header, host helpers behave like persistkern.host, foreign descriptors are
+accepted, and the scenario-backend aggregation matches the reference's."""
+from __future__ import annotations
+
+import ctypes as C
+import re
+import statistics
+from pathlib import Path
+
+import pytest
+
+from paper_2310_01212_b200 import _lib, backend, errors, host, protocol
+from paper_2310_01212_b200.device import WorkDescriptor, as_work
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = (ROOT / "include" / "lk.h").read_text()
+
+
+def declared_functions() -> set[str]:
+    body = re.sub(r"/\*.*?\*/", "", HEADER, flags=re.S)
+    return set(re.findall(r"\b(lk_[a-z0-9_]+)\s*\(", body))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    names = declared_functions()
+    assert len(names) >= 35
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(_lib.SIGNATURES) == names   # the binding covers exactly the header
+
+
+def test_abi_version_and_strerror_without_gpu():
+    lib = _lib.load()
+    assert lib.lk_abi_version() == 1
+    for code in range(0, -11, -1):
+        assert lib.lk_strerror(code)
+    assert lib.lk_strerror(-99) == b"unknown error"
+
+
+def test_struct_sizes_match_header():
+    assert C.sizeof(_lib.lk_desc) == 64
+    assert C.sizeof(_lib.lk_config) == 64
+    assert C.sizeof(_lib.lk_trace_rec) == 32
+    fields = [f for f, _ in _lib.lk_config._fields_]
+    body = re.sub(r"/\*.*?\*/", "", HEADER, flags=re.S)
+    m = re.search(r"typedef struct lk_config \{(.*?)\} lk_config;", body, re.S)
+    hdr = re.findall(r"\b([a-z_]+);", m.group(1))
+    assert fields == hdr
+
+
+def test_error_codes_map_to_reference_exceptions():
+    cases = {_lib.LK_E_USAGE: errors.UsageError, _lib.LK_E_BUSY: errors.BusyTriggerError,
+             _lib.LK_E_DISPOSE_BUSY: errors.DisposeWhileBusyError, _lib.LK_E_HANG: errors.HangDetected,
+             _lib.LK_E_INIT: errors.InitError, _lib.LK_E_CONFIG: errors.ConfigError,
+             _lib.LK_E_PROTOCOL: errors.ProtocolViolation}
+    for rc, exc in cases.items():
+        with pytest.raises(exc):
+            _lib.raise_for(rc)
+    _lib.check(0)
+
+
+def test_no_gpu_create_fails_loudly():
+    """Without a GPU the product refuses to run: no CPU fallback path."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = _lib.lk_config(num_workers=4)
+    h, ns = C.c_void_p(), C.c_uint64()
+    rc = _lib.load().lk_create(C.byref(cfg), C.byref(h), C.byref(ns))
+    assert rc != 0 and not h.value
+
+
+def test_mask_helpers_match_reference_semantics():
+    assert host.full_mask(148) == (1 << 148) - 1
+    assert host.sms_in_mask(0b1011) == [0, 1, 3]
+    assert host.mask_of([0, 1, 3]) == 0b1011
+    with pytest.raises(errors.UsageError):
+        host._check_mask(0, 4)
+    with pytest.raises(errors.UsageError):
+        host._check_mask(1 << 4, 4)
+    assert host._check_mask((1 << 148) - 1, 148) == list(range(148))
+    assert _lib.mask_bytes(1 << 130, 3) == (1 << 130).to_bytes(24, "little")
+
+
+def test_phase_timing_contract():
+    with pytest.raises(ValueError):
+        host.PhaseTiming(host.PHASE_TRIGGER, 5, 0)
+    with pytest.raises(ValueError):
+        host.PhaseTiming(host.PHASE_INIT, -1)
+    csv = host.timings_csv([(0, host.MODEL_LK, host.PhaseTiming(host.PHASE_WAIT, 7, 1))], backend="b200")
+    assert csv.splitlines() == ["run_id,model,phase,sm_mask,cycles,backend", "0,LK,Wait,1,7,b200"]
+
+
+def test_descriptor_validation():
+    with pytest.raises(errors.ConfigError):
+        WorkDescriptor(slot=-1)
+    with pytest.raises(errors.UnsupportedWorkloadError):
+        WorkDescriptor(slot=0, kind="matmul")
+    with pytest.raises(errors.ConfigError):
+        WorkDescriptor(slot=0, kind="busy_loop", data_in_ref=1)
+    with pytest.raises(errors.ConfigError):
+        WorkDescriptor(slot=0, kind="saxpy_f32")
+    d = WorkDescriptor(slot=3, kind="saxpy_f32", data_in_ref=(4096, 8192), data_out_ref=8192,
+                       alpha=2.0, n=1000).to_c()
+    assert (d.kind, d.n, d.in0, d.in1, d.out, d.flags) == (3, 1000, 4096, 8192, 8192, 0)
+    d = WorkDescriptor(slot=3, kind="vector_add_i32", data_in_ref=(4100, 8192), data_out_ref=16,
+                       n=7).to_c()
+    assert d.flags & _lib.DF_SCALAR
+
+
+def test_foreign_descriptor_accepted():
+    class RefWork:   # shape of persistkern.device.WorkDescriptor (P/device.py:48-66)
+        def __init__(self, slot, iterations):
+            self.slot, self.iterations, self.kind = slot, iterations, "busy_loop"
+            self.data_in_ref = self.data_out_ref = None
+    r = RefWork(5, 20_000)
+    w = as_work(r)
+    assert (w.slot, w.iterations, w.kind) == (5, 20_000, "busy_loop")
+    assert as_work(r) is w   # cached: re-triggers stay words-only
+    with pytest.raises(errors.UsageError):
+        as_work(object())
+
+
+def test_reference_descriptor_accepted(reference):
+    from persistkern.device import WorkDescriptor as RefWork
+    w = as_work(RefWork(slot=2, iterations=64))
+    assert w.to_c().iterations == 64 and w.to_c().kind == _lib.KIND_IDS["busy_loop"]
+
+
+def test_backend_aggregate_matches_reference_formula():
+    s = [5, 9, 1, 7]
+    r = backend.aggregate("LK", "Trigger", s)
+    assert (r.avg, r.worst, r.best, r.samples) == (statistics.fmean(s), 9, 1, 4)
+    assert r.stddev == statistics.pstdev(s)
+    assert backend.aggregate("LK", "Init", [3]).stddev == 0.0
+    csv = backend.rows_csv([r])
+    assert csv.splitlines()[1].startswith("LK,Trigger,5.5000,9,1,")
+
+
+def test_backend_aggregate_agrees_with_reference(reference):
+    from persistkern import bench as ref_bench
+    s = [11, 3, 8]
+    mine = backend.aggregate("BASE", "Launch", s)
+    theirs = ref_bench._aggregate("BASE", "Launch", s)
+    assert (mine.avg, mine.worst, mine.best, mine.stddev, mine.samples) == \
+        (theirs.avg, theirs.worst, theirs.best, theirs.stddev, theirs.samples)
+
+
+def test_trace_file_roundtrip():
+    recs = [protocol.TraceRecord(0, "D", 0, protocol.INIT), protocol.TraceRecord(1, "D", 0, protocol.NOP),
+            protocol.TraceRecord(2, "H", 0, 16), protocol.TraceRecord(3, "D", 0, protocol.WORKING)]
+    text = protocol.format_trace(recs)
+    assert protocol.parse_trace(text) == recs
+    assert protocol.validate_trace([(r.side, r.sm_id, r.word) for r in recs]) is None
