@@ -361,6 +361,55 @@ def measure_payload(session, kind, sizes_mib, reps, rotate_bytes):
     return out
 
 
+def measure_interference(session, lat_workers, rounds, stream_mib):
+    """configs[3]: a latency partition (workers [0, lat_workers), closed-loop
+    empty tasks round-robin, driven from C) measured solo, then while the
+    other workers run hbm_stream (src -> dst, stream_mib MiB each) re-triggered
+    back to back by a second host thread.  Same session, disjoint worker sets,
+    so the two host threads never contend for a worker."""
+    from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+    n = session.num_workers
+    lat_masks = [1 << i for i in range(lat_workers)]
+    stream_mask = ((1 << n) - 1) & ~((1 << lat_workers) - 1)
+    elems = (stream_mib << 20) // 4
+    src, dst = DeviceBuffer(4 * elems), DeviceBuffer(4 * elems)
+    sw = WorkDescriptor(slot=900, kind="hbm_stream", data_in_ref=src, data_out_ref=dst, iterations=1)
+    session.register(sw, stream_mask)
+    session.bench_roundtrip(lat_masks, 0, 5000)
+    _, solo, _ = session.bench_roundtrip(lat_masks, 0, rounds)
+
+    stop = threading.Event()
+    stream_stats = {"dispatches": 0, "ns": 0, "spans_ns": []}
+
+    def streamer():
+        t0 = time.perf_counter_ns()
+        while not stop.is_set():
+            session.trigger(stream_mask, sw)
+            session.wait(stream_mask)
+            stream_stats["dispatches"] += 1
+        stream_stats["ns"] = time.perf_counter_ns() - t0
+
+    th = threading.Thread(target=streamer, daemon=True)
+    th.start()
+    while stream_stats["dispatches"] < 2:
+        time.sleep(0.001)
+    _, co, _ = session.bench_roundtrip(lat_masks, 0, rounds)
+    stop.set()
+    th.join()
+    b, e = session.last_spans()
+    span = int(e[lat_workers:].max()) - int(b[lat_workers:].min())
+    src.free()
+    dst.free()
+    moved = 8 * elems * stream_stats["dispatches"]
+    return {"latency_partition_workers": lat_workers, "stream_partition_workers": n - lat_workers,
+            "stream_bytes_per_dispatch": 8 * elems,
+            "solo": lat_summary(solo), "co_running": lat_summary(co),
+            "jitter_delta_us": round((pct(co, 99.9) - pct(co, 50)) / 1e3 - (pct(solo, 99.9) - pct(solo, 50)) / 1e3, 3),
+            "stream_gbs_host": round(moved / max(1, stream_stats["ns"]), 1),
+            "stream_gbs_device_last": round(8 * elems / max(1, span), 1),
+            "stream_dispatches": stream_stats["dispatches"]}
+
+
 def standalone_kernel_gbs(device, kind, mib, reps=20):
     """Same work function as an ordinary kernel (148 CTAs), CUDA-event timed."""
     from paper_2310_01212_b200 import native
@@ -446,6 +495,9 @@ def run_lk_arm(args, world, rank, local):
                                                4 * L2_BYTES)
         payload["block_reduce_f32"] = measure_payload(session, "block_reduce_f32", args.payload_mib,
                                                       args.payload_reps, 4 * L2_BYTES)
+    if not args.no_interference and rank == 0 and n >= args.lat_workers + 8:
+        extras["interference"] = measure_interference(session, args.lat_workers, args.interf_rounds,
+                                                      args.stream_mib)
     smids = session.smid_map
     session.dispose()
     session.close()
@@ -551,6 +603,10 @@ def main():
     ap.add_argument("--payload-reps", type=int, default=30)
     ap.add_argument("--no-payload", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-interference", action="store_true")
+    ap.add_argument("--lat-workers", type=int, default=16, help="latency partition size (configs[3])")
+    ap.add_argument("--interf-rounds", type=int, default=100_000)
+    ap.add_argument("--stream-mib", type=int, default=512, help="hbm_stream src (= dst) MiB")
     ap.add_argument("--cpu-budget-s", type=float, default=30.0)
     ap.add_argument("--ref-rounds", type=int, default=8, help="reference arm round trips per step")
     args = ap.parse_args()

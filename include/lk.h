@@ -105,9 +105,16 @@ typedef struct lk_config {
   uint64_t wait_timeout_ns;      /* wait_timeout_s (native.py:52) */
   uint32_t flags;                /* LK_CF_* */
   uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 4 */
-  uint32_t poll_spacing_ns;      /* stagger between replica loads; 0 = 200 */
-  uint32_t reserved;
+  uint32_t poll_spacing_ns;      /* stagger between replica loads / sweeps; 0 = 300 */
+  uint32_t poll_mode;            /* LK_POLL_GATEWAY (0, default) or LK_POLL_DIRECT */
 } lk_config;
+
+/* How to_gpu words reach the workers.  GATEWAY: one warp polls a dense host
+ * doorbell array for every worker and forwards new values to per-worker
+ * mailboxes in device memory (few PCIe reads in flight).  DIRECT: every
+ * worker polls its own host cell replicas over PCIe. */
+#define LK_POLL_GATEWAY 0u
+#define LK_POLL_DIRECT  1u
 
 #define LK_CF_ACQUIRE_POLL   1u  /* poll with ld.acquire.sys instead of ld.relaxed.sys */
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
@@ -221,6 +228,9 @@ int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks,
 /* Device-side spans of the last dispatch per worker (globaltimer ns):
  * begin (WORK observed) and end (work done, before FINISHED). */
 int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n);
+/* Device timeline of the last dispatch per worker, 4 globaltimer stamps each
+ * (t[4*i+0..3]): to_gpu value seen, work begin, work end, FINISHED issued. */
+int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n);
 
 /* Raw host<->GPU ping-pong floor: one thread polls a mapped host word and
  * echoes it back; rounds samples of the round trip. */

@@ -38,6 +38,8 @@ KIND_IDS = {
 DF_SCALAR = 1
 CF_ACQUIRE_POLL = 1
 CF_FENCE_ALWAYS = 2
+POLL_GATEWAY = 0
+POLL_DIRECT = 1
 
 WERR_NAMES = {
     0: "none",
@@ -82,7 +84,7 @@ class lk_config(C.Structure):
         ("flags", C.c_uint32),
         ("poll_replicas", C.c_uint32),
         ("poll_spacing_ns", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("poll_mode", C.c_uint32),
     ]
 
 
@@ -132,6 +134,7 @@ SIGNATURES = {
     "lk_validate_trace": (I32, [P, P, P, U64, PI64, C.c_char_p, U32, PU64, U32, PU32]),
     "lk_bench_roundtrip": (I32, [P, MASK, U32, U32, U32, U64, P, P, P]),
     "lk_last_spans": (I32, [P, P, P, U32]),
+    "lk_last_timeline": (I32, [P, P, U32]),
     "lk_pingpong": (I32, [I32, U64, P]),
     "lk_baseline_create": (I32, [I32, U32, C.POINTER(P)]),
     "lk_baseline_launch": (I32, [P, C.POINTER(lk_desc), U32, PU64]),

@@ -23,7 +23,6 @@
 #include <atomic>
 #include <mutex>
 #include <string>
-#include <unordered_map>
 #include <vector>
 
 #if defined(__x86_64__)
@@ -118,7 +117,10 @@ struct lk_session {
 
   // pinned mapped host block
   uint8_t* host_block = nullptr;
-  unsigned long long* to_gpu = nullptr;       // worker i replica k at [(i*replicas+k)*cell_u64]
+  unsigned long long* to_gpu = nullptr;       // DIRECT: worker i replica k at [(i*replicas+k)*cell_u64]
+  unsigned long long* bell = nullptr;         // GATEWAY: replica k, worker i at [k*bell_stride + i]
+  uint32_t bell_stride = 0;
+  bool gateway = true;
   volatile unsigned long long* status = nullptr;  // stride cell_u64
   volatile unsigned long long* err = nullptr;
   volatile uint32_t* smid = nullptr;
@@ -130,13 +132,20 @@ struct lk_session {
   unsigned long long* d_mask = nullptr;
   uint32_t* d_ctr = nullptr;
   unsigned long long* d_spans = nullptr;
+  unsigned long long* d_dmb = nullptr;
+  uint32_t* d_exited = nullptr;
   lk_dev_trace* d_trace = nullptr;
   uint32_t* d_tcnt = nullptr;
 
   // host bookkeeping (guarded by mu)
   std::mutex mu;
   std::vector<uint64_t> pending;                          // nwords
-  std::unordered_map<uint32_t, std::vector<uint64_t>> pending_by_slot;
+  // pending_by_slot (native.py:97): per-slot worker masks of un-waited
+  // dispatches, flat (num_slots * nwords), plus the list of slots in flight.
+  std::vector<uint64_t> slot_pend;
+  std::vector<uint8_t> slot_busy;
+  std::vector<uint32_t> inflight;
+  std::vector<uint64_t> scratch;                          // nwords, under mu
   std::vector<uint8_t> registered;                        // per slot
   std::vector<lk_desc> reg_desc;                          // host copy per slot
   std::vector<std::vector<uint64_t>> reg_mask;            // per slot (nwords)
@@ -153,15 +162,22 @@ struct lk_session {
 
   inline uint32_t word(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64]); }
   inline uint32_t phase(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64] >> 32); }
-  // One logical to_gpu write: {word, seq} into every replica line.
+  // One logical to_gpu write: {word, seq} into every replica (seq = this
+  // worker's host write index; the device acts only on newer seqs, so the
+  // replicas, written one after another, can never step it backwards).
   inline void host_write(uint32_t i, uint32_t w) {
     const uint32_t sq = ++host_seq[i];
     if (cfg.record_trace) host_log[i].push_back(HostRec{sq, w, now_ns()});
     const unsigned long long v = uint64_t(w) | (uint64_t(sq) << 32);
+    if (gateway) {
+      for (uint32_t k = 0; k < replicas; ++k) __atomic_store_n(bell + uint64_t(k) * bell_stride + i, v, __ATOMIC_RELEASE);
+      return;
+    }
     unsigned long long* c = to_gpu + uint64_t(i) * replicas * cell_u64;
     for (uint32_t k = 0; k < replicas; ++k) __atomic_store_n(c + k * cell_u64, v, __ATOMIC_RELEASE);
   }
   inline uint32_t to_gpu_word(uint32_t i) const {
+    if (gateway) return uint32_t(__atomic_load_n(bell + i, __ATOMIC_ACQUIRE));
     return uint32_t(__atomic_load_n(to_gpu + uint64_t(i) * replicas * cell_u64, __ATOMIC_ACQUIRE));
   }
 };
@@ -282,13 +298,16 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.cell_stride != 8 && cfg.cell_stride != 16 && cfg.cell_stride != 32 && cfg.cell_stride != 64 &&
       cfg.cell_stride != 128)
     return fail(LK_E_CONFIG, "cell_stride must be 8, 16, 32, 64 or 128");
-  if (cfg.poll_replicas == 0) cfg.poll_replicas = 4;
+  if (cfg.poll_mode > LK_POLL_DIRECT) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
+  if (cfg.poll_replicas == 0) cfg.poll_replicas = cfg.poll_mode == LK_POLL_GATEWAY ? 2 : 1;
   if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)
     return fail(LK_E_CONFIG, "poll_replicas must be 1, 2, 4 or 8");
-  if (cfg.poll_spacing_ns == 0) cfg.poll_spacing_ns = 200;
+  if (cfg.poll_mode == LK_POLL_GATEWAY && cfg.poll_replicas == 8)
+    return fail(LK_E_CONFIG, "gateway mode takes 1, 2 or 4 doorbell replicas");
+  if (cfg.poll_spacing_ns == 0) cfg.poll_spacing_ns = 300;
   if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 512;
-  if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 1024)
-    return fail(LK_E_CONFIG, "threads_per_worker must be a multiple of 32 and <= 1024");
+  if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 608)
+    return fail(LK_E_CONFIG, "threads_per_worker must be a multiple of 32 and <= 608");
   if (cfg.num_slots == 0) cfg.num_slots = 1024;
   if (cfg.trace_capacity == 0) cfg.trace_capacity = 65536;
   if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
@@ -314,8 +333,14 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->device = cfg.device;
   s->cell_u64 = cfg.cell_stride / 8;
   s->replicas = cfg.poll_replicas;
+  s->gateway = cfg.poll_mode == LK_POLL_GATEWAY;
+  s->bell_stride = (s->nw + 63) / 64 * 64;
   s->pending.assign(s->nwords, 0);
   s->registered.assign(cfg.num_slots, 0);
+  s->slot_pend.assign(size_t(cfg.num_slots) * s->nwords, 0);
+  s->slot_busy.assign(cfg.num_slots, 0);
+  s->inflight.reserve(64);
+  s->scratch.assign(s->nwords, 0);
   s->reg_desc.resize(cfg.num_slots);
   s->reg_mask.resize(cfg.num_slots);
   s->host_seq.assign(s->nw, 0);
@@ -331,9 +356,11 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     return rc;
   };
 
-  // --- pinned mapped mailboxes: to_gpu replicas | status | err | smid, 4 KiB aligned
+  // --- pinned mapped mailboxes: to_gpu (DIRECT replicas | GATEWAY doorbell
+  // replicas) | status | err | smid, 4 KiB aligned
   auto al = [](size_t x) { return (x + 4095) & ~size_t(4095); };
-  const size_t tob = al(size_t(s->nw) * s->replicas * cfg.cell_stride);
+  const size_t tob = s->gateway ? al(size_t(s->replicas) * s->bell_stride * 8)
+                                : al(size_t(s->nw) * s->replicas * cfg.cell_stride);
   const size_t cells = al(size_t(s->nw) * cfg.cell_stride);
   const size_t errb = al(size_t(s->nw) * 8), smidb = al(size_t(s->nw) * 4);
   const size_t host_bytes = tob + cells + errb + smidb;
@@ -342,24 +369,29 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(ce)));
   memset(s->host_block, 0, host_bytes);
   s->to_gpu = reinterpret_cast<unsigned long long*>(s->host_block);
+  s->bell = s->to_gpu;
   s->status = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob);
   s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob + cells);
   s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + tob + cells + errb);
   for (uint32_t i = 0; i < s->nw; ++i) {
-    for (uint32_t k = 0; k < s->replicas; ++k)
-      s->to_gpu[(uint64_t(i) * s->replicas + k) * s->cell_u64] = LK_NOP;  // {NOP, seq 0}
+    for (uint32_t k = 0; k < s->replicas; ++k) {
+      if (s->gateway) s->bell[uint64_t(k) * s->bell_stride + i] = LK_NOP;   // {NOP, seq 0}
+      else s->to_gpu[(uint64_t(i) * s->replicas + k) * s->cell_u64] = LK_NOP;
+    }
     s->status[uint64_t(i) * s->cell_u64] = uint64_t(LK_NOP) | (uint64_t(LK_PHASE_BOOTING) << 32);
     s->smid[i] = 0xFFFFFFFFu;
   }
 
-  // --- device block: desc | masks | ctr | spans | trace | tcnt
+  // --- device block: desc | masks | ctr | spans | dmb | exited | trace | tcnt
   const size_t descb = al(size_t(cfg.num_slots) * sizeof(lk_desc));
   const size_t maskb = al(size_t(cfg.num_slots) * s->nwords * 8);
   const size_t ctrb = al(size_t(cfg.num_slots) * 4);
-  const size_t spanb = al(size_t(s->nw) * 16);
+  const size_t spanb = al(size_t(s->nw) * 32);
+  const size_t dmbb = al(size_t(s->nw) * 128);
+  const size_t exb = al(4);
   const size_t traceb = cfg.record_trace ? al(size_t(s->nw) * cfg.trace_capacity * sizeof(lk_dev_trace)) : 0;
   const size_t tcntb = al(size_t(s->nw) * 4);
-  const size_t dev_bytes = descb + maskb + ctrb + spanb + traceb + tcntb;
+  const size_t dev_bytes = descb + maskb + ctrb + spanb + dmbb + exb + traceb + tcntb;
   ce = dev_alloc(reinterpret_cast<void**>(&s->dev_block), dev_bytes);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "device alloc: %s", cudaGetErrorString(ce)));
   ce = cudaMemsetAsync(s->dev_block, 0, dev_bytes, svc_stream());
@@ -370,6 +402,8 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->d_mask = reinterpret_cast<unsigned long long*>(p); p += maskb;
   s->d_ctr = reinterpret_cast<uint32_t*>(p); p += ctrb;
   s->d_spans = reinterpret_cast<unsigned long long*>(p); p += spanb;
+  s->d_dmb = reinterpret_cast<unsigned long long*>(p); p += dmbb;
+  s->d_exited = reinterpret_cast<uint32_t*>(p); p += exb;
   s->d_trace = traceb ? reinterpret_cast<lk_dev_trace*>(p) : nullptr; p += traceb;
   s->d_tcnt = reinterpret_cast<uint32_t*>(p);
 
@@ -381,10 +415,13 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   // --- one CTA per SM: dynamic smem above half the SM's capacity
   s->smem = size_t(prop.sharedMemPerMultiprocessor) / 2 + 8192;
   if (s->smem > size_t(prop.sharedMemPerBlockOptin) - 1024) s->smem = size_t(prop.sharedMemPerBlockOptin) - 1024;
+  ce = lk_preload_kernels();
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "kernel load: %s", cudaGetErrorString(ce)));
   ce = lk_persistent_configure(s->smem);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "smem attr: %s", cudaGetErrorString(ce)));
   int bps = 0;
-  ce = lk_persistent_occupancy(s->threads, s->smem, &bps);
+  const uint32_t launch_threads = s->threads + 32;   // + the gateway warp (CTA 0; retires elsewhere)
+  ce = lk_persistent_occupancy(launch_threads, s->smem, &bps);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "occupancy: %s", cudaGetErrorString(ce)));
   if (bps != 1) return cleanup(fail(LK_E_INIT, "expected exactly 1 resident worker per SM, got %d", bps));
 
@@ -409,7 +446,15 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.record_trace = cfg.record_trace ? 1 : 0;
   a.backoff_ns = cfg.poll_backoff_ns;
   a.flags = cfg.flags;
-  ce = lk_launch_persistent(a, s->nw, s->threads, s->smem, s->stream);
+  a.bell = s->bell;
+  a.dmb = s->d_dmb;
+  a.exited = s->d_exited;
+  a.bell_stride = s->bell_stride;
+  a.dmb_u64 = 16;
+  a.nw = s->nw;
+  a.wthreads = s->threads;
+  a.poll_mode = cfg.poll_mode;
+  ce = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(ce)));
 
   // --- boot: every worker publishes INIT then NOP (native.py:113-118)
@@ -442,7 +487,7 @@ extern "C" int lk_register_desc(lk_session* s, uint32_t slot, const lk_desc* d, 
     return fail(LK_E_USAGE, "slot %u outside the %u-entry descriptor table", slot, s->cfg.num_slots);
   if (d->kind >= LK_KIND_COUNT) return fail(LK_E_USAGE, "unknown work kind %u", d->kind);
   std::lock_guard<std::mutex> g(s->mu);
-  if (s->pending_by_slot.count(slot))
+  if (s->slot_busy[slot])
     return fail(LK_E_USAGE, "descriptor slot %u still referenced by an un-waited dispatch", slot);
   return stage_locked(s, slot, d, mask, nwords);
 }
@@ -482,7 +527,7 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   for (uint32_t i : ids)
     if (s->pending[i >> 6] >> (i & 63) & 1) busy.push_back(i);
   if (!busy.empty()) return fail(LK_E_BUSY, "worker(s) %s still busy", ids_str(busy).c_str());
-  if (s->pending_by_slot.count(slot))
+  if (slot < s->cfg.num_slots && s->slot_busy[slot])
     return fail(LK_E_USAGE, "descriptor slot %u still referenced by an un-waited dispatch", slot);
   if (slot >= s->cfg.num_slots)
     return fail(LK_E_USAGE, "slot %u outside the %u-entry descriptor table", slot, s->cfg.num_slots);
@@ -501,12 +546,13 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   const uint32_t word = LK_WORK_BASE + slot;
   for (uint32_t i : ids) s->host_write(i, word);
   const uint64_t t1 = now_ns();
-  std::vector<uint64_t> m(s->nwords, 0);
+  uint64_t* sp = s->slot_pend.data() + uint64_t(slot) * s->nwords;
   for (uint32_t i : ids) {
     s->pending[i >> 6] |= 1ull << (i & 63);
-    m[i >> 6] |= 1ull << (i & 63);
+    sp[i >> 6] |= 1ull << (i & 63);
   }
-  s->pending_by_slot[slot] = std::move(m);
+  s->slot_busy[slot] = 1;
+  s->inflight.push_back(slot);
   if (elapsed_ns) *elapsed_ns = t1 - t0;
   return LK_OK;
 }
@@ -515,7 +561,7 @@ extern "C" int lk_trigger(lk_session* s, const uint64_t* mask, uint32_t nwords, 
                           const lk_desc* d, uint64_t* elapsed_ns) {
   if (!s || !mask) return fail(LK_E_USAGE, "null argument");
   std::lock_guard<std::mutex> g(s->mu);
-  std::vector<uint32_t> ids;
+  static thread_local std::vector<uint32_t> ids;
   return trigger_locked(s, mask, nwords, slot, d, ids, elapsed_ns);
 }
 
@@ -538,16 +584,26 @@ static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::
   if (rc) return rc;
   {
     std::lock_guard<std::mutex> g(s->mu);
-    std::vector<uint64_t> m(s->nwords, 0);
+    std::vector<uint64_t>& m = s->scratch;
+    std::fill(m.begin(), m.end(), 0);
     for (uint32_t i : ids) m[i >> 6] |= 1ull << (i & 63);
     for (uint32_t k = 0; k < s->nwords; ++k) s->pending[k] &= ~m[k];
-    for (auto it = s->pending_by_slot.begin(); it != s->pending_by_slot.end();) {
+    // a slot is freed only once every worker it was triggered on was waited (native.py:266-272)
+    for (size_t j = 0; j < s->inflight.size();) {
+      const uint32_t slot = s->inflight[j];
+      uint64_t* sp = s->slot_pend.data() + uint64_t(slot) * s->nwords;
       bool any = false;
       for (uint32_t k = 0; k < s->nwords; ++k) {
-        it->second[k] &= ~m[k];
-        any |= it->second[k] != 0;
+        sp[k] &= ~m[k];
+        any |= sp[k] != 0;
       }
-      if (any) ++it; else it = s->pending_by_slot.erase(it);
+      if (any) {
+        ++j;
+      } else {
+        s->slot_busy[slot] = 0;
+        s->inflight[j] = s->inflight.back();
+        s->inflight.pop_back();
+      }
     }
   }
   if (finished_ns) *finished_ns = finished_at - t0;
@@ -557,7 +613,7 @@ static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::
 
 extern "C" int lk_wait(lk_session* s, const uint64_t* mask, uint32_t nwords, uint64_t* finished_ns) {
   if (!s || !mask) return fail(LK_E_USAGE, "null argument");
-  std::vector<uint32_t> ids;
+  static thread_local std::vector<uint32_t> ids;
   return wait_impl(s, mask, nwords, ids, finished_ns, 0, nullptr);
 }
 
@@ -706,14 +762,22 @@ extern "C" int lk_kernel_alive(lk_session* s, uint32_t* alive) {
   return LK_OK;
 }
 
+extern "C" int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n) {
+  if (!s || !t) return fail(LK_E_USAGE, "null argument");
+  const uint32_t m = std::min(n, s->nw);
+  LK_CUDA(cudaMemcpyAsync(t, s->d_spans, size_t(m) * 32, cudaMemcpyDeviceToHost, s->copy_stream));
+  LK_CUDA(cudaStreamSynchronize(s->copy_stream));
+  return LK_OK;
+}
+
 extern "C" int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n) {
   if (!s) return fail(LK_E_USAGE, "null session");
-  std::vector<unsigned long long> sp(2 * size_t(s->nw));
-  LK_CUDA(cudaMemcpyAsync(sp.data(), s->d_spans, sp.size() * 8, cudaMemcpyDeviceToHost, s->copy_stream));
-  LK_CUDA(cudaStreamSynchronize(s->copy_stream));
+  std::vector<uint64_t> sp(4 * size_t(s->nw));
+  int rc = lk_last_timeline(s, sp.data(), s->nw);
+  if (rc) return rc;
   for (uint32_t i = 0; i < std::min(n, s->nw); ++i) {
-    if (begin_ns) begin_ns[i] = sp[2 * i];
-    if (end_ns) end_ns[i] = sp[2 * i + 1];
+    if (begin_ns) begin_ns[i] = sp[4 * i + 1];
+    if (end_ns) end_ns[i] = sp[4 * i + 2];
   }
   return LK_OK;
 }

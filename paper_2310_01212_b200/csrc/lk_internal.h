@@ -24,7 +24,17 @@ struct lk_dev_args {
   const lk_desc* desc;             // device, num_slots entries
   const unsigned long long* slot_mask;  // device, num_slots * nwords
   uint32_t* reduce_ctr;            // device, num_slots
-  unsigned long long* spans;       // device, 2 per worker: begin, end (globaltimer)
+  unsigned long long* spans;       // device, 4 per worker (globaltimer): value seen, work begin,
+                                   // work end, FINISHED issued -- of the last dispatch
+  const unsigned long long* bell;  // host-mapped doorbell (GATEWAY): replica k, worker i at
+                                   // bell[k*bell_stride + i] = word | seq<<32
+  unsigned long long* dmb;         // device mailboxes (GATEWAY), worker i at dmb[i*dmb_u64]
+  uint32_t* exited;                // device: workers that left their loop
+  uint32_t bell_stride;            // cells per doorbell replica (multiple of 64)
+  uint32_t dmb_u64;
+  uint32_t nw;                     // workers
+  uint32_t wthreads;               // worker threads per CTA (the gateway warp comes after)
+  uint32_t poll_mode;              // LK_POLL_*
   lk_dev_trace* trace;             // device, num_workers * trace_cap
   uint32_t* trace_cnt;             // device, num_workers
   uint32_t cell_u64;               // cell stride in u64 (to_gpu replicas and status)
@@ -42,6 +52,7 @@ struct lk_dev_args {
 cudaError_t lk_launch_persistent(const lk_dev_args& a, uint32_t grid, uint32_t threads,
                                  size_t smem, cudaStream_t st);
 cudaError_t lk_persistent_configure(size_t smem);
+cudaError_t lk_preload_kernels();
 cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_per_sm);
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads,
                            uint32_t* reduce_ctr, cudaStream_t st);

@@ -2,11 +2,19 @@
 //
 //  * lk_persistent_kernel: one CTA per SM for the whole session (the paper's
 //    persistent worker; reference loop native.py:149-199).
-//    Thread 0 of each CTA is the elected poller: it spins on its to_gpu cell
-//    in pinned host memory (ld.*.sys over PCIe), runs the shared state machine
-//    (lk_protocol.cuh) and publishes its from_gpu/status cell with sys-scope
-//    stores.  The other threads park on a CTA barrier (no issue slots used)
+//    Thread 0 of each CTA is the elected worker thread: it runs the shared
+//    state machine (lk_protocol.cuh) on every new to_gpu value and publishes
+//    its from_gpu/status cell in pinned host memory with sys-scope stores.
+//    The other worker threads park on a named barrier (no issue slots used)
 //    and only wake for payload work items.
+//    How to_gpu values reach thread 0 (lk_config.poll_mode):
+//     - GATEWAY (default): one extra warp in CTA 0 polls the dense host
+//       doorbell array (all workers' to_gpu cells, K staggered replica sweeps
+//       in flight, ~10 PCIe line reads per sweep) and forwards each new value
+//       to the worker's mailbox line in device memory; workers poll L2.  The
+//       PCIe link sees tens of outstanding reads instead of 148 x K, and no
+//       worker thread ever holds an in-flight PCIe load.
+//     - DIRECT: every worker polls its own host cell replicas over PCIe.
 //  * lk_work_kernel: the same work functions as an ordinary kernel, for the
 //    cudaLaunchKernel+cudaStreamSynchronize baseline (ThreadSpawnBaseline
 //    analogue, native.py:304-331).
@@ -24,6 +32,9 @@
 namespace {
 
 constexpr uint32_t kMaxThreads = 1024;
+// Persistent CTA: up to 608 worker threads + the gateway warp; the bound
+// leaves ~96 registers per thread for the gateway's in-flight sweeps.
+constexpr uint32_t kPersistMaxThreads = 640;
 constexpr uint32_t kCmdWork = 1;
 constexpr uint32_t kCmdExit = 2;
 
@@ -57,6 +68,27 @@ __device__ __forceinline__ uint32_t smid() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
   return s;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_relaxed_sys_v2(const unsigned long long* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+// Named barrier 1 over the T worker threads of the CTA (the gateway warp of
+// CTA 0 never joins it).
+__device__ __forceinline__ void wsync(uint32_t T) { asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory"); }
 __device__ __forceinline__ uint4 ld_cg4(const uint4* p) {
   uint4 v;
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -108,8 +140,8 @@ __device__ __forceinline__ uint4 vop(const Op& op, uint4 x, uint4 y) {
 
 // out[i] = op(in0[i], in1[i]) over [p.b, p.e), all threads of the CTA.
 template <int U, bool kTwo, class Op>
-__device__ __forceinline__ void map_chunk(const lk_desc& d, Part p, const Op& op) {
-  const uint32_t T = blockDim.x, t = threadIdx.x;
+__device__ __forceinline__ void map_chunk(const lk_desc& d, Part p, const Op& op, uint32_t T) {
+  const uint32_t t = threadIdx.x;
   const uint32_t* a = reinterpret_cast<const uint32_t*>(d.in0);
   const uint32_t* c = reinterpret_cast<const uint32_t*>(d.in1);
   uint32_t* o = reinterpret_cast<uint32_t*>(d.out);
@@ -157,8 +189,8 @@ struct ReduceSmem {
 // fp64 into *(double*)aux.
 template <int U>
 __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t rank, uint32_t count,
-                                             uint32_t* ctr, ReduceSmem& sm) {
-  const uint32_t T = blockDim.x, t = threadIdx.x;
+                                             uint32_t* ctr, ReduceSmem& sm, uint32_t T) {
+  const uint32_t t = threadIdx.x;
   const float* x = reinterpret_cast<const float*>(d.in0);
   float acc = 0.f;
   if (d.flags & LK_DF_SCALAR) {
@@ -189,7 +221,7 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
   acc = warp_sum(acc);
   const uint32_t warp = t >> 5, lane = t & 31, nwarps = (T + 31) >> 5;
   if (lane == 0) sm.part[warp] = acc;
-  __syncthreads();
+  wsync(T);
   if (warp == 0) {
     float v = lane < nwarps ? sm.part[lane] : 0.f;
     v = warp_sum(v);
@@ -203,7 +235,7 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
       sm.last = last;
     }
   }
-  __syncthreads();
+  wsync(T);
   if (sm.last && warp == 0) {
     __threadfence();
     const uint32_t* partials = reinterpret_cast<const uint32_t*>(d.out);
@@ -227,17 +259,17 @@ __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
 
 // Payload work shared by both kernels; every thread of the CTA calls it.
 __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
-                                          uint32_t* ctr, ReduceSmem& rs) {
+                                          uint32_t* ctr, ReduceSmem& rs, uint32_t T) {
   const Part p = partition(d.n, rank, count);
   switch (d.kind) {
-    case LK_KIND_VECTOR_ADD_I32: map_chunk<4, true>(d, p, OpAddI32{}); break;
-    case LK_KIND_SAXPY_F32: map_chunk<4, true>(d, p, OpSaxpy{d.alpha}); break;
+    case LK_KIND_VECTOR_ADD_I32: map_chunk<4, true>(d, p, OpAddI32{}, T); break;
+    case LK_KIND_SAXPY_F32: map_chunk<4, true>(d, p, OpSaxpy{d.alpha}, T); break;
     case LK_KIND_HBM_STREAM: {
       const uint64_t passes = d.iterations ? d.iterations : 1;
-      for (uint64_t k = 0; k < passes; ++k) map_chunk<8, false>(d, p, OpCopy{});
+      for (uint64_t k = 0; k < passes; ++k) map_chunk<8, false>(d, p, OpCopy{}, T);
       break;
     }
-    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs); break;
+    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs, T); break;
     default: break;
   }
 }
@@ -250,6 +282,7 @@ struct Elected {           // thread 0's private protocol state
   uint32_t cur;            // current to_gpu word
   uint32_t tcnt;
   bool dirty;              // cur not yet stepped to a fixed point
+  uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
 };
 
 __device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t word,
@@ -335,6 +368,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
           e.seq = uint32_t(c >> 32);
           e.cur = uint32_t(c);
           e.dirty = true;
+          e.t_seen = globaltimer();
           fresh = true;
           break;
         }
@@ -347,12 +381,105 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
   }
 }
 
+// GATEWAY mode: the worker's to_gpu value arrives in its device mailbox line
+// (written by the gateway warp); poll it in L2, one load in flight.
+__device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  const unsigned long long* mb = a.dmb + uint64_t(wid) * a.dmb_u64;
+  for (;;) {
+    const uint32_t act = settle(a, wid, e);
+    if (act != LK_ACT_NONE) return act;
+    for (;;) {
+      const unsigned long long c = ld_relaxed_gpu64(mb);
+      if (uint32_t(c >> 32) > e.seq) {
+        e.seq = uint32_t(c >> 32);
+        e.cur = uint32_t(c);
+        e.dirty = true;
+        e.t_seen = globaltimer();
+        break;
+      }
+      if (a.backoff_ns) __nanosleep(a.backoff_ns);
+    }
+  }
+}
+
 __device__ __noinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  if (a.poll_mode == LK_POLL_GATEWAY) return poll_mailbox(a, wid, e);
   switch (a.replicas) {
     case 1: return poll_k<1>(a, wid, e);
     case 2: return poll_k<2>(a, wid, e);
     case 8: return poll_k<8>(a, wid, e);
     default: return poll_k<4>(a, wid, e);
+  }
+}
+
+// ---------------------------------------------------------------- gateway
+// One warp samples every worker's to_gpu cell in the dense host doorbell
+// array: lane l covers cells {64j + 2l, 64j + 2l + 1} (16-B loads, j < J <= 4,
+// so up to 256 workers), K replica arrays swept one after another, spaced
+// spacing_ns, one sweep per replica in flight.  A cell whose seq is newer
+// than the last forwarded one is copied to the worker's mailbox line in
+// device memory (relaxed: the descriptor a WORK word names was staged by a
+// completed DMA before the host wrote the word).  Exits once every worker
+// has left its loop.
+template <int K, int J>
+__device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = a.nw;
+  uint32_t last[2 * J];
+#pragma unroll
+  for (int i = 0; i < 2 * J; ++i) last[i] = 0;
+  ulonglong2 v[K][J];
+  auto cell = [&](int j) { return uint32_t(64 * j) + 2 * lane; };
+  auto issue = [&](int k) {
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (cell(j) < nw) v[k][j] = ld_relaxed_sys_v2(a.bell + uint64_t(k) * a.bell_stride + cell(j));
+  };
+  auto fwd = [&](uint32_t c, unsigned long long val, uint32_t& seen) {
+    const uint32_t sq = uint32_t(val >> 32);
+    if (c < nw && sq > seen) {
+      seen = sq;
+      st_relaxed_gpu64(a.dmb + uint64_t(c) * a.dmb_u64, val);
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    issue(k);
+    if (K > 1) __nanosleep(a.spacing_ns);
+  }
+  for (uint32_t it = 0;; ++it) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (cell(j) < nw) {
+          fwd(cell(j), v[k][j].x, last[2 * j]);
+          fwd(cell(j) + 1, v[k][j].y, last[2 * j + 1]);
+        }
+      }
+      issue(k);
+      if (K > 1) __nanosleep(a.spacing_ns);
+      else if (a.backoff_ns) __nanosleep(a.backoff_ns);
+    }
+    if ((it & 31u) == 0 && ld_relaxed_gpu32(a.exited) >= nw) return;
+  }
+}
+
+template <int J>
+__device__ __forceinline__ void gateway_j(const lk_dev_args& a) {
+  switch (a.replicas) {
+    case 1: gateway_k<1, J>(a); return;
+    case 4: gateway_k<4, J>(a); return;
+    default: gateway_k<2, J>(a); return;
+  }
+}
+
+__device__ __noinline__ void gateway(const lk_dev_args& a) {
+  switch ((a.nw + 63) / 64) {
+    case 1: gateway_j<1>(a); return;
+    case 2: gateway_j<2>(a); return;
+    case 3: gateway_j<3>(a); return;
+    default: gateway_j<4>(a); return;
   }
 }
 
@@ -362,9 +489,14 @@ struct PersistSmem {
   ReduceSmem red;
 };
 
-__global__ void __launch_bounds__(kMaxThreads, 1) lk_persistent_kernel(const lk_dev_args a) {
+__global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const lk_dev_args a) {
   __shared__ PersistSmem sm;
   const uint32_t wid = blockIdx.x;
+  const uint32_t T = a.wthreads;
+  if (threadIdx.x >= T) {           // the extra warp: CTA 0 hosts the gateway, the rest retire
+    if (wid == 0 && a.poll_mode == LK_POLL_GATEWAY) gateway(a);
+    return;
+  }
   Elected e;
   e.st = lk_wstate{LK_PHASE_BOOTING, 0};
   e.pub = LK_NOP;  // cells start at the NOP sentinel (protocol.py:217-218)
@@ -372,6 +504,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) lk_persistent_kernel(const lk_
   e.cur = LK_NOP;
   e.tcnt = 0;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
+  e.t_seen = 0;
   uint64_t t_begin = 0;
   if (threadIdx.x == 0) st_relaxed_sys_u32(a.smid + wid, smid());
 
@@ -380,7 +513,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) lk_persistent_kernel(const lk_
       for (;;) {
         const uint32_t act = poll(a, wid, e);
         if (act == LK_ACT_EXIT) { sm.cmd = kCmdExit; break; }
-        t_begin = globaltimer();
         const uint32_t slot = e.st.slot;
         if (slot >= a.num_slots) { report_error(a, wid, e, LK_WERR_BAD_SLOT, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
         lk_desc d;
@@ -392,11 +524,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) lk_persistent_kernel(const lk_
         }
         if (d.kind >= LK_KIND_COUNT) { report_error(a, wid, e, LK_WERR_BAD_KIND, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
         if (single_thread_kind(d.kind)) {
+          t_begin = globaltimer();
           if (d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
-          a.spans[2 * wid] = t_begin;
-          a.spans[2 * wid + 1] = globaltimer();
+          const uint64_t t_end = globaltimer();
           const lk_step_out o = lk_complete_work(e.st);
           publish(a, wid, e, o.publish, (a.flags & LK_CF_FENCE_ALWAYS) != 0);
+          unsigned long long* tl = a.spans + 4ull * wid;
+          tl[0] = e.t_seen; tl[1] = t_begin; tl[2] = t_end; tl[3] = globaltimer();
           continue;
         }
         // payload item: rank/count from the slot's trigger mask
@@ -414,21 +548,24 @@ __global__ void __launch_bounds__(kMaxThreads, 1) lk_persistent_kernel(const lk_
         sm.count = count ? count : 1;
         sm.slot = slot;
         sm.cmd = kCmdWork;
+        t_begin = globaltimer();
         break;
       }
     }
-    __syncthreads();
-    if (sm.cmd == kCmdExit) return;
+    wsync(T);
+    if (sm.cmd == kCmdExit) break;
     const lk_desc d = sm.desc;
-    run_multi(d, sm.rank, sm.count, a.reduce_ctr + sm.slot, sm.red);
-    __syncthreads();
+    run_multi(d, sm.rank, sm.count, a.reduce_ctr + sm.slot, sm.red, T);
+    wsync(T);
     if (threadIdx.x == 0) {
-      a.spans[2 * wid] = t_begin;
-      a.spans[2 * wid + 1] = globaltimer();
+      const uint64_t t_end = globaltimer();
       const lk_step_out o = lk_complete_work(e.st);
       publish(a, wid, e, o.publish, true);  // payload visible before FINISHED
+      unsigned long long* tl = a.spans + 4ull * wid;
+      tl[0] = e.t_seen; tl[1] = t_begin; tl[2] = t_end; tl[3] = globaltimer();
     }
   }
+  if (threadIdx.x == 0) atomicAdd(a.exited, 1u);   // lets the gateway retire
 }
 
 // ---------------------------------------------------------------- baseline
@@ -438,7 +575,7 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
     if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
     return;
   }
-  run_multi(d, blockIdx.x, gridDim.x, ctr, rs);
+  run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x);
 }
 
 // ---------------------------------------------------------------- ping-pong
@@ -452,6 +589,17 @@ __global__ void lk_pingpong_kernel(volatile uint32_t* flag, volatile uint32_t* e
 }
 
 }  // namespace
+
+// CUDA 12 loads kernels lazily on first launch, and loading a module while a
+// spinning kernel is resident can wait on it forever.  Load every kernel of
+// this library before the persistent kernel launches.
+cudaError_t lk_preload_kernels() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, lk_work_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_pingpong_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_persistent_kernel);
+  return e;
+}
 
 cudaError_t lk_persistent_configure(size_t smem) {
   return cudaFuncSetAttribute(lk_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -34,6 +34,7 @@ log = logging.getLogger(__name__)
 PURE_SPIN = "pure_spin"
 SPIN_THEN_YIELD = "spin_then_yield"
 BACKEND = "b200"
+POLL_MODES = {"gateway": _lib.POLL_GATEWAY, "direct": _lib.POLL_DIRECT}
 
 
 @dataclass(frozen=True)
@@ -57,8 +58,9 @@ class NativeConfig:
     threads_per_worker: int = 512
     poll_backoff_ns: int = 0
     cell_stride: int = 128
-    poll_replicas: int = 4
-    poll_spacing_ns: int = 200
+    poll_mode: str = "gateway"      # "gateway": one warp polls all host cells, forwards via L2; "direct"
+    poll_replicas: int = 0          # 0 = default (gateway 2, direct 1)
+    poll_spacing_ns: int = 300
     num_slots: int = 1024
     trace_capacity: int = 65536
     acquire_poll: bool = False
@@ -73,6 +75,8 @@ class NativeConfig:
             raise UsageError("spin_yield_threshold must be positive")
         if self.wait_timeout_s <= 0:
             raise UsageError("wait_timeout_s must be positive")
+        if self.poll_mode not in POLL_MODES:
+            raise UsageError(f"unknown poll mode {self.poll_mode!r}")
 
     def to_c(self) -> "_lib.lk_config":
         c = _lib.lk_config()
@@ -88,6 +92,7 @@ class NativeConfig:
         c.num_slots = self.num_slots
         c.poll_replicas = self.poll_replicas
         c.poll_spacing_ns = self.poll_spacing_ns
+        c.poll_mode = POLL_MODES[self.poll_mode]
         c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0))
@@ -99,6 +104,25 @@ def pin_host_thread(device: int) -> int:
     n = C.c_uint32()
     _lib.check(_lib.load().lk_pin_thread_near(device, C.byref(n)))
     return n.value
+
+
+_LAZY_WARNED = False
+
+
+def _warn_lazy_loading() -> None:
+    """CUDA 12 loads kernel modules lazily on first launch, and a module load
+    while the persistent kernel is resident can wait on it forever.  liblk.so
+    preloads its own kernels; other libraries' kernels (torch ...) must be
+    launched once before start(), or CUDA_MODULE_LOADING=EAGER set."""
+    global _LAZY_WARNED
+    import os
+    import sys
+    if _LAZY_WARNED or os.environ.get("CUDA_MODULE_LOADING", "LAZY").upper() == "EAGER":
+        return
+    if "torch" in sys.modules:
+        _LAZY_WARNED = True
+        log.info("CUDA lazy module loading is on: launch every torch kernel you will use while "
+                 "the LK session is live once before start() (or set CUDA_MODULE_LOADING=EAGER)")
 
 
 class _WorkerHandle:
@@ -137,6 +161,7 @@ class NativeSession:
     def start(cls, cfg: Optional[NativeConfig] = None) -> tuple["NativeSession", PhaseTiming]:
         cfg = cfg or NativeConfig()
         lib = _lib.load()
+        _warn_lazy_loading()
         t0 = time.perf_counter_ns()
         if cfg.pin_to_cores:
             try:
@@ -362,6 +387,13 @@ class NativeSession:
                                           trig.ctypes.data, done.ctypes.data, cyc.ctypes.data)
         _lib.check(rc)
         return trig, done, cyc
+
+    def last_timeline(self) -> np.ndarray:
+        """(num_workers, 4) globaltimer ns of each worker's last dispatch: to_gpu
+        value seen, work begin, work end, FINISHED issued."""
+        t = np.zeros((self.num_workers, 4), dtype=np.uint64)
+        _lib.check(self._lib.lk_last_timeline(self._h, t.ctypes.data, self.num_workers))
+        return t
 
     def last_spans(self):
         """Device globaltimer (begin, end) of each worker's last dispatch."""

@@ -11,6 +11,7 @@ from __future__ import annotations
 import random
 import statistics
 
+import numpy as np
 import pytest
 
 from oracle import projection
@@ -303,6 +304,36 @@ def test_criterion_7_random_programs_on_gpu():
         session.wait(covered)
     session.dispose()
     assert_trace_ok(session, program, 8)
+
+
+@pytest.mark.parametrize("mode,replicas", [("direct", 1), ("direct", 4), ("gateway", 1), ("gateway", 4)])
+def test_poll_modes_random_programs(mode, replicas):
+    """Both to_gpu delivery paths (gateway warp + device mailboxes, direct
+    PCIe polling) and replica counts run the same random programs with
+    validated traces and golden projections."""
+    rng = random.Random(7 + replicas)
+    session = start(12, trace_capacity=4096, poll_mode=mode, poll_replicas=replicas)
+    program = []
+    for k in range(80):
+        sms = rng.sample(range(12), rng.randint(1, 12))
+        m = host.mask_of(sms)
+        session.trigger(m, WorkDescriptor(slot=k % 16, iterations=rng.randrange(200)))
+        program.append((m, k % 16))
+        session.wait(m)
+    session.dispose()
+    assert_trace_ok(session, program, 12)
+
+
+def test_device_timeline_is_ordered():
+    session = start(None)
+    n = session.num_workers
+    session.register(WorkDescriptor(slot=0, kind="empty"))
+    session.bench_roundtrip([1 << i for i in range(n)], 0, 2 * n)
+    t = session.last_timeline().astype(np.int64)
+    session.dispose()
+    assert (t[:, 0] > 0).all()
+    assert (np.diff(t, axis=1) >= 0).all()          # seen <= begin <= end <= finished
+    assert np.median(t[:, 3] - t[:, 0]) < 20_000     # device-side handling well under 20 us
 
 
 @pytest.mark.slow

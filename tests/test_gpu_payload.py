@@ -22,9 +22,13 @@ RTOL_F32_REDUCE = 1e-6
 
 @pytest.fixture(scope="module")
 def session():
-    try:   # bring torch's CUDA state up before the persistent kernel is resident
+    try:   # bring torch's CUDA state AND the kernels the torch test uses up before the
+        # persistent kernel is resident: CUDA 12 loads kernels lazily, and a module
+        # load while a spinning kernel is resident waits on it forever.
         import torch
-        torch.zeros(1, device="cuda")
+        t = torch.arange(8, dtype=torch.int32, device="cuda")
+        (t + 1).float().cpu()
+        torch.empty_like(t).copy_(t)
         torch.cuda.synchronize()
     except Exception:
         pass
