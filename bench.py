@@ -444,7 +444,8 @@ def run_lk_arm(args, world, rank, local):
         pinned = 0
     cfg = native.NativeConfig(num_workers=args.workers, device=device, spin_strategy=native.PURE_SPIN,
                               poll_backoff_ns=args.backoff_ns, cell_stride=args.cell_stride,
-                              poll_replicas=args.replicas, poll_spacing_ns=args.spacing_ns)
+                              poll_replicas=args.replicas, poll_spacing_ns=args.spacing_ns,
+                              poll_mode=args.poll_mode, tma_payload=not args.lsu_payload)
     session, init = native.NativeSession.start(cfg)
     n = session.num_workers
     empty = WorkDescriptor(slot=0, kind="empty")
@@ -472,7 +473,11 @@ def run_lk_arm(args, world, rank, local):
     done_all = np.concatenate(done_all)
     cyc_all = np.concatenate(cyc_all)
 
-    extras = {}
+    tl = session.last_timeline().astype(np.int64)
+    extras = {"device_handling_us": {
+        "what": "globaltimer, each worker's last timed dispatch: to_gpu value seen -> FINISHED store issued",
+        "p50": round(float(np.median(tl[:, 3] - tl[:, 0])) / 1e3, 3),
+        "max": round(float((tl[:, 3] - tl[:, 0]).max()) / 1e3, 3)}}
     # full-148-worker dispatch
     full = host.full_mask(n)
     _, fdone, fcyc = session.bench_roundtrip([full], 0, args.full_rounds)
@@ -556,7 +561,8 @@ def run_lk_arm(args, world, rank, local):
                                "round-robin single-worker masks", "workers": n, "rounds_per_step": R,
                    "total_rounds": int(units), "threads_per_worker": cfg.threads_per_worker,
                    "cell_stride": cfg.cell_stride, "poll_backoff_ns": cfg.poll_backoff_ns,
-                   "poll_replicas": cfg.poll_replicas, "poll_spacing_ns": cfg.poll_spacing_ns,
+                   "poll_mode": cfg.poll_mode, "poll_replicas": cfg.poll_replicas,
+                   "poll_spacing_ns": cfg.poll_spacing_ns, "payload_path": "tma" if cfg.tma_payload else "lsu",
                    "host_cores_pinned": pinned, "l2": "n/a for the empty task (no payload); payload "
                    "GB/s rotate buffers over >= 4x L2",
                    "timing": "host CLOCK_MONOTONIC per round; max over ranks"},
@@ -593,8 +599,10 @@ def main():
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--backoff-ns", type=int, default=0)
     ap.add_argument("--cell-stride", type=int, default=128)
-    ap.add_argument("--replicas", type=int, default=4)
-    ap.add_argument("--spacing-ns", type=int, default=200)
+    ap.add_argument("--poll-mode", choices=["gateway", "direct"], default="gateway")
+    ap.add_argument("--replicas", type=int, default=0, help="0 = mode default")
+    ap.add_argument("--spacing-ns", type=int, default=300)
+    ap.add_argument("--lsu-payload", action="store_true", help="payload via 128-bit LSU loads, not the TMA ring")
     ap.add_argument("--full-rounds", type=int, default=100_000)
     ap.add_argument("--e2e-rounds", type=int, default=100_000)
     ap.add_argument("--base-rounds", type=int, default=100_000)

@@ -118,6 +118,7 @@ typedef struct lk_config {
 
 #define LK_CF_ACQUIRE_POLL   1u  /* poll with ld.acquire.sys instead of ld.relaxed.sys */
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
+#define LK_CF_LSU_PAYLOAD    4u  /* payload items with 128-bit LSU loads instead of the TMA bulk ring */
 
 /* One linearized protocol write; replaces TraceRecord (protocol.py:253-261). */
 typedef struct lk_trace_rec {
@@ -249,6 +250,10 @@ int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t 
  * launches, avg ms per launch. */
 int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_t grid,
                             uint32_t reps, float* avg_ms);
+/* 1 (default): payload work functions stream through the same TMA bulk ring
+ * as the persistent kernel (96 KiB dynamic shared memory per CTA); 0: LSU
+ * path, which also fits beside a resident LK session. */
+int lk_baseline_set_tma(lk_baseline* b, int on);
 int lk_baseline_destroy(lk_baseline* b);
 
 /* ---- host helpers ----------------------------------------------------------- */

@@ -38,6 +38,7 @@ KIND_IDS = {
 DF_SCALAR = 1
 CF_ACQUIRE_POLL = 1
 CF_FENCE_ALWAYS = 2
+CF_LSU_PAYLOAD = 4
 POLL_GATEWAY = 0
 POLL_DIRECT = 1
 
@@ -142,6 +143,7 @@ SIGNATURES = {
     "lk_baseline_bench": (I32, [P, C.POINTER(lk_desc), U32, U64, P, P]),
     "lk_baseline_time_kernel": (I32, [P, C.POINTER(lk_desc), U32, U32, C.POINTER(C.c_float)]),
     "lk_baseline_destroy": (I32, [P]),
+    "lk_baseline_set_tma": (I32, [P, I32]),
     "lk_pin_thread_near": (I32, [I32, PU32]),
     "lk_device_count": (I32, [C.POINTER(C.c_int)]),
     "lk_sm_count": (I32, [I32, C.POINTER(C.c_int)]),

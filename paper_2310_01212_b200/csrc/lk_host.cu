@@ -415,6 +415,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   // --- one CTA per SM: dynamic smem above half the SM's capacity
   s->smem = size_t(prop.sharedMemPerMultiprocessor) / 2 + 8192;
   if (s->smem > size_t(prop.sharedMemPerBlockOptin) - 1024) s->smem = size_t(prop.sharedMemPerBlockOptin) - 1024;
+  const bool use_tma = !(cfg.flags & LK_CF_LSU_PAYLOAD);
+  if (use_tma && s->smem < lk_ring_bytes())
+    return cleanup(fail(LK_E_INIT, "payload ring needs %zu B of shared memory, have %zu", lk_ring_bytes(), s->smem));
   ce = lk_preload_kernels();
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "kernel load: %s", cudaGetErrorString(ce)));
   ce = lk_persistent_configure(s->smem);
@@ -454,6 +457,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.nw = s->nw;
   a.wthreads = s->threads;
   a.poll_mode = cfg.poll_mode;
+  a.use_tma = use_tma ? 1 : 0;
   ce = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(ce)));
 
@@ -927,6 +931,7 @@ struct lk_baseline {
   cudaStream_t stream;
   uint32_t* d_ctr;
   bool in_flight;
+  int use_tma;
   cudaEvent_t e0, e1;
 };
 
@@ -939,6 +944,8 @@ extern "C" int lk_baseline_create(int device, uint32_t threads, lk_baseline** ou
   b->device = device;
   b->threads = threads;
   b->in_flight = false;
+  b->use_tma = 1;
+  LK_CUDA(lk_preload_kernels());
   LK_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
   LK_CUDA(dev_alloc(reinterpret_cast<void**>(&b->d_ctr), 4));
   LK_CUDA(cudaMemsetAsync(b->d_ctr, 0, 4, svc_stream()));
@@ -953,7 +960,7 @@ extern "C" int lk_baseline_launch(lk_baseline* b, const lk_desc* d, uint32_t gri
   if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
   if (b->in_flight) return fail(LK_E_USAGE, "previous task not yet joined");
   const uint64_t t0 = now_ns();
-  cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream);
+  cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
   const uint64_t t1 = now_ns();
   if (ce != cudaSuccess) return fail(LK_E_CUDA, "launch: %s", cudaGetErrorString(ce));
   b->in_flight = true;
@@ -976,7 +983,7 @@ extern "C" int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid
   if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
   for (uint64_t k = 0; k < rounds; ++k) {
     const uint64_t t0 = now_ns();
-    cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream);
+    cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
     const uint64_t t1 = now_ns();
     if (ce != cudaSuccess) return fail(LK_E_CUDA, "launch: %s", cudaGetErrorString(ce));
     LK_CUDA(cudaStreamSynchronize(b->stream));
@@ -992,7 +999,7 @@ extern "C" int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_
   if (!b || !d || !avg_ms || reps == 0) return fail(LK_E_USAGE, "bad argument");
   LK_CUDA(cudaEventRecord(b->e0, b->stream));
   for (uint32_t k = 0; k < reps; ++k) {
-    cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream);
+    cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
     if (ce != cudaSuccess) return fail(LK_E_CUDA, "launch: %s", cudaGetErrorString(ce));
   }
   LK_CUDA(cudaEventRecord(b->e1, b->stream));
@@ -1000,6 +1007,12 @@ extern "C" int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_
   float ms = 0.f;
   LK_CUDA(cudaEventElapsedTime(&ms, b->e0, b->e1));
   *avg_ms = ms / float(reps);
+  return LK_OK;
+}
+
+extern "C" int lk_baseline_set_tma(lk_baseline* b, int on) {
+  if (!b) return fail(LK_E_USAGE, "null argument");
+  b->use_tma = on ? 1 : 0;
   return LK_OK;
 }
 

@@ -110,6 +110,99 @@ __device__ __forceinline__ void st4(uint4* p, uint4 v) {
                "r"(v.w) : "memory");
 }
 
+// ---------------------------------------------------------------- TMA bulk ring
+// Payload tiles stream HBM -> shared memory with cp.async.bulk (the TMA
+// engine's 1-D bulk copy: no tensor map, no register staging), completion
+// counted on an mbarrier by transaction bytes.  kStages tiles of kStageBytes
+// are in flight per SM (96 KiB: ~14 MiB across 148 SMs, far above the
+// ~4.5 MiB Little's law asks for at ~6.5 TB/s x ~700 ns), issued by one
+// elected thread while every worker thread consumes.  The ring persists
+// across dispatches: `g` counts tiles consumed since the barriers were
+// initialised (identical in every thread), so stage = g % kStages and the
+// mbarrier phase parity = (g / kStages) & 1.
+constexpr uint32_t kStageBytes = 16384;
+constexpr uint32_t kStages = 6;
+constexpr uint32_t kRingBytes = kStageBytes * kStages;
+
+struct Ring {
+  uint8_t* buf;       // kStages x kStageBytes, 128-B aligned, dynamic shared memory
+  uint64_t* full;     // kStages mbarriers: 1 arrival (expect_tx) + tx bytes
+  uint64_t* empty;    // kStages mbarriers: T arrivals (every consumer)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LK_MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LK_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds4(const uint8_t* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
+// Called by every worker thread once, before the first dispatch.
+__device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < kStages; ++k) {
+      mbar_init(r.full + k, 1);
+      mbar_init(r.empty + k, T);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  wsync(T);
+}
+
+// Stream tiles [0, ntiles) of a chunk through the ring: thread 0 keeps up to
+// kStages-1 tiles ahead; `load(i, stage_ptr, bar)` issues tile i's bulk copies
+// (after arming the barrier with its byte count), `use(i, stage_ptr)` consumes
+// it in every thread.
+template <class Load, class Use>
+__device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntiles, const Load& load,
+                                            const Use& use) {
+  const uint32_t c0 = g;
+  auto fill = [&](uint32_t i) {
+    const uint32_t f = c0 + i, st = f % kStages;
+    mbar_wait(r.empty + st, ((f / kStages) & 1u) ^ 1u);   // previous use of this stage released
+    load(i, r.buf + st * kStageBytes, r.full + st);
+  };
+  if (threadIdx.x == 0)
+    for (uint32_t i = 0; i < ntiles && i < kStages - 1; ++i) fill(i);
+  for (uint32_t i = 0; i < ntiles; ++i) {
+    if (threadIdx.x == 0 && i + kStages - 1 < ntiles) fill(i + kStages - 1);
+    const uint32_t c = c0 + i, st = c % kStages;
+    mbar_wait(r.full + st, (c / kStages) & 1u);
+    use(i, r.buf + st * kStageBytes);
+    mbar_arrive(r.empty + st);
+  }
+  g = c0 + ntiles;
+}
+
 // ---------------------------------------------------------------- work items
 // Shard [0, n) over `count` workers in 128-B (32-element) aligned chunks.
 struct Part { uint64_t b, e; };
@@ -168,6 +261,44 @@ __device__ __forceinline__ void map_chunk(const lk_desc& d, Part p, const Op& op
   for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
 }
 
+// map_chunk through the TMA ring: tiles of kStageBytes/2 per input (2 inputs)
+// or kStageBytes (1 input); each thread reads its 16-B lanes of the tile from
+// shared memory and stores the result straight to global memory.
+template <bool kTwo, class Op>
+__device__ __forceinline__ void map_tma(const lk_desc& d, Part p, const Op& op, uint32_t T, Ring& r,
+                                        uint32_t& g) {
+  const uint32_t t = threadIdx.x;
+  const uint4* a4 = reinterpret_cast<const uint4*>(d.in0);
+  const uint4* c4 = reinterpret_cast<const uint4*>(d.in1);
+  uint4* o4 = reinterpret_cast<uint4*>(d.out);
+  const uint64_t vb = p.b >> 2, ve = p.e >> 2;
+  constexpr uint32_t kTileV = kTwo ? kStageBytes / 32 : kStageBytes / 16;   // uint4 per input per tile
+  const uint64_t nv = ve > vb ? ve - vb : 0;
+  const uint32_t ntiles = uint32_t((nv + kTileV - 1) / kTileV);
+  ring_stream(
+      r, g, ntiles,
+      [&](uint32_t i, uint8_t* stage, uint64_t* bar) {
+        const uint64_t v0 = vb + uint64_t(i) * kTileV;
+        const uint32_t bytes = uint32_t(min(uint64_t(kTileV), ve - v0)) * 16u;
+        mbar_expect_tx(bar, kTwo ? 2 * bytes : bytes);
+        bulk_g2s(stage, a4 + v0, bytes, bar);
+        if (kTwo) bulk_g2s(stage + kStageBytes / 2, c4 + v0, bytes, bar);
+      },
+      [&](uint32_t i, const uint8_t* stage) {
+        const uint64_t v0 = vb + uint64_t(i) * kTileV;
+        const uint32_t nvt = uint32_t(min(uint64_t(kTileV), ve - v0));
+        for (uint32_t v = t; v < nvt; v += T) {
+          const uint4 x = lds4(stage + 16 * v);
+          const uint4 y = kTwo ? lds4(stage + kStageBytes / 2 + 16 * v) : x;
+          st4(o4 + v0 + v, vop(op, x, y));
+        }
+      });
+  const uint32_t* a = reinterpret_cast<const uint32_t*>(d.in0);
+  const uint32_t* c = reinterpret_cast<const uint32_t*>(d.in1);
+  uint32_t* o = reinterpret_cast<uint32_t*>(d.out);
+  for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -189,11 +320,36 @@ struct ReduceSmem {
 // fp64 into *(double*)aux.
 template <int U>
 __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t rank, uint32_t count,
-                                             uint32_t* ctr, ReduceSmem& sm, uint32_t T) {
+                                             uint32_t* ctr, ReduceSmem& sm, uint32_t T, Ring* ring,
+                                             uint32_t& g) {
   const uint32_t t = threadIdx.x;
   const float* x = reinterpret_cast<const float*>(d.in0);
   float acc = 0.f;
-  if (d.flags & LK_DF_SCALAR) {
+  if (ring && !(d.flags & LK_DF_SCALAR)) {
+    const uint4* x4 = reinterpret_cast<const uint4*>(x);
+    const uint64_t vb = p.b >> 2, ve = p.e >> 2;
+    constexpr uint32_t kTileV = kStageBytes / 16;
+    const uint64_t nv = ve > vb ? ve - vb : 0;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    ring_stream(
+        *ring, g, uint32_t((nv + kTileV - 1) / kTileV),
+        [&](uint32_t i, uint8_t* stage, uint64_t* bar) {
+          const uint64_t v0 = vb + uint64_t(i) * kTileV;
+          const uint32_t bytes = uint32_t(min(uint64_t(kTileV), ve - v0)) * 16u;
+          mbar_expect_tx(bar, bytes);
+          bulk_g2s(stage, x4 + v0, bytes, bar);
+        },
+        [&](uint32_t i, const uint8_t* stage) {
+          const uint32_t nvt = uint32_t(min(uint64_t(kTileV), ve - (vb + uint64_t(i) * kTileV)));
+          for (uint32_t v = t; v < nvt; v += T) {
+            const uint4 r = lds4(stage + 16 * v);
+            s.x += __uint_as_float(r.x); s.y += __uint_as_float(r.y);
+            s.z += __uint_as_float(r.z); s.w += __uint_as_float(r.w);
+          }
+        });
+    acc = (s.x + s.y) + (s.z + s.w);
+    for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
+  } else if (d.flags & LK_DF_SCALAR) {
     for (uint64_t i = p.b + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
   } else {
     const uint4* x4 = reinterpret_cast<const uint4*>(x);
@@ -258,18 +414,30 @@ __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
 }
 
 // Payload work shared by both kernels; every thread of the CTA calls it.
+// ring == nullptr (or misaligned buffers): 128-bit LSU loads; else the TMA ring.
 __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
-                                          uint32_t* ctr, ReduceSmem& rs, uint32_t T) {
+                                          uint32_t* ctr, ReduceSmem& rs, uint32_t T, Ring* ring,
+                                          uint32_t& g) {
   const Part p = partition(d.n, rank, count);
+  const bool tma = ring != nullptr && !(d.flags & LK_DF_SCALAR);
   switch (d.kind) {
-    case LK_KIND_VECTOR_ADD_I32: map_chunk<4, true>(d, p, OpAddI32{}, T); break;
-    case LK_KIND_SAXPY_F32: map_chunk<4, true>(d, p, OpSaxpy{d.alpha}, T); break;
+    case LK_KIND_VECTOR_ADD_I32:
+      if (tma) map_tma<true>(d, p, OpAddI32{}, T, *ring, g);
+      else map_chunk<4, true>(d, p, OpAddI32{}, T);
+      break;
+    case LK_KIND_SAXPY_F32:
+      if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, *ring, g);
+      else map_chunk<4, true>(d, p, OpSaxpy{d.alpha}, T);
+      break;
     case LK_KIND_HBM_STREAM: {
       const uint64_t passes = d.iterations ? d.iterations : 1;
-      for (uint64_t k = 0; k < passes; ++k) map_chunk<8, false>(d, p, OpCopy{}, T);
+      for (uint64_t k = 0; k < passes; ++k) {
+        if (tma) map_tma<false>(d, p, OpCopy{}, T, *ring, g);
+        else map_chunk<8, false>(d, p, OpCopy{}, T);
+      }
       break;
     }
-    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs, T); break;
+    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs, T, ring, g); break;
     default: break;
   }
 }
@@ -487,6 +655,7 @@ struct PersistSmem {
   lk_desc desc;
   uint32_t cmd, rank, count, slot;
   ReduceSmem red;
+  uint64_t full[kStages], empty[kStages];
 };
 
 __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const lk_dev_args a) {
@@ -497,6 +666,11 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     if (wid == 0 && a.poll_mode == LK_POLL_GATEWAY) gateway(a);
     return;
   }
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
+  Ring ring{dyn_smem, sm.full, sm.empty};
+  Ring* rp = a.use_tma ? &ring : nullptr;
+  uint32_t g = 0;
+  if (rp) ring_init(ring, T);
   Elected e;
   e.st = lk_wstate{LK_PHASE_BOOTING, 0};
   e.pub = LK_NOP;  // cells start at the NOP sentinel (protocol.py:217-218)
@@ -555,7 +729,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     wsync(T);
     if (sm.cmd == kCmdExit) break;
     const lk_desc d = sm.desc;
-    run_multi(d, sm.rank, sm.count, a.reduce_ctr + sm.slot, sm.red, T);
+    run_multi(d, sm.rank, sm.count, a.reduce_ctr + sm.slot, sm.red, T, rp, g);
     wsync(T);
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();
@@ -569,13 +743,18 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
 }
 
 // ---------------------------------------------------------------- baseline
-__global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, uint32_t* ctr) {
+__global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, uint32_t* ctr, int use_tma) {
   __shared__ ReduceSmem rs;
+  __shared__ uint64_t full[kStages], empty[kStages];
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
   if (single_thread_kind(d.kind)) {
     if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
     return;
   }
-  run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x);
+  Ring ring{dyn_smem, full, empty};
+  uint32_t g = 0;
+  if (use_tma) ring_init(ring, blockDim.x);
+  run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, use_tma ? &ring : nullptr, g);
 }
 
 // ---------------------------------------------------------------- ping-pong
@@ -596,6 +775,8 @@ __global__ void lk_pingpong_kernel(volatile uint32_t* flag, volatile uint32_t* e
 cudaError_t lk_preload_kernels() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, lk_work_kernel);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lk_work_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRingBytes));
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_pingpong_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_persistent_kernel);
   return e;
@@ -617,10 +798,12 @@ cudaError_t lk_launch_persistent(const lk_dev_args& a, uint32_t grid, uint32_t t
 }
 
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads, uint32_t* reduce_ctr,
-                           cudaStream_t st) {
-  lk_work_kernel<<<grid, threads, 0, st>>>(d, reduce_ctr);
+                           cudaStream_t st, int use_tma) {
+  lk_work_kernel<<<grid, threads, use_tma ? kRingBytes : 0, st>>>(d, reduce_ctr, use_tma);
   return cudaGetLastError();
 }
+
+size_t lk_ring_bytes() { return kRingBytes; }
 
 cudaError_t lk_launch_pingpong(volatile uint32_t* flag, volatile uint32_t* echo, uint64_t rounds,
                                cudaStream_t st) {

@@ -65,6 +65,7 @@ class NativeConfig:
     trace_capacity: int = 65536
     acquire_poll: bool = False
     fence_always: bool = False
+    tma_payload: bool = True        # payload tiles via the TMA bulk ring (False: 128-bit LSU loads)
 
     def __post_init__(self) -> None:
         if self.num_workers is not None and self.num_workers < 1:
@@ -95,7 +96,8 @@ class NativeConfig:
         c.poll_mode = POLL_MODES[self.poll_mode]
         c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
-                   | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0))
+                   | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
+                   | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD))
         return c
 
 
@@ -411,10 +413,12 @@ def _dev_addr(buf) -> int:
 class LaunchSyncBaseline:
     """cudaLaunchKernel + cudaStreamSynchronize per task (the CUDA "spawn")."""
 
-    def __init__(self, device: int = 0, threads_per_worker: int = 512, grid: Optional[int] = None):
+    def __init__(self, device: int = 0, threads_per_worker: int = 512, grid: Optional[int] = None,
+                 tma_payload: bool = True):
         self._lib = _lib.load()
         self._h = C.c_void_p()
         _lib.check(self._lib.lk_baseline_create(device, threads_per_worker, C.byref(self._h)))
+        _lib.check(self._lib.lk_baseline_set_tma(self._h, 1 if tma_payload else 0))
         if grid is None:
             n = C.c_int()
             _lib.check(self._lib.lk_sm_count(device, C.byref(n)))

@@ -1,0 +1,59 @@
+"""The conventional launch+sync baseline (ThreadSpawnBaseline analogue,
+native.py:304-331) runs the same device work functions; it must produce the
+oracle's results through both payload paths (TMA bulk ring and LSU loads).
+
+Kept in its own module: an LK session owns every SM (one resident CTA each,
+registers and shared memory sized for exactly one), so a baseline kernel can
+only be scheduled when no session is live."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import work as W
+from paper_2310_01212_b200 import native
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+
+pytestmark = pytest.mark.gpu
+
+
+def _i32(n, seed):
+    return np.random.default_rng(seed).integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+
+
+def _f32(n, seed, lo=-1.0, hi=1.0):
+    return np.random.default_rng(seed).uniform(lo, hi, n).astype(np.float32)
+
+
+@pytest.mark.parametrize("tma", [True, False])
+@pytest.mark.parametrize("n", [65536, 1000003, 37])
+def test_baseline_kernel_same_results(tma, n):
+    b = native.LaunchSyncBaseline(tma_payload=tma)
+    a, c = _i32(n, 0), _i32(n, 1)
+    da, dc, do = DeviceBuffer.from_array(a), DeviceBuffer.from_array(c), DeviceBuffer(4 * n)
+    b.launch(WorkDescriptor(slot=0, kind="vector_add_i32", data_in_ref=(da, dc), data_out_ref=do))
+    b.wait()
+    np.testing.assert_array_equal(do.download(np.int32, n), W.vector_add_i32(a, c))
+    x, y = _f32(n, 2), _f32(n, 3)
+    dx, dy, dz = DeviceBuffer.from_array(x), DeviceBuffer.from_array(y), DeviceBuffer(4 * n)
+    b.launch(WorkDescriptor(slot=0, kind="saxpy_f32", data_in_ref=(dx, dy), data_out_ref=dz, alpha=1.5))
+    b.wait()
+    np.testing.assert_array_equal(dz.download(np.float32, n).view(np.uint32),
+                                  W.saxpy_f32(1.5, x, y).view(np.uint32))
+    xi = np.random.default_rng(9).integers(0, 8, n).astype(np.float32)
+    dxi, dp, dt = DeviceBuffer.from_array(xi), DeviceBuffer(4 * b.grid), DeviceBuffer(8)
+    b.launch(WorkDescriptor(slot=0, kind="block_reduce_f32", data_in_ref=dxi, data_out_ref=dp, total_ref=dt))
+    b.wait()
+    np.testing.assert_array_equal(dp.download(np.float32, b.grid).astype(np.float64),
+                                  W.block_reduce_partials(xi, b.grid))
+    assert dt.download(np.float64, 1)[0] == W.block_reduce_total(xi)
+    b.close()
+
+
+def test_baseline_time_kernel_reports_positive():
+    n = 1 << 20
+    b = native.LaunchSyncBaseline()
+    x, y = DeviceBuffer(4 * n), DeviceBuffer(4 * n)
+    ms = b.time_kernel(WorkDescriptor(slot=0, kind="saxpy_f32", data_in_ref=(x, y), data_out_ref=y), 3)
+    assert 0 < ms < 100
+    b.close()

@@ -20,8 +20,8 @@ pytestmark = pytest.mark.gpu
 RTOL_F32_REDUCE = 1e-6
 
 
-@pytest.fixture(scope="module")
-def session():
+@pytest.fixture(scope="module", params=["tma", "lsu"])
+def session(request):
     try:   # bring torch's CUDA state AND the kernels the torch test uses up before the
         # persistent kernel is resident: CUDA 12 loads kernels lazily, and a module
         # load while a spinning kernel is resident waits on it forever.
@@ -32,16 +32,10 @@ def session():
         torch.cuda.synchronize()
     except Exception:
         pass
-    s, _ = native.NativeSession.start(native.NativeConfig(spin_yield_threshold=200))
+    s, _ = native.NativeSession.start(native.NativeConfig(spin_yield_threshold=200,
+                                                          tma_payload=request.param == "tma"))
     yield s
     s.close()
-
-
-@pytest.fixture(scope="module")
-def baseline():
-    b = native.LaunchSyncBaseline()
-    yield b
-    b.close()
 
 
 def _i32(n, seed):
@@ -169,20 +163,6 @@ def test_full_size_saxpy_64mib_matches_oracle(session):
         WorkDescriptor(slot=50, kind="saxpy_f32", data_in_ref=(dx, dy), data_out_ref=do, alpha=1.5))
     np.testing.assert_array_equal(do.download(np.float32, n).view(np.uint32),
                                   W.saxpy_f32(1.5, x, y).view(np.uint32))
-
-
-def test_baseline_kernel_same_results(baseline):
-    n = 65536
-    a, b = _i32(n, 0), _i32(n, 1)
-    da, db, do = DeviceBuffer.from_array(a), DeviceBuffer.from_array(b), DeviceBuffer(4 * n)
-    baseline.launch(WorkDescriptor(slot=0, kind="vector_add_i32", data_in_ref=(da, db), data_out_ref=do))
-    baseline.wait()
-    np.testing.assert_array_equal(do.download(np.int32, n), W.vector_add_i32(a, b))
-    x, y = _f32(n, 2), _f32(n, 3)
-    dx, dy, dz = DeviceBuffer.from_array(x), DeviceBuffer.from_array(y), DeviceBuffer(4 * n)
-    baseline.launch(WorkDescriptor(slot=0, kind="saxpy_f32", data_in_ref=(dx, dy), data_out_ref=dz, alpha=1.5))
-    baseline.wait()
-    np.testing.assert_array_equal(dz.download(np.float32, n), W.saxpy_f32(1.5, x, y))
 
 
 def test_torch_tensors_as_payload_refs(session):
