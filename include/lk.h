@@ -119,6 +119,7 @@ typedef struct lk_config {
 #define LK_CF_ACQUIRE_POLL   1u  /* poll with ld.acquire.sys instead of ld.relaxed.sys */
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
 #define LK_CF_LSU_PAYLOAD    4u  /* payload items with 128-bit LSU loads instead of the TMA bulk ring */
+#define LK_CF_TIMELINE       8u  /* GATEWAY: stamp forward times into the device timeline (+1 L2 load per value) */
 
 /* One linearized protocol write; replaces TraceRecord (protocol.py:253-261). */
 typedef struct lk_trace_rec {
@@ -229,9 +230,17 @@ int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks,
 /* Device-side spans of the last dispatch per worker (globaltimer ns):
  * begin (WORK observed) and end (work done, before FINISHED). */
 int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n);
-/* Device timeline of the last dispatch per worker, 4 globaltimer stamps each
- * (t[4*i+0..3]): to_gpu value seen, work begin, work end, FINISHED issued. */
+/* Device timeline of the last dispatch per worker, 8 words each (t[8*i+k]):
+ * globaltimer ns at k=0 to_gpu value seen, 1 work begin, 2 work end,
+ * 3 FINISHED issued, 4 gateway forward (LK_CF_TIMELINE, else 0); clock64 at
+ * 5 value seen, 6 work begin, 7 FINISHED issued. */
 int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n);
+/* Host side of the same dispatches (CLOCK_MONOTONIC ns, t[3*i+k]): k=0
+ * trigger call start, 1 WORK word written, 2 FINISHED observed by wait. */
+int lk_last_host_times(lk_session* s, uint64_t* t, uint32_t n);
+/* globaltimer - CLOCK_MONOTONIC offset (ns) from `rounds` host<->GPU echoes,
+ * taken from the echo with the shortest round trip (*best_rtt_ns). */
+int lk_clock_offset(int device, uint32_t rounds, int64_t* offset_ns, uint64_t* best_rtt_ns);
 
 /* Raw host<->GPU ping-pong floor: one thread polls a mapped host word and
  * echoes it back; rounds samples of the round trip. */

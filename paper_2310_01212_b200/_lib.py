@@ -39,6 +39,7 @@ DF_SCALAR = 1
 CF_ACQUIRE_POLL = 1
 CF_FENCE_ALWAYS = 2
 CF_LSU_PAYLOAD = 4
+CF_TIMELINE = 8
 POLL_GATEWAY = 0
 POLL_DIRECT = 1
 
@@ -136,6 +137,8 @@ SIGNATURES = {
     "lk_bench_roundtrip": (I32, [P, MASK, U32, U32, U32, U64, P, P, P]),
     "lk_last_spans": (I32, [P, P, P, U32]),
     "lk_last_timeline": (I32, [P, P, U32]),
+    "lk_last_host_times": (I32, [P, P, U32]),
+    "lk_clock_offset": (I32, [I32, U32, PI64, PU64]),
     "lk_pingpong": (I32, [I32, U64, P]),
     "lk_baseline_create": (I32, [I32, U32, C.POINTER(P)]),
     "lk_baseline_launch": (I32, [P, C.POINTER(lk_desc), U32, PU64]),

@@ -123,6 +123,7 @@ struct lk_session {
   bool gateway = true;
   volatile unsigned long long* status = nullptr;  // stride cell_u64
   volatile unsigned long long* err = nullptr;
+  volatile uint32_t* err_any = nullptr;
   volatile uint32_t* smid = nullptr;
   uint32_t cell_u64 = 16, replicas = 4;
 
@@ -152,6 +153,9 @@ struct lk_session {
   bool disposed = false;
   bool kernel_done = false;
   uint64_t t_create = 0;
+
+  // host half of the last dispatch per worker (lk_last_host_times)
+  std::vector<uint64_t> host_times;                       // 3 per worker
 
   // tracing
   std::vector<uint32_t> host_seq;                         // per worker
@@ -216,6 +220,7 @@ static std::string ids_str(const std::vector<uint32_t>& v) {
 
 // Worker errors surface on the next host call (native.py:128-131).
 static int check_workers(lk_session* s) {
+  if (*s->err_any == 0) return LK_OK;   // set (after err[i]) by any worker that records an error
   for (uint32_t i = 0; i < s->nw; ++i) {
     const unsigned long long e = s->err[i];
     if (e) return fail(LK_E_WORKER_DIED, "worker %u died: device error %u on word %u", i, uint32_t(e),
@@ -344,6 +349,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->reg_desc.resize(cfg.num_slots);
   s->reg_mask.resize(cfg.num_slots);
   s->host_seq.assign(s->nw, 0);
+  s->host_times.assign(3 * size_t(s->nw), 0);
   s->host_log.resize(s->nw);
   s->t_create = t0;
 
@@ -362,7 +368,8 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   const size_t tob = s->gateway ? al(size_t(s->replicas) * s->bell_stride * 8)
                                 : al(size_t(s->nw) * s->replicas * cfg.cell_stride);
   const size_t cells = al(size_t(s->nw) * cfg.cell_stride);
-  const size_t errb = al(size_t(s->nw) * 8), smidb = al(size_t(s->nw) * 4);
+  const size_t err_words = (size_t(s->nw) + 15) / 16 * 16;   // err[] then err_any on its own line
+  const size_t errb = al(err_words * 8 + 128), smidb = al(size_t(s->nw) * 4);
   const size_t host_bytes = tob + cells + errb + smidb;
   cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&s->host_block), host_bytes,
                                  cudaHostAllocMapped | cudaHostAllocPortable);
@@ -373,6 +380,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->status = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob);
   s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob + cells);
   s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + tob + cells + errb);
+  s->err_any = reinterpret_cast<volatile uint32_t*>(s->err + err_words);
   for (uint32_t i = 0; i < s->nw; ++i) {
     for (uint32_t k = 0; k < s->replicas; ++k) {
       if (s->gateway) s->bell[uint64_t(k) * s->bell_stride + i] = LK_NOP;   // {NOP, seq 0}
@@ -386,7 +394,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   const size_t descb = al(size_t(cfg.num_slots) * sizeof(lk_desc));
   const size_t maskb = al(size_t(cfg.num_slots) * s->nwords * 8);
   const size_t ctrb = al(size_t(cfg.num_slots) * 4);
-  const size_t spanb = al(size_t(s->nw) * 32);
+  const size_t spanb = al(size_t(s->nw) * 8 * LK_TIMELINE_WORDS);
   const size_t dmbb = al(size_t(s->nw) * 128);
   const size_t exb = al(4);
   const size_t traceb = cfg.record_trace ? al(size_t(s->nw) * cfg.trace_capacity * sizeof(lk_dev_trace)) : 0;
@@ -433,6 +441,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.to_gpu = s->to_gpu;
   a.status = const_cast<unsigned long long*>(s->status);
   a.err = const_cast<unsigned long long*>(s->err);
+  a.err_any = const_cast<uint32_t*>(s->err_any);
   a.smid = const_cast<uint32_t*>(s->smid);
   a.desc = s->d_desc;
   a.slot_mask = s->d_mask;
@@ -523,7 +532,8 @@ static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* d, const ui
 // workers, slot lock, idle cells; then stage the descriptor (when given) and
 // write the WORK word to every masked worker, ascending.
 static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, uint32_t slot,
-                          const lk_desc* d, std::vector<uint32_t>& ids, uint64_t* elapsed_ns) {
+                          const lk_desc* d, std::vector<uint32_t>& ids, uint64_t* elapsed_ns,
+                          uint64_t t_call) {
   int rc = require_live(s);
   if (rc) return rc;
   if (!mask_ids(s, mask, nwords, ids, &rc)) return rc;
@@ -550,6 +560,10 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   const uint32_t word = LK_WORK_BASE + slot;
   for (uint32_t i : ids) s->host_write(i, word);
   const uint64_t t1 = now_ns();
+  for (uint32_t i : ids) {
+    s->host_times[3 * i] = t_call;
+    s->host_times[3 * i + 1] = t1;
+  }
   uint64_t* sp = s->slot_pend.data() + uint64_t(slot) * s->nwords;
   for (uint32_t i : ids) {
     s->pending[i >> 6] |= 1ull << (i & 63);
@@ -566,7 +580,7 @@ extern "C" int lk_trigger(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   if (!s || !mask) return fail(LK_E_USAGE, "null argument");
   std::lock_guard<std::mutex> g(s->mu);
   static thread_local std::vector<uint32_t> ids;
-  return trigger_locked(s, mask, nwords, slot, d, ids, elapsed_ns);
+  return trigger_locked(s, mask, nwords, slot, d, ids, elapsed_ns, now_ns());
 }
 
 static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::vector<uint32_t>& ids,
@@ -583,6 +597,7 @@ static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::
   int rc = spin_words(s, ids, LK_FINISHED, "wait for FINISHED");
   if (rc) return rc;
   const uint64_t finished_at = now_ns();
+  for (uint32_t i : ids) s->host_times[3 * i + 2] = finished_at;
   for (uint32_t i : ids) s->host_write(i, LK_NOP);
   rc = spin_words(s, ids, LK_NOP, "wait for ack consumption");
   if (rc) return rc;
@@ -634,7 +649,7 @@ extern "C" int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t
     int rc;
     {
       std::lock_guard<std::mutex> g(s->mu);
-      rc = trigger_locked(s, m, nwords, slot, nullptr, ids, &el);
+      rc = trigger_locked(s, m, nwords, slot, nullptr, ids, &el, t0);
     }
     if (rc) return rc;
     uint64_t done_abs = 0;
@@ -769,19 +784,66 @@ extern "C" int lk_kernel_alive(lk_session* s, uint32_t* alive) {
 extern "C" int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n) {
   if (!s || !t) return fail(LK_E_USAGE, "null argument");
   const uint32_t m = std::min(n, s->nw);
-  LK_CUDA(cudaMemcpyAsync(t, s->d_spans, size_t(m) * 32, cudaMemcpyDeviceToHost, s->copy_stream));
+  LK_CUDA(cudaMemcpyAsync(t, s->d_spans, size_t(m) * 8 * LK_TIMELINE_WORDS, cudaMemcpyDeviceToHost,
+                          s->copy_stream));
   LK_CUDA(cudaStreamSynchronize(s->copy_stream));
+  return LK_OK;
+}
+
+extern "C" int lk_last_host_times(lk_session* s, uint64_t* t, uint32_t n) {
+  if (!s || !t) return fail(LK_E_USAGE, "null argument");
+  std::lock_guard<std::mutex> g(s->mu);
+  const uint32_t m = std::min(n, s->nw);
+  memcpy(t, s->host_times.data(), size_t(m) * 24);
+  return LK_OK;
+}
+
+extern "C" int lk_clock_offset(int device, uint32_t rounds, int64_t* offset_ns, uint64_t* best_rtt_ns) {
+  if (!offset_ns || rounds == 0) return fail(LK_E_USAGE, "bad argument");
+  LK_CUDA(cudaSetDevice(device));
+  LK_CUDA(lk_preload_kernels());
+  uint8_t* cells = nullptr;
+  LK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cells), 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(cells, 0, 4096);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(cells);
+  volatile unsigned long long* echo = reinterpret_cast<volatile unsigned long long*>(cells + 128);
+  cudaStream_t st;
+  LK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaError_t ce = lk_launch_clocksync(flag, const_cast<unsigned long long*>(echo), rounds, st);
+  if (ce != cudaSuccess) return fail(LK_E_CUDA, "clocksync launch: %s", cudaGetErrorString(ce));
+  uint64_t best = ~0ull;
+  int64_t off = 0;
+  for (uint32_t r = 1; r <= rounds; ++r) {
+    const uint64_t t0 = now_ns();
+    __atomic_store_n(flag, r, __ATOMIC_RELEASE);
+    const uint64_t deadline = t0 + 2000000000ull;
+    while (uint32_t(__atomic_load_n(reinterpret_cast<volatile uint32_t*>(echo + 1), __ATOMIC_ACQUIRE)) != r) {
+      LK_PAUSE();
+      if (now_ns() > deadline) return fail(LK_E_HANG, "clock sync stalled at round %u (kernel left running)", r);
+    }
+    const uint64_t t1 = now_ns();
+    const uint64_t g = echo[0];
+    if (t1 - t0 < best) {
+      best = t1 - t0;
+      off = int64_t(g) - int64_t(t0 + (t1 - t0) / 2);
+    }
+  }
+  LK_CUDA(cudaStreamSynchronize(st));
+  cudaStreamDestroy(st);
+  cudaFreeHost(cells);
+  *offset_ns = off;
+  if (best_rtt_ns) *best_rtt_ns = best;
   return LK_OK;
 }
 
 extern "C" int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n) {
   if (!s) return fail(LK_E_USAGE, "null session");
-  std::vector<uint64_t> sp(4 * size_t(s->nw));
+  std::vector<uint64_t> sp(LK_TIMELINE_WORDS * size_t(s->nw));
   int rc = lk_last_timeline(s, sp.data(), s->nw);
   if (rc) return rc;
   for (uint32_t i = 0; i < std::min(n, s->nw); ++i) {
-    if (begin_ns) begin_ns[i] = sp[4 * i + 1];
-    if (end_ns) end_ns[i] = sp[4 * i + 2];
+    if (begin_ns) begin_ns[i] = sp[LK_TIMELINE_WORDS * i + 1];
+    if (end_ns) end_ns[i] = sp[LK_TIMELINE_WORDS * i + 2];
   }
   return LK_OK;
 }

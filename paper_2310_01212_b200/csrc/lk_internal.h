@@ -20,12 +20,13 @@ struct lk_dev_args {
                                      // word | seq<<32 (seq = host write index, monotone per worker)
   unsigned long long* status;      // host-mapped, cell i at status[i*cell_u64]: word | phase<<32
   unsigned long long* err;         // host-mapped, err[i] = code | word<<32
+  uint32_t* err_any;               // host-mapped, set to 1 after any err[i] is written
   uint32_t* smid;                  // host-mapped, smid[i]
   const lk_desc* desc;             // device, num_slots entries
   const unsigned long long* slot_mask;  // device, num_slots * nwords
   uint32_t* reduce_ctr;            // device, num_slots
-  unsigned long long* spans;       // device, 4 per worker (globaltimer): value seen, work begin,
-                                   // work end, FINISHED issued -- of the last dispatch
+  unsigned long long* spans;       // device, LK_TIMELINE_WORDS per worker: the last dispatch's
+                                   // timeline (lk_last_timeline)
   const unsigned long long* bell;  // host-mapped doorbell (GATEWAY): replica k, worker i at
                                    // bell[k*bell_stride + i] = word | seq<<32
   unsigned long long* dmb;         // device mailboxes (GATEWAY), worker i at dmb[i*dmb_u64]
@@ -54,6 +55,9 @@ cudaError_t lk_launch_persistent(const lk_dev_args& a, uint32_t grid, uint32_t t
                                  size_t smem, cudaStream_t st);
 cudaError_t lk_persistent_configure(size_t smem);
 cudaError_t lk_preload_kernels();
+cudaError_t lk_launch_clocksync(const uint32_t* flag, unsigned long long* echo, uint32_t rounds,
+                                cudaStream_t st);
+#define LK_TIMELINE_WORDS 8
 cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_per_sm);
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads,
                            uint32_t* reduce_ctr, cudaStream_t st, int use_tma);

@@ -451,6 +451,8 @@ struct Elected {           // thread 0's private protocol state
   uint32_t tcnt;
   bool dirty;              // cur not yet stepped to a fixed point
   uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
+  uint64_t c_seen;         // clock64 at the same point
+  uint64_t t_fwd;          // GATEWAY + LK_CF_TIMELINE: globaltimer when the gateway forwarded it
 };
 
 __device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t word,
@@ -473,6 +475,7 @@ __device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elec
 __device__ __forceinline__ void report_error(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t werr,
                                              uint32_t word) {
   st_relaxed_sys(a.err + wid, uint64_t(werr) | (uint64_t(word) << 32));
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.err_any), "r"(1u) : "memory");
   e.st.phase = LK_PHASE_EXITED;
   publish(a, wid, e, e.pub, true);
 }
@@ -537,6 +540,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
           e.cur = uint32_t(c);
           e.dirty = true;
           e.t_seen = globaltimer();
+          e.c_seen = clock64();
           fresh = true;
           break;
         }
@@ -563,6 +567,8 @@ __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t 
         e.cur = uint32_t(c);
         e.dirty = true;
         e.t_seen = globaltimer();
+        e.c_seen = clock64();
+        if (a.flags & LK_CF_TIMELINE) e.t_fwd = ld_relaxed_gpu64(mb + 1);
         break;
       }
       if (a.backoff_ns) __nanosleep(a.backoff_ns);
@@ -607,6 +613,7 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
     const uint32_t sq = uint32_t(val >> 32);
     if (c < nw && sq > seen) {
       seen = sq;
+      if (a.flags & LK_CF_TIMELINE) st_relaxed_gpu64(a.dmb + uint64_t(c) * a.dmb_u64 + 1, globaltimer());
       st_relaxed_gpu64(a.dmb + uint64_t(c) * a.dmb_u64, val);
     }
   };
@@ -651,6 +658,17 @@ __device__ __noinline__ void gateway(const lk_dev_args& a) {
   }
 }
 
+// Per-worker record of the last dispatch (lk_last_timeline): globaltimer at
+// value seen / work begin / work end / FINISHED issued, gateway forward time,
+// and clock64 at seen / work begin / FINISHED issued.
+__device__ __forceinline__ void write_timeline(const lk_dev_args& a, uint32_t wid, const Elected& e,
+                                               uint64_t t_begin, uint64_t t_end, uint64_t c_begin,
+                                               uint64_t c_fin) {
+  unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
+  tl[0] = e.t_seen; tl[1] = t_begin; tl[2] = t_end; tl[3] = globaltimer();
+  tl[4] = e.t_fwd; tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
+}
+
 struct PersistSmem {
   lk_desc desc;
   uint32_t cmd, rank, count, slot;
@@ -679,7 +697,9 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.tcnt = 0;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   e.t_seen = 0;
-  uint64_t t_begin = 0;
+  e.c_seen = 0;
+  e.t_fwd = 0;
+  uint64_t t_begin = 0, c_begin = 0;
   if (threadIdx.x == 0) st_relaxed_sys_u32(a.smid + wid, smid());
 
   for (;;) {
@@ -698,13 +718,14 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
         }
         if (d.kind >= LK_KIND_COUNT) { report_error(a, wid, e, LK_WERR_BAD_KIND, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
         if (single_thread_kind(d.kind)) {
+          c_begin = clock64();
           t_begin = globaltimer();
           if (d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
           const uint64_t t_end = globaltimer();
           const lk_step_out o = lk_complete_work(e.st);
           publish(a, wid, e, o.publish, (a.flags & LK_CF_FENCE_ALWAYS) != 0);
-          unsigned long long* tl = a.spans + 4ull * wid;
-          tl[0] = e.t_seen; tl[1] = t_begin; tl[2] = t_end; tl[3] = globaltimer();
+          const uint64_t c_fin = clock64();
+          write_timeline(a, wid, e, t_begin, t_end, c_begin, c_fin);
           continue;
         }
         // payload item: rank/count from the slot's trigger mask
@@ -722,6 +743,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
         sm.count = count ? count : 1;
         sm.slot = slot;
         sm.cmd = kCmdWork;
+        c_begin = clock64();
         t_begin = globaltimer();
         break;
       }
@@ -735,8 +757,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
       const uint64_t t_end = globaltimer();
       const lk_step_out o = lk_complete_work(e.st);
       publish(a, wid, e, o.publish, true);  // payload visible before FINISHED
-      unsigned long long* tl = a.spans + 4ull * wid;
-      tl[0] = e.t_seen; tl[1] = t_begin; tl[2] = t_end; tl[3] = globaltimer();
+      write_timeline(a, wid, e, t_begin, t_end, c_begin, clock64());
     }
   }
   if (threadIdx.x == 0) atomicAdd(a.exited, 1u);   // lets the gateway retire
@@ -767,7 +788,23 @@ __global__ void lk_pingpong_kernel(volatile uint32_t* flag, volatile uint32_t* e
   }
 }
 
+// Host/device clock correlation: echo %globaltimer for each host flag value.
+__global__ void lk_clocksync_kernel(const uint32_t* flag, unsigned long long* echo, uint32_t rounds) {
+  for (uint32_t r = 1; r <= rounds; ++r) {
+    while (ld_relaxed_sys(flag) != r) {
+    }
+    st_relaxed_sys(echo, globaltimer());
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(echo + 1), "r"(r) : "memory");
+  }
+}
+
 }  // namespace
+
+cudaError_t lk_launch_clocksync(const uint32_t* flag, unsigned long long* echo, uint32_t rounds,
+                                cudaStream_t st) {
+  lk_clocksync_kernel<<<1, 1, 0, st>>>(flag, echo, rounds);
+  return cudaGetLastError();
+}
 
 // CUDA 12 loads kernels lazily on first launch, and loading a module while a
 // spinning kernel is resident can wait on it forever.  Load every kernel of
@@ -778,6 +815,7 @@ cudaError_t lk_preload_kernels() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(lk_work_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRingBytes));
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_pingpong_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_clocksync_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_persistent_kernel);
   return e;
 }

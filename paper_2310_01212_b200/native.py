@@ -66,6 +66,7 @@ class NativeConfig:
     acquire_poll: bool = False
     fence_always: bool = False
     tma_payload: bool = True        # payload tiles via the TMA bulk ring (False: 128-bit LSU loads)
+    timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
 
     def __post_init__(self) -> None:
         if self.num_workers is not None and self.num_workers < 1:
@@ -97,7 +98,8 @@ class NativeConfig:
         c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
-                   | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD))
+                   | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)
+                   | (_lib.CF_TIMELINE if self.timeline else 0))
         return c
 
 
@@ -391,10 +393,18 @@ class NativeSession:
         return trig, done, cyc
 
     def last_timeline(self) -> np.ndarray:
-        """(num_workers, 4) globaltimer ns of each worker's last dispatch: to_gpu
-        value seen, work begin, work end, FINISHED issued."""
-        t = np.zeros((self.num_workers, 4), dtype=np.uint64)
+        """(num_workers, 8) record of each worker's last dispatch: globaltimer ns
+        at value seen, work begin, work end, FINISHED issued, gateway forward
+        (timeline=True); clock64 at value seen, work begin, FINISHED issued."""
+        t = np.zeros((self.num_workers, 8), dtype=np.uint64)
         _lib.check(self._lib.lk_last_timeline(self._h, t.ctypes.data, self.num_workers))
+        return t
+
+    def last_host_times(self) -> np.ndarray:
+        """(num_workers, 3) CLOCK_MONOTONIC ns of each worker's last dispatch:
+        trigger start, WORK written, FINISHED observed."""
+        t = np.zeros((self.num_workers, 3), dtype=np.uint64)
+        _lib.check(self._lib.lk_last_host_times(self._h, t.ctypes.data, self.num_workers))
         return t
 
     def last_spans(self):
@@ -478,6 +488,13 @@ class LaunchSyncBaseline:
 
 # The reference's spawn-per-task baseline name, for drop-in call sites.
 ThreadSpawnBaseline = LaunchSyncBaseline
+
+
+def clock_offset(device: int = 0, rounds: int = 2000) -> tuple[int, int]:
+    """(globaltimer - CLOCK_MONOTONIC ns, best echo round trip ns)."""
+    off, rtt = C.c_int64(), C.c_uint64()
+    _lib.check(_lib.load().lk_clock_offset(device, rounds, C.byref(off), C.byref(rtt)))
+    return off.value, rtt.value
 
 
 def pingpong(device: int, rounds: int) -> np.ndarray:

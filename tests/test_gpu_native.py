@@ -330,10 +330,13 @@ def test_device_timeline_is_ordered():
     session.register(WorkDescriptor(slot=0, kind="empty"))
     session.bench_roundtrip([1 << i for i in range(n)], 0, 2 * n)
     t = session.last_timeline().astype(np.int64)
+    h = session.last_host_times().astype(np.int64)
     session.dispose()
     assert (t[:, 0] > 0).all()
-    assert (np.diff(t, axis=1) >= 0).all()          # seen <= begin <= end <= finished
+    assert (np.diff(t[:, :4], axis=1) >= 0).all()   # seen <= begin <= end <= finished
+    assert (np.diff(t[:, 5:8], axis=1) >= 0).all()  # clock64: seen <= begin <= finished
     assert np.median(t[:, 3] - t[:, 0]) < 20_000     # device-side handling well under 20 us
+    assert (np.diff(h, axis=1) >= 0).all()           # host: trigger <= written <= FINISHED seen
 
 
 @pytest.mark.slow
