@@ -599,8 +599,8 @@ def main():
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--backoff-ns", type=int, default=0)
     ap.add_argument("--cell-stride", type=int, default=128)
-    ap.add_argument("--poll-mode", choices=["gateway", "direct"], default="gateway")
-    ap.add_argument("--replicas", type=int, default=0, help="0 = mode default")
+    ap.add_argument("--poll-mode", choices=["gateway", "direct"], default="direct")
+    ap.add_argument("--replicas", type=int, default=1)
     ap.add_argument("--spacing-ns", type=int, default=300)
     ap.add_argument("--lsu-payload", action="store_true", help="payload via 128-bit LSU loads, not the TMA ring")
     ap.add_argument("--full-rounds", type=int, default=100_000)

@@ -67,6 +67,10 @@ extern "C" {
 #define LK_KIND_HBM_STREAM        5u  /* out[i] = in0[i], `iterations` passes (>=1) */
 #define LK_KIND_COUNT             6u
 
+/* to_gpu hint bits (top byte of a cell; set by the host from the staged
+ * descriptor of the slot a WORK word names) */
+#define LK_HINT_EMPTY  1u   /* the slot holds an EMPTY descriptor: no descriptor fetch */
+
 /* descriptor flags */
 #define LK_DF_SCALAR   1u   /* pointers not 16-B aligned: scalar path */
 
@@ -104,17 +108,18 @@ typedef struct lk_config {
   uint32_t num_slots;            /* descriptor table entries; 0 = 1024 */
   uint64_t wait_timeout_ns;      /* wait_timeout_s (native.py:52) */
   uint32_t flags;                /* LK_CF_* */
-  uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 4 */
+  uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 1 */
   uint32_t poll_spacing_ns;      /* stagger between replica loads / sweeps; 0 = 300 */
-  uint32_t poll_mode;            /* LK_POLL_GATEWAY (0, default) or LK_POLL_DIRECT */
+  uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default) or LK_POLL_GATEWAY */
 } lk_config;
 
-/* How to_gpu words reach the workers.  GATEWAY: one warp polls a dense host
+/* How to_gpu words reach the workers.  DIRECT: every worker polls its own
+ * host cell (replicas) over PCIe.  GATEWAY: one warp polls a dense host
  * doorbell array for every worker and forwards new values to per-worker
- * mailboxes in device memory (few PCIe reads in flight).  DIRECT: every
- * worker polls its own host cell replicas over PCIe. */
-#define LK_POLL_GATEWAY 0u
-#define LK_POLL_DIRECT  1u
+ * mailboxes in device memory (fewer PCIe reads in flight, one extra L2 hop;
+ * measured slower on the B200 hosts, kept as an option). */
+#define LK_POLL_DIRECT  0u
+#define LK_POLL_GATEWAY 1u
 
 #define LK_CF_ACQUIRE_POLL   1u  /* poll with ld.acquire.sys instead of ld.relaxed.sys */
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */

@@ -40,8 +40,9 @@ CF_ACQUIRE_POLL = 1
 CF_FENCE_ALWAYS = 2
 CF_LSU_PAYLOAD = 4
 CF_TIMELINE = 8
-POLL_GATEWAY = 0
-POLL_DIRECT = 1
+POLL_DIRECT = 0
+POLL_GATEWAY = 1
+HINT_EMPTY = 1
 
 WERR_NAMES = {
     0: "none",

@@ -169,10 +169,11 @@ struct lk_session {
   // One logical to_gpu write: {word, seq} into every replica (seq = this
   // worker's host write index; the device acts only on newer seqs, so the
   // replicas, written one after another, can never step it backwards).
-  inline void host_write(uint32_t i, uint32_t w) {
+  // Cell value {word:32, seq:24, hint:8} (lk_kernels.cu: accept).
+  inline void host_write(uint32_t i, uint32_t w, uint32_t hint = 0) {
     const uint32_t sq = ++host_seq[i];
     if (cfg.record_trace) host_log[i].push_back(HostRec{sq, w, now_ns()});
-    const unsigned long long v = uint64_t(w) | (uint64_t(sq) << 32);
+    const unsigned long long v = uint64_t(w) | (uint64_t(sq & 0xFFFFFFu) << 32) | (uint64_t(hint & 0xFFu) << 56);
     if (gateway) {
       for (uint32_t k = 0; k < replicas; ++k) __atomic_store_n(bell + uint64_t(k) * bell_stride + i, v, __ATOMIC_RELEASE);
       return;
@@ -304,7 +305,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
       cfg.cell_stride != 128)
     return fail(LK_E_CONFIG, "cell_stride must be 8, 16, 32, 64 or 128");
   if (cfg.poll_mode > LK_POLL_DIRECT) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
-  if (cfg.poll_replicas == 0) cfg.poll_replicas = cfg.poll_mode == LK_POLL_GATEWAY ? 2 : 1;
+  if (cfg.poll_replicas == 0) cfg.poll_replicas = 1;
   if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)
     return fail(LK_E_CONFIG, "poll_replicas must be 1, 2, 4 or 8");
   if (cfg.poll_mode == LK_POLL_GATEWAY && cfg.poll_replicas == 8)
@@ -558,7 +559,8 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
     return fail(LK_E_USAGE, "descriptor slot %u not registered", slot);
   }
   const uint32_t word = LK_WORK_BASE + slot;
-  for (uint32_t i : ids) s->host_write(i, word);
+  const uint32_t hint = s->reg_desc[slot].kind == LK_KIND_EMPTY ? LK_HINT_EMPTY : 0u;
+  for (uint32_t i : ids) s->host_write(i, word, hint);
   const uint64_t t1 = now_ns();
   for (uint32_t i : ids) {
     s->host_times[3 * i] = t_call;

@@ -171,7 +171,7 @@ __device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
   if (threadIdx.x == 0) {
     for (uint32_t k = 0; k < kStages; ++k) {
       mbar_init(r.full + k, 1);
-      mbar_init(r.empty + k, T);
+      mbar_init(r.empty + k, T / 32);   // one arrival per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -181,7 +181,7 @@ __device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
 // Stream tiles [0, ntiles) of a chunk through the ring: thread 0 keeps up to
 // kStages-1 tiles ahead; `load(i, stage_ptr, bar)` issues tile i's bulk copies
 // (after arming the barrier with its byte count), `use(i, stage_ptr)` consumes
-// it in every thread.
+// it in every thread, and each warp releases the stage with one arrival.
 template <class Load, class Use>
 __device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntiles, const Load& load,
                                             const Use& use) {
@@ -198,7 +198,8 @@ __device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntile
     const uint32_t c = c0 + i, st = c % kStages;
     mbar_wait(r.full + st, (c / kStages) & 1u);
     use(i, r.buf + st * kStageBytes);
-    mbar_arrive(r.empty + st);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(r.empty + st);
   }
   g = c0 + ntiles;
 }
@@ -448,6 +449,7 @@ struct Elected {           // thread 0's private protocol state
   uint32_t pub;            // word currently in our from_gpu cell
   uint32_t seq;            // host write index of the current to_gpu word
   uint32_t cur;            // current to_gpu word
+  uint32_t hint;           // host hint bits of the current value (LK_HINT_*)
   uint32_t tcnt;
   bool dirty;              // cur not yet stepped to a fixed point
   uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
@@ -487,6 +489,23 @@ __device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* 
   return v;
 }
 
+// A to_gpu value is {word:32, seq:24, hint:8}; seq is the host's per-worker
+// write index mod 2^24 (serial-number compare: a worker is never 2^23 writes
+// behind, every write waits on its handshake) and is widened back to 32 bits
+// here, so trace records carry the host's full write index.
+__device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool timeline) {
+  const uint32_t sq = uint32_t(c >> 32) & 0xFFFFFFu;
+  const uint32_t delta = (sq - e.seq) & 0xFFFFFFu;
+  if (delta == 0 || delta >= 0x800000u) return false;
+  e.seq += delta;
+  e.cur = uint32_t(c);
+  e.hint = uint32_t(c >> 56);
+  e.dirty = true;
+  e.c_seen = clock64();
+  if (timeline) e.t_seen = globaltimer();
+  return true;
+}
+
 // Step the current word to a fixed point, exactly as the reference worker
 // re-reads a level-triggered cell until it stops making progress
 // (native.py:158-195).  Returns an action, or LK_ACT_NONE once settled.
@@ -522,6 +541,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
   const unsigned long long* base = a.to_gpu + uint64_t(wid) * K * a.cell_u64;
   const uint32_t step = a.cell_u64;
   const bool acquire = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
+  const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
   for (;;) {
     const uint32_t act = settle(a, wid, e);
     if (act != LK_ACT_NONE) return act;
@@ -534,13 +554,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
     for (bool fresh = false; !fresh;) {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const unsigned long long c = v[k];
-        if (uint32_t(c >> 32) > e.seq) {
-          e.seq = uint32_t(c >> 32);
-          e.cur = uint32_t(c);
-          e.dirty = true;
-          e.t_seen = globaltimer();
-          e.c_seen = clock64();
+        if (accept(e, v[k], timeline)) {
           fresh = true;
           break;
         }
@@ -557,18 +571,13 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
 // (written by the gateway warp); poll it in L2, one load in flight.
 __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t wid, Elected& e) {
   const unsigned long long* mb = a.dmb + uint64_t(wid) * a.dmb_u64;
+  const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
   for (;;) {
     const uint32_t act = settle(a, wid, e);
     if (act != LK_ACT_NONE) return act;
     for (;;) {
-      const unsigned long long c = ld_relaxed_gpu64(mb);
-      if (uint32_t(c >> 32) > e.seq) {
-        e.seq = uint32_t(c >> 32);
-        e.cur = uint32_t(c);
-        e.dirty = true;
-        e.t_seen = globaltimer();
-        e.c_seen = clock64();
-        if (a.flags & LK_CF_TIMELINE) e.t_fwd = ld_relaxed_gpu64(mb + 1);
+      if (accept(e, ld_relaxed_gpu64(mb), timeline)) {
+        if (timeline) e.t_fwd = ld_relaxed_gpu64(mb + 1);
         break;
       }
       if (a.backoff_ns) __nanosleep(a.backoff_ns);
@@ -576,7 +585,8 @@ __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t 
   }
 }
 
-__device__ __noinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e) {
+// Inlined into the worker loop so the protocol state stays in registers.
+__device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e) {
   if (a.poll_mode == LK_POLL_GATEWAY) return poll_mailbox(a, wid, e);
   switch (a.replicas) {
     case 1: return poll_k<1>(a, wid, e);
@@ -610,9 +620,9 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
       if (cell(j) < nw) v[k][j] = ld_relaxed_sys_v2(a.bell + uint64_t(k) * a.bell_stride + cell(j));
   };
   auto fwd = [&](uint32_t c, unsigned long long val, uint32_t& seen) {
-    const uint32_t sq = uint32_t(val >> 32);
-    if (c < nw && sq > seen) {
-      seen = sq;
+    const uint32_t delta = (uint32_t(val >> 32) - seen) & 0xFFFFFFu;   // 24-bit serial compare
+    if (c < nw && delta != 0 && delta < 0x800000u) {
+      seen += delta;
       if (a.flags & LK_CF_TIMELINE) st_relaxed_gpu64(a.dmb + uint64_t(c) * a.dmb_u64 + 1, globaltimer());
       st_relaxed_gpu64(a.dmb + uint64_t(c) * a.dmb_u64, val);
     }
@@ -661,11 +671,13 @@ __device__ __noinline__ void gateway(const lk_dev_args& a) {
 // Per-worker record of the last dispatch (lk_last_timeline): globaltimer at
 // value seen / work begin / work end / FINISHED issued, gateway forward time,
 // and clock64 at seen / work begin / FINISHED issued.
+// globaltimer reads cost a few hundred cycles each, so the single-thread
+// (latency) kinds stamp clock64 only unless LK_CF_TIMELINE asks for both.
 __device__ __forceinline__ void write_timeline(const lk_dev_args& a, uint32_t wid, const Elected& e,
                                                uint64_t t_begin, uint64_t t_end, uint64_t c_begin,
-                                               uint64_t c_fin) {
+                                               uint64_t c_fin, bool globaltime) {
   unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
-  tl[0] = e.t_seen; tl[1] = t_begin; tl[2] = t_end; tl[3] = globaltimer();
+  tl[0] = e.t_seen; tl[1] = t_begin; tl[2] = t_end; tl[3] = globaltime ? globaltimer() : 0;
   tl[4] = e.t_fwd; tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
 }
 
@@ -676,7 +688,7 @@ struct PersistSmem {
   uint64_t full[kStages], empty[kStages];
 };
 
-__global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const lk_dev_args a) {
+__global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const __grid_constant__ lk_dev_args a) {
   __shared__ PersistSmem sm;
   const uint32_t wid = blockIdx.x;
   const uint32_t T = a.wthreads;
@@ -694,6 +706,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.pub = LK_NOP;  // cells start at the NOP sentinel (protocol.py:217-218)
   e.seq = 0;       // the host's initial {NOP, seq 0} value
   e.cur = LK_NOP;
+  e.hint = 0;
   e.tcnt = 0;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   e.t_seen = 0;
@@ -709,6 +722,17 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
         if (act == LK_ACT_EXIT) { sm.cmd = kCmdExit; break; }
         const uint32_t slot = e.st.slot;
         if (slot >= a.num_slots) { report_error(a, wid, e, LK_WERR_BAD_SLOT, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
+        if (e.hint & LK_HINT_EMPTY) {
+          // the host staged an EMPTY descriptor in this slot and said so in the
+          // word's hint bits: complete without the descriptor round trip to L2
+          const uint64_t c_begin_e = clock64();
+          const bool tl = (a.flags & LK_CF_TIMELINE) != 0;
+          const uint64_t t_b = tl ? globaltimer() : 0;
+          const lk_step_out o = lk_complete_work(e.st);
+          publish(a, wid, e, o.publish, (a.flags & LK_CF_FENCE_ALWAYS) != 0);
+          write_timeline(a, wid, e, t_b, t_b, c_begin_e, clock64(), tl);
+          continue;
+        }
         lk_desc d;
         {
           const uint4* src = reinterpret_cast<const uint4*>(a.desc + slot);
@@ -718,14 +742,14 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
         }
         if (d.kind >= LK_KIND_COUNT) { report_error(a, wid, e, LK_WERR_BAD_KIND, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
         if (single_thread_kind(d.kind)) {
+          const bool tl = (a.flags & LK_CF_TIMELINE) != 0;
           c_begin = clock64();
-          t_begin = globaltimer();
+          t_begin = tl ? globaltimer() : 0;
           if (d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
-          const uint64_t t_end = globaltimer();
+          const uint64_t t_end = tl ? globaltimer() : 0;
           const lk_step_out o = lk_complete_work(e.st);
           publish(a, wid, e, o.publish, (a.flags & LK_CF_FENCE_ALWAYS) != 0);
-          const uint64_t c_fin = clock64();
-          write_timeline(a, wid, e, t_begin, t_end, c_begin, c_fin);
+          write_timeline(a, wid, e, t_begin, t_end, c_begin, clock64(), tl);
           continue;
         }
         // payload item: rank/count from the slot's trigger mask
@@ -757,7 +781,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
       const uint64_t t_end = globaltimer();
       const lk_step_out o = lk_complete_work(e.st);
       publish(a, wid, e, o.publish, true);  // payload visible before FINISHED
-      write_timeline(a, wid, e, t_begin, t_end, c_begin, clock64());
+      write_timeline(a, wid, e, t_begin, t_end, c_begin, clock64(), true);
     }
   }
   if (threadIdx.x == 0) atomicAdd(a.exited, 1u);   // lets the gateway retire
@@ -794,7 +818,8 @@ __global__ void lk_clocksync_kernel(const uint32_t* flag, unsigned long long* ec
     while (ld_relaxed_sys(flag) != r) {
     }
     st_relaxed_sys(echo, globaltimer());
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(echo + 1), "r"(r) : "memory");
+    // same 128-B line, posted in order: no release fence (MEMBAR.SYS would skew the echo)
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(echo + 1), "r"(r) : "memory");
   }
 }
 

@@ -58,8 +58,9 @@ class NativeConfig:
     threads_per_worker: int = 512
     poll_backoff_ns: int = 0
     cell_stride: int = 128
-    poll_mode: str = "gateway"      # "gateway": one warp polls all host cells, forwards via L2; "direct"
-    poll_replicas: int = 0          # 0 = default (gateway 2, direct 1)
+    poll_mode: str = "direct"       # "direct": each worker polls its host cell; "gateway": one warp
+                                    # polls all host cells and forwards through device memory
+    poll_replicas: int = 1          # to_gpu replicas polled per worker (gateway: doorbell sweeps)
     poll_spacing_ns: int = 300
     num_slots: int = 1024
     trace_capacity: int = 65536

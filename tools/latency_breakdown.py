@@ -15,13 +15,12 @@ from paper_2310_01212_b200.device import WorkDescriptor  # noqa: E402
 native.pin_host_thread(0)
 
 
-def breakdown(label, rounds=20000, **kw):
-    s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, timeline=True, **kw))
+def breakdown(label, rounds=20000, timeline=True, **kw):
+    s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, timeline=timeline, **kw))
     n = s.num_workers
     s.register(WorkDescriptor(slot=0, kind="empty"))
     masks = [1 << i for i in range(n)]
     s.bench_roundtrip(masks, 0, 2000)
-    off0, rtt0 = native.clock_offset(0, 500) if False else (None, None)
     _, done, _ = s.bench_roundtrip(masks, 0, rounds)
     t = s.last_timeline().astype(np.int64)
     h = s.last_host_times().astype(np.int64)
@@ -50,6 +49,7 @@ def breakdown(label, rounds=20000, **kw):
 
 
 if __name__ == "__main__":
+    breakdown("direct K=1 (no globaltimer)", timeline=False, poll_mode="direct", poll_replicas=1)
     breakdown("direct K=1", poll_mode="direct", poll_replicas=1)
     breakdown("direct K=2", poll_mode="direct", poll_replicas=2)
     breakdown("gateway K=1", poll_mode="gateway", poll_replicas=1)
