@@ -118,9 +118,14 @@ struct lk_session {
   // pinned mapped host block
   uint8_t* host_block = nullptr;
   unsigned long long* to_gpu = nullptr;       // DIRECT: worker i replica k at [(i*replicas+k)*cell_u64]
-  unsigned long long* bell = nullptr;         // GATEWAY: replica k, worker i at [k*bell_stride + i]
-  uint32_t bell_stride = 0;
-  bool gateway = true;
+  unsigned long long* ring = nullptr;         // GATEWAY: event ring replicas (8 u64 per entry)
+  volatile unsigned long long* gw_tail = nullptr;   // GATEWAY: events consumed (device-written)
+  uint32_t ring_entries = 256;
+  uint32_t ev_head = 0;                       // GATEWAY: events appended
+  std::vector<uint32_t> last_word;            // GATEWAY: shadow of each worker's to_gpu value
+  std::mutex post_mu;
+  std::vector<uint32_t> all_ids;
+  bool gateway = false;
   volatile unsigned long long* status = nullptr;  // stride cell_u64
   volatile unsigned long long* err = nullptr;
   volatile uint32_t* err_any = nullptr;
@@ -169,20 +174,50 @@ struct lk_session {
   // One logical to_gpu write: {word, seq} into every replica (seq = this
   // worker's host write index; the device acts only on newer seqs, so the
   // replicas, written one after another, can never step it backwards).
-  // Cell value {word:32, seq:24, hint:8} (lk_kernels.cu: accept).
+  // DIRECT: one worker's cell value {word:32, seq:24, hint:8} (lk_kernels.cu: accept).
   inline void host_write(uint32_t i, uint32_t w, uint32_t hint = 0) {
     const uint32_t sq = ++host_seq[i];
     if (cfg.record_trace) host_log[i].push_back(HostRec{sq, w, now_ns()});
     const unsigned long long v = uint64_t(w) | (uint64_t(sq & 0xFFFFFFu) << 32) | (uint64_t(hint & 0xFFu) << 56);
-    if (gateway) {
-      for (uint32_t k = 0; k < replicas; ++k) __atomic_store_n(bell + uint64_t(k) * bell_stride + i, v, __ATOMIC_RELEASE);
-      return;
-    }
     unsigned long long* c = to_gpu + uint64_t(i) * replicas * cell_u64;
     for (uint32_t k = 0; k < replicas; ++k) __atomic_store_n(c + k * cell_u64, v, __ATOMIC_RELEASE);
   }
+  // One logical write of `w` to every worker in ids (ascending), i.e. the
+  // reference's `for i in sm_ids: _host_write(i, word)` (native.py:224-225).
+  // GATEWAY: a single ring event carries the word and the worker mask.
+  // Returns false if the ring stayed full past the timeout.
+  bool post(const std::vector<uint32_t>& ids, uint32_t w, uint32_t hint = 0) {
+    if (!gateway) {
+      for (uint32_t i : ids) host_write(i, w, hint);
+      return true;
+    }
+    std::lock_guard<std::mutex> g(post_mu);   // trigger and wait may run on different host threads
+    const uint64_t deadline = now_ns() + cfg.wait_timeout_ns;
+    while (ev_head - uint32_t(*gw_tail) >= ring_entries - 1) {   // flow control
+      LK_PAUSE();
+      if (now_ns() > deadline) return false;
+    }
+    const uint32_t seq = ++ev_head;
+    const uint64_t tag = uint64_t(seq & 0xFFFFu) << 48;
+    uint64_t mw[4] = {0, 0, 0, 0};
+    const uint64_t t = cfg.record_trace ? now_ns() : 0;
+    for (uint32_t i : ids) {
+      mw[i / 48] |= 1ull << (i % 48);
+      const uint32_t sq = ++host_seq[i];
+      last_word[i] = w;
+      if (cfg.record_trace) host_log[i].push_back(HostRec{sq, w, t});
+    }
+    const uint32_t e = (seq - 1) % ring_entries;
+    for (uint32_t k = 0; k < replicas; ++k) {
+      unsigned long long* ent = ring + (uint64_t(k) * ring_entries + e) * 8;
+      for (int j = 0; j < 4; ++j) __atomic_store_n(ent + 1 + j, mw[j] | tag, __ATOMIC_RELAXED);
+      __atomic_store_n(ent + 5, uint64_t(hint & 0xFFu) | tag, __ATOMIC_RELAXED);
+      __atomic_store_n(ent, uint64_t(seq) | (uint64_t(w) << 32), __ATOMIC_RELEASE);   // last: publishes the entry
+    }
+    return true;
+  }
   inline uint32_t to_gpu_word(uint32_t i) const {
-    if (gateway) return uint32_t(__atomic_load_n(bell + i, __ATOMIC_ACQUIRE));
+    if (gateway) return last_word[i];
     return uint32_t(__atomic_load_n(to_gpu + uint64_t(i) * replicas * cell_u64, __ATOMIC_ACQUIRE));
   }
 };
@@ -304,12 +339,12 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.cell_stride != 8 && cfg.cell_stride != 16 && cfg.cell_stride != 32 && cfg.cell_stride != 64 &&
       cfg.cell_stride != 128)
     return fail(LK_E_CONFIG, "cell_stride must be 8, 16, 32, 64 or 128");
-  if (cfg.poll_mode > LK_POLL_DIRECT) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
+  if (cfg.poll_mode > LK_POLL_GATEWAY) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
   if (cfg.poll_replicas == 0) cfg.poll_replicas = 1;
   if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)
     return fail(LK_E_CONFIG, "poll_replicas must be 1, 2, 4 or 8");
   if (cfg.poll_mode == LK_POLL_GATEWAY && cfg.poll_replicas == 8)
-    return fail(LK_E_CONFIG, "gateway mode takes 1, 2 or 4 doorbell replicas");
+    return fail(LK_E_CONFIG, "gateway mode takes 1, 2 or 4 event-ring replicas");
   if (cfg.poll_spacing_ns == 0) cfg.poll_spacing_ns = 300;
   if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 512;
   if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 608)
@@ -340,7 +375,12 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->cell_u64 = cfg.cell_stride / 8;
   s->replicas = cfg.poll_replicas;
   s->gateway = cfg.poll_mode == LK_POLL_GATEWAY;
-  s->bell_stride = (s->nw + 63) / 64 * 64;
+  s->last_word.assign(s->nw, LK_NOP);
+  for (uint32_t i = 0; i < s->nw; ++i) s->all_ids.push_back(i);
+  if (s->gateway && s->nw > 192) {
+    delete s;
+    return fail(LK_E_CONFIG, "gateway mode supports up to 192 workers (4 x 48-bit event masks)");
+  }
   s->pending.assign(s->nwords, 0);
   s->registered.assign(cfg.num_slots, 0);
   s->slot_pend.assign(size_t(cfg.num_slots) * s->nwords, 0);
@@ -366,7 +406,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   // --- pinned mapped mailboxes: to_gpu (DIRECT replicas | GATEWAY doorbell
   // replicas) | status | err | smid, 4 KiB aligned
   auto al = [](size_t x) { return (x + 4095) & ~size_t(4095); };
-  const size_t tob = s->gateway ? al(size_t(s->replicas) * s->bell_stride * 8)
+  const size_t tob = s->gateway ? al(size_t(s->replicas) * s->ring_entries * 64 + 128)
                                 : al(size_t(s->nw) * s->replicas * cfg.cell_stride);
   const size_t cells = al(size_t(s->nw) * cfg.cell_stride);
   const size_t err_words = (size_t(s->nw) + 15) / 16 * 16;   // err[] then err_any on its own line
@@ -377,15 +417,15 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(ce)));
   memset(s->host_block, 0, host_bytes);
   s->to_gpu = reinterpret_cast<unsigned long long*>(s->host_block);
-  s->bell = s->to_gpu;
+  s->ring = s->to_gpu;
+  s->gw_tail = s->to_gpu + size_t(s->replicas) * s->ring_entries * 8;   // own line after the rings
   s->status = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob);
   s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob + cells);
   s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + tob + cells + errb);
   s->err_any = reinterpret_cast<volatile uint32_t*>(s->err + err_words);
   for (uint32_t i = 0; i < s->nw; ++i) {
     for (uint32_t k = 0; k < s->replicas; ++k) {
-      if (s->gateway) s->bell[uint64_t(k) * s->bell_stride + i] = LK_NOP;   // {NOP, seq 0}
-      else s->to_gpu[(uint64_t(i) * s->replicas + k) * s->cell_u64] = LK_NOP;
+      if (!s->gateway) s->to_gpu[(uint64_t(i) * s->replicas + k) * s->cell_u64] = LK_NOP;   // {NOP, seq 0}
     }
     s->status[uint64_t(i) * s->cell_u64] = uint64_t(LK_NOP) | (uint64_t(LK_PHASE_BOOTING) << 32);
     s->smid[i] = 0xFFFFFFFFu;
@@ -459,10 +499,11 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.record_trace = cfg.record_trace ? 1 : 0;
   a.backoff_ns = cfg.poll_backoff_ns;
   a.flags = cfg.flags;
-  a.bell = s->bell;
+  a.ring = s->ring;
+  a.gw_tail = const_cast<unsigned long long*>(s->gw_tail);
   a.dmb = s->d_dmb;
   a.exited = s->d_exited;
-  a.bell_stride = s->bell_stride;
+  a.ring_entries = s->ring_entries;
   a.dmb_u64 = 16;
   a.nw = s->nw;
   a.wthreads = s->threads;
@@ -560,7 +601,7 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   }
   const uint32_t word = LK_WORK_BASE + slot;
   const uint32_t hint = s->reg_desc[slot].kind == LK_KIND_EMPTY ? LK_HINT_EMPTY : 0u;
-  for (uint32_t i : ids) s->host_write(i, word, hint);
+  if (!s->post(ids, word, hint)) return fail(LK_E_HANG, "event ring full: gateway not consuming");
   const uint64_t t1 = now_ns();
   for (uint32_t i : ids) {
     s->host_times[3 * i] = t_call;
@@ -600,7 +641,7 @@ static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::
   if (rc) return rc;
   const uint64_t finished_at = now_ns();
   for (uint32_t i : ids) s->host_times[3 * i + 2] = finished_at;
-  for (uint32_t i : ids) s->host_write(i, LK_NOP);
+  if (!s->post(ids, LK_NOP)) return fail(LK_E_HANG, "event ring full: gateway not consuming");
   rc = spin_words(s, ids, LK_NOP, "wait for ack consumption");
   if (rc) return rc;
   {
@@ -676,7 +717,7 @@ extern "C" int lk_dispose(lk_session* s, uint64_t* elapsed_ns) {
     if (s->pending[i >> 6] >> (i & 63) & 1) busy.push_back(i);
   if (!busy.empty()) return fail(LK_E_DISPOSE_BUSY, "worker(s) %s still working", ids_str(busy).c_str());
   const uint64_t t0 = now_ns();
-  for (uint32_t i = 0; i < s->nw; ++i) s->host_write(i, LK_EXIT);
+  if (!s->post(s->all_ids, LK_EXIT)) return fail(LK_E_HANG, "event ring full: gateway not consuming");
   const uint64_t deadline = t0 + s->cfg.wait_timeout_ns;
   for (;;) {
     const int ks = kernel_status(s);
@@ -700,7 +741,7 @@ extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
     s->disposed = true;
     return LK_OK;
   }
-  for (uint32_t i = 0; i < s->nw; ++i) s->host_write(i, LK_EXIT);
+  s->post(s->all_ids, LK_EXIT);
   const uint64_t deadline = now_ns() + (timeout_ns ? timeout_ns : s->cfg.wait_timeout_ns);
   for (;;) {
     const int ks = kernel_status(s);
@@ -745,7 +786,7 @@ extern "C" int lk_read_cells(lk_session* s, uint32_t* to_gpu, uint32_t* from_gpu
 extern "C" int lk_debug_poke(lk_session* s, uint32_t worker, uint32_t word) {
   if (!s || worker >= s->nw) return fail(LK_E_USAGE, "bad worker");
   std::lock_guard<std::mutex> g(s->mu);
-  s->host_write(worker, word);
+  s->post(std::vector<uint32_t>{worker}, word);
   return LK_OK;
 }
 

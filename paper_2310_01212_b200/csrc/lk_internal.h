@@ -27,11 +27,12 @@ struct lk_dev_args {
   uint32_t* reduce_ctr;            // device, num_slots
   unsigned long long* spans;       // device, LK_TIMELINE_WORDS per worker: the last dispatch's
                                    // timeline (lk_last_timeline)
-  const unsigned long long* bell;  // host-mapped doorbell (GATEWAY): replica k, worker i at
-                                   // bell[k*bell_stride + i] = word | seq<<32
+  const unsigned long long* ring;  // host-mapped event ring (GATEWAY): replica k, entry e at
+                                   // ring[(k*ring_entries + e)*8], 8 u64 per entry
+  unsigned long long* gw_tail;     // host-mapped: events the gateway has consumed
   unsigned long long* dmb;         // device mailboxes (GATEWAY), worker i at dmb[i*dmb_u64]
   uint32_t* exited;                // device: workers that left their loop
-  uint32_t bell_stride;            // cells per doorbell replica (multiple of 64)
+  uint32_t ring_entries;           // entries per event-ring replica
   uint32_t dmb_u64;
   uint32_t nw;                     // workers
   uint32_t wthreads;               // worker threads per CTA (the gateway warp comes after)

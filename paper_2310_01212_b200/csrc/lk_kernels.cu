@@ -597,35 +597,37 @@ __device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Ele
 }
 
 // ---------------------------------------------------------------- gateway
-// One warp samples every worker's to_gpu cell in the dense host doorbell
-// array: lane l covers cells {64j + 2l, 64j + 2l + 1} (16-B loads, j < J <= 4,
-// so up to 256 workers), K replica arrays swept one after another, spaced
-// spacing_ns, one sweep per replica in flight.  A cell whose seq is newer
-// than the last forwarded one is copied to the worker's mailbox line in
-// device memory (relaxed: the descriptor a WORK word names was staged by a
-// completed DMA before the host wrote the word).  Exits once every worker
-// has left its loop.
-template <int K, int J>
+// GATEWAY mode.  The host does not write per-worker cells; it appends one
+// event per logical write (a trigger, an ack, EXIT) to a ring in pinned host
+// memory: entry = 8 u64 on one 64-B line,
+//   w[0] = seq:32 | word:32           (written last: the "new event" signal)
+//   w[1..4] = mask bits [48j, 48j+48) | tag:16 << 48
+//   w[5] = hint | tag:16 << 48        (tag = seq & 0xFFFF: torn-read check)
+// in K replica rings.  One warp of CTA 0 polls the entry it expects next on
+// each replica, one load per lane (lanes 0..5) in flight per replica,
+// staggered spacing_ns.  The PCIe link therefore carries ~6K small reads in
+// flight instead of one per worker, which is what kept the per-read round
+// trip long in DIRECT mode.  An accepted event is fanned out to every masked
+// worker's mailbox line in device memory ({word, per-worker seq24, hint}, the
+// same value DIRECT mode reads from host memory), and the consumed count is
+// posted back to the host (ring flow control).  Exits once every worker has
+// left its loop.
+constexpr uint32_t kRingMaskBits = 48;
+constexpr uint32_t kRingMaxWorkers = 4 * kRingMaskBits;   // 192
+
+template <int K>
 __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t nw = a.nw;
-  uint32_t last[2 * J];
+  const uint32_t nw = a.nw, N = a.ring_entries;
+  const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
+  uint32_t wseq[6];                               // per-worker write counts, workers lane + 32q
 #pragma unroll
-  for (int i = 0; i < 2 * J; ++i) last[i] = 0;
-  ulonglong2 v[K][J];
-  auto cell = [&](int j) { return uint32_t(64 * j) + 2 * lane; };
+  for (int q = 0; q < 6; ++q) wseq[q] = 0;
+  uint32_t expect = 1;                            // next event seq
+  unsigned long long v[K];
   auto issue = [&](int k) {
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-      if (cell(j) < nw) v[k][j] = ld_relaxed_sys_v2(a.bell + uint64_t(k) * a.bell_stride + cell(j));
-  };
-  auto fwd = [&](uint32_t c, unsigned long long val, uint32_t& seen) {
-    const uint32_t delta = (uint32_t(val >> 32) - seen) & 0xFFFFFFu;   // 24-bit serial compare
-    if (c < nw && delta != 0 && delta < 0x800000u) {
-      seen += delta;
-      if (a.flags & LK_CF_TIMELINE) st_relaxed_gpu64(a.dmb + uint64_t(c) * a.dmb_u64 + 1, globaltimer());
-      st_relaxed_gpu64(a.dmb + uint64_t(c) * a.dmb_u64, val);
-    }
+    if (lane < 6)
+      v[k] = ld_cell(a.ring + (uint64_t(k) * N + (expect - 1) % N) * 8 + lane, false);
   };
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -635,36 +637,46 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
   for (uint32_t it = 0;; ++it) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
+      // lanes 0..5 hold the 6 words of the entry this replica load saw
+      const unsigned long long w = lane < 6 ? v[k] : 0ull;
+      const unsigned long long w0 = __shfl_sync(0xffffffffu, w, 0);
+      const uint32_t tag = expect & 0xFFFFu;
+      const bool mine = lane == 0 ? uint32_t(w0) == expect
+                                  : (lane < 6 ? uint32_t(w >> 48) == tag : true);
+      if (__all_sync(0xffffffffu, mine)) {
+        const uint32_t word = uint32_t(w0 >> 32);
+        const uint32_t hint = uint32_t(__shfl_sync(0xffffffffu, w, 5)) & 0xFFu;
+        unsigned long long m[4];
 #pragma unroll
-      for (int j = 0; j < J; ++j) {
-        if (cell(j) < nw) {
-          fwd(cell(j), v[k][j].x, last[2 * j]);
-          fwd(cell(j) + 1, v[k][j].y, last[2 * j + 1]);
+        for (int j = 0; j < 4; ++j) m[j] = __shfl_sync(0xffffffffu, w, j + 1) & ((1ull << kRingMaskBits) - 1);
+        const uint64_t t_fwd = timeline ? globaltimer() : 0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const uint32_t i = lane + 32u * q;
+          if (i < nw && (m[i / kRingMaskBits] >> (i % kRingMaskBits) & 1ull)) {
+            ++wseq[q];
+            unsigned long long* mb = a.dmb + uint64_t(i) * a.dmb_u64;
+            if (timeline) st_relaxed_gpu64(mb + 1, t_fwd);
+            st_relaxed_gpu64(mb, uint64_t(word) | (uint64_t(wseq[q] & 0xFFFFFFu) << 32) |
+                                     (uint64_t(hint) << 56));
+          }
         }
+        if (lane == 0) st_relaxed_sys(a.gw_tail, expect);   // consumed: ring slot reusable
+        ++expect;
       }
       issue(k);
       if (K > 1) __nanosleep(a.spacing_ns);
       else if (a.backoff_ns) __nanosleep(a.backoff_ns);
     }
-    if ((it & 31u) == 0 && ld_relaxed_gpu32(a.exited) >= nw) return;
-  }
-}
-
-template <int J>
-__device__ __forceinline__ void gateway_j(const lk_dev_args& a) {
-  switch (a.replicas) {
-    case 1: gateway_k<1, J>(a); return;
-    case 4: gateway_k<4, J>(a); return;
-    default: gateway_k<2, J>(a); return;
+    if ((it & 63u) == 0 && ld_relaxed_gpu32(a.exited) >= nw) return;
   }
 }
 
 __device__ __noinline__ void gateway(const lk_dev_args& a) {
-  switch ((a.nw + 63) / 64) {
-    case 1: gateway_j<1>(a); return;
-    case 2: gateway_j<2>(a); return;
-    case 3: gateway_j<3>(a); return;
-    default: gateway_j<4>(a); return;
+  switch (a.replicas) {
+    case 1: gateway_k<1>(a); return;
+    case 4: gateway_k<4>(a); return;
+    default: gateway_k<2>(a); return;
   }
 }
 

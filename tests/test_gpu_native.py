@@ -324,6 +324,23 @@ def test_poll_modes_random_programs(mode, replicas):
     assert_trace_ok(session, program, 12)
 
 
+@pytest.mark.parametrize("replicas", [1, 2])
+def test_gateway_back_to_back_single_worker_triggers(replicas):
+    """148 separate trigger events queued before any wait, then one ack event
+    for the whole mask: the event ring carries them all in order."""
+    session = start(None, trace_capacity=256, poll_mode="gateway", poll_replicas=replicas)
+    n = session.num_workers
+    work = WorkDescriptor(slot=0, kind="empty")
+    for rep in range(3):
+        for i in range(n):
+            session.trigger(1 << i, WorkDescriptor(slot=1 + (i % 64) + 64 * (rep % 2), iterations=i % 7))
+        session.wait((1 << n) - 1)
+    session.trigger(1, work)
+    session.wait(1)
+    session.dispose()
+    assert_trace_ok(session)
+
+
 def test_device_timeline_is_ordered():
     session = start(None)
     n = session.num_workers

@@ -49,10 +49,12 @@ def breakdown(label, rounds=20000, timeline=True, **kw):
 
 
 if __name__ == "__main__":
-    breakdown("direct K=1 (no globaltimer)", timeline=False, poll_mode="direct", poll_replicas=1)
+    breakdown("direct K=1 (clock64 only)", timeline=False, poll_mode="direct", poll_replicas=1)
     breakdown("direct K=1", poll_mode="direct", poll_replicas=1)
-    breakdown("direct K=2", poll_mode="direct", poll_replicas=2)
-    breakdown("gateway K=1", poll_mode="gateway", poll_replicas=1)
-    breakdown("gateway K=2", poll_mode="gateway", poll_replicas=2)
+    for k in (1, 2, 4):
+        breakdown(f"gateway K={k} (clock64 only)", timeline=False, poll_mode="gateway", poll_replicas=k)
+        breakdown(f"gateway K={k}", poll_mode="gateway", poll_replicas=k)
+    breakdown("gateway K=2 d=150", poll_mode="gateway", poll_replicas=2, poll_spacing_ns=150)
+    breakdown("gateway K=2 d=600", poll_mode="gateway", poll_replicas=2, poll_spacing_ns=600)
     breakdown("direct K=1 16w", poll_mode="direct", poll_replicas=1, num_workers=16)
-    breakdown("gateway K=1 16w", poll_mode="gateway", poll_replicas=1, num_workers=16)
+    breakdown("gateway K=2 16w", poll_mode="gateway", poll_replicas=2, num_workers=16)
