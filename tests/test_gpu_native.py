@@ -333,7 +333,7 @@ def test_gateway_back_to_back_single_worker_triggers(replicas):
     work = WorkDescriptor(slot=0, kind="empty")
     for rep in range(3):
         for i in range(n):
-            session.trigger(1 << i, WorkDescriptor(slot=1 + (i % 64) + 64 * (rep % 2), iterations=i % 7))
+            session.trigger(1 << i, WorkDescriptor(slot=1 + i + 150 * (rep % 2), iterations=i % 7))
         session.wait((1 << n) - 1)
     session.trigger(1, work)
     session.wait(1)
