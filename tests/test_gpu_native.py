@@ -341,8 +341,9 @@ def test_gateway_back_to_back_single_worker_triggers(replicas):
     assert_trace_ok(session)
 
 
-def test_device_timeline_is_ordered():
-    session = start(None)
+@pytest.mark.parametrize("mode", ["direct", "gateway"])
+def test_device_timeline_is_ordered(mode):
+    session = start(None, timeline=True, poll_mode=mode)
     n = session.num_workers
     session.register(WorkDescriptor(slot=0, kind="empty"))
     session.bench_roundtrip([1 << i for i in range(n)], 0, 2 * n)
@@ -351,6 +352,8 @@ def test_device_timeline_is_ordered():
     session.dispose()
     assert (t[:, 0] > 0).all()
     assert (np.diff(t[:, :4], axis=1) >= 0).all()   # seen <= begin <= end <= finished
+    if mode == "gateway":
+        assert (t[:, 4] > 0).all() and (t[:, 4] <= t[:, 0]).all()   # forwarded before seen
     assert (np.diff(t[:, 5:8], axis=1) >= 0).all()  # clock64: seen <= begin <= finished
     assert np.median(t[:, 3] - t[:, 0]) < 20_000     # device-side handling well under 20 us
     assert (np.diff(h, axis=1) >= 0).all()           # host: trigger <= written <= FINISHED seen
