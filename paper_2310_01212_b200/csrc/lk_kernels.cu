@@ -506,6 +506,46 @@ __device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool ti
   return true;
 }
 
+__device__ __forceinline__ void publish_fast(const lk_dev_args& a, uint32_t wid, uint32_t word,
+                                             uint32_t phase) {
+  st_relaxed_sys(a.status + uint64_t(wid) * a.cell_u64, uint64_t(word) | (uint64_t(phase) << 32));
+}
+
+// The two transitions every empty-task round trip makes, settled in place
+// right where the new value was seen (no descriptor fetch, no trip through
+// the general dispatch code and its cold instruction-cache lines):
+//   IDLE x WORK(s), slot s staged EMPTY (hint) -> publish WORKING, FINISHED;
+//      re-stepping the same word in FINISHED publishes FINISHED again (a no-op)
+//   FINISHED x NOP -> publish NOP, IDLE; re-stepping NOP in IDLE is a no-op.
+// Exactly lk_worker_step + lk_complete_work for these cases (protocol.py:151-206);
+// anything else -- and every case while a trace is recorded -- takes settle().
+__device__ __forceinline__ bool fast_step(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  if (a.record_trace | (a.flags & LK_CF_FENCE_ALWAYS)) return false;
+  const uint32_t w = e.cur;
+  if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && (e.hint & LK_HINT_EMPTY) &&
+      w - LK_WORK_BASE < a.num_slots) {
+    const uint64_t c_begin = clock64();
+    publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
+    publish_fast(a, wid, LK_FINISHED, LK_PHASE_FINISHED);
+    const uint64_t c_fin = clock64();
+    e.st = lk_wstate{LK_PHASE_FINISHED, w - LK_WORK_BASE};
+    e.pub = LK_FINISHED;
+    e.dirty = false;
+    unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
+    tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
+    if (a.flags & LK_CF_TIMELINE) { tl[0] = e.t_seen; tl[4] = e.t_fwd; }
+    return true;
+  }
+  if (e.st.phase == LK_PHASE_FINISHED && w == LK_NOP) {
+    publish_fast(a, wid, LK_NOP, LK_PHASE_IDLE);
+    e.st.phase = LK_PHASE_IDLE;
+    e.pub = LK_NOP;
+    e.dirty = false;
+    return true;
+  }
+  return false;
+}
+
 // Step the current word to a fixed point, exactly as the reference worker
 // re-reads a level-triggered cell until it stops making progress
 // (native.py:158-195).  Returns an action, or LK_ACT_NONE once settled.
@@ -555,8 +595,10 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (accept(e, v[k], timeline)) {
-          fresh = true;
-          break;
+          fresh = !fast_step(a, wid, e);   // fast path settled it: keep polling
+          if (fresh) break;
+          v[k] = ld_cell(base + k * step, acquire);
+          continue;
         }
         v[k] = ld_cell(base + k * step, acquire);
         if (K > 1) __nanosleep(a.spacing_ns);
@@ -578,7 +620,8 @@ __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t 
     for (;;) {
       if (accept(e, ld_relaxed_gpu64(mb), timeline)) {
         if (timeline) e.t_fwd = ld_relaxed_gpu64(mb + 1);
-        break;
+        if (!fast_step(a, wid, e)) break;
+        continue;
       }
       if (a.backoff_ns) __nanosleep(a.backoff_ns);
     }
@@ -792,7 +835,15 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();
       const lk_step_out o = lk_complete_work(e.st);
-      publish(a, wid, e, o.publish, true);  // payload visible before FINISHED
+      // Payload stores of every worker thread (ordered before this thread by the
+      // barrier) reach L2, the coherence point the host's copy engine reads,
+      // before FINISHED is posted: a gpu-scope fence (~L2 round trip).  A
+      // sys-scope release would also wait for this thread's earlier posted
+      // host writes (WORKING) to cross PCIe (~1.5 us, tools/probe_costs.cu);
+      // LK_CF_FENCE_ALWAYS asks for it (outputs in host-mapped memory).
+      const bool sys = (a.flags & LK_CF_FENCE_ALWAYS) != 0;
+      if (!sys) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      publish(a, wid, e, o.publish, sys);
       write_timeline(a, wid, e, t_begin, t_end, c_begin, clock64(), true);
     }
   }

@@ -34,6 +34,7 @@ def breakdown(label, rounds=20000, timeline=True, **kw):
         "done_p50": float(np.percentile(done, 50)) / 1e3,
         "host_trigger": m(h[:, 1] - h[:, 0]),
         "write->seen": m(dev[:, 0] - h[:, 1]),
+        "done_p99.9": float(np.percentile(done, 99.9)) / 1e3,
         "seen->begin(cyc)": float(np.median(t[:, 6] - t[:, 5])),
         "begin->fin(cyc)": float(np.median(t[:, 7] - t[:, 6])),
         "seen->fin": m(dev[:, 3] - dev[:, 0]),
@@ -51,10 +52,8 @@ def breakdown(label, rounds=20000, timeline=True, **kw):
 if __name__ == "__main__":
     breakdown("direct K=1 (clock64 only)", timeline=False, poll_mode="direct", poll_replicas=1)
     breakdown("direct K=1", poll_mode="direct", poll_replicas=1)
-    for k in (1, 2, 4):
-        breakdown(f"gateway K={k} (clock64 only)", timeline=False, poll_mode="gateway", poll_replicas=k)
-        breakdown(f"gateway K={k}", poll_mode="gateway", poll_replicas=k)
-    breakdown("gateway K=2 d=150", poll_mode="gateway", poll_replicas=2, poll_spacing_ns=150)
-    breakdown("gateway K=2 d=600", poll_mode="gateway", poll_replicas=2, poll_spacing_ns=600)
+    breakdown("direct K=2", poll_mode="direct", poll_replicas=2)
+    breakdown("gateway K=1 (clock64 only)", timeline=False, poll_mode="gateway", poll_replicas=1)
+    breakdown("gateway K=1", poll_mode="gateway", poll_replicas=1)
     breakdown("direct K=1 16w", poll_mode="direct", poll_replicas=1, num_workers=16)
-    breakdown("gateway K=2 16w", poll_mode="gateway", poll_replicas=2, num_workers=16)
+    breakdown("direct K=1 1w", poll_mode="direct", poll_replicas=1, num_workers=1)
