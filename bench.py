@@ -43,6 +43,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 MEASURED_PEAKS = ROOT / "MEASURED_PEAKS.json"
+SM_MAX_GHZ = 1.965
 FALLBACK_HBM_GBS = 6650.0
 L2_BYTES = 126 * 1024 * 1024
 
@@ -361,6 +362,37 @@ def measure_payload(session, kind, sizes_mib, reps, rotate_bytes):
     return out
 
 
+def measure_config0(session, rounds, n=65536):
+    from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+    a = np.random.default_rng(0).integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    b = np.random.default_rng(1).integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    da, db = DeviceBuffer.from_array(a), DeviceBuffer.from_array(b)
+    outs = [DeviceBuffer(4 * n) for _ in range(4)]
+    works = [WorkDescriptor(slot=700 + i, kind="vector_add_i32", data_in_ref=(da, db), data_out_ref=outs[i])
+             for i in range(4)]
+    for i, w in enumerate(works):
+        session.register(w, 1 << i)
+    for k in range(200):
+        session.trigger(1 << (k % 4), works[k % 4])
+        session.wait(1 << (k % 4))
+    lat = []
+    t0 = time.perf_counter_ns()
+    for k in range(rounds):
+        m = 1 << (k % 4)
+        a0 = time.perf_counter_ns()
+        session.trigger(m, works[k % 4])
+        session.wait(m)
+        lat.append(time.perf_counter_ns() - a0)
+    dt = (time.perf_counter_ns() - t0) / 1e9
+    from oracle import work as W
+    ok = all(np.array_equal(o.download(np.int32, n), W.vector_add_i32(a, b)) for o in outs)
+    for buf in [da, db] + outs:
+        buf.free()
+    return {"what": "configs[0] workload on the GPU: 4 workers round robin, one int32 vector add of "
+                    "64 Ki elements per task, Python API trigger+wait", "tasks_per_s": round(rounds / dt, 1),
+            "latency": lat_summary(lat), "bit_exact_vs_oracle": bool(ok)}
+
+
 def measure_interference(session, lat_workers, rounds, stream_mib):
     """configs[3]: a latency partition (workers [0, lat_workers), closed-loop
     empty tasks round-robin, driven from C) measured solo, then while the
@@ -474,10 +506,11 @@ def run_lk_arm(args, world, rank, local):
     cyc_all = np.concatenate(cyc_all)
 
     tl = session.last_timeline().astype(np.int64)
-    extras = {"device_handling_us": {
-        "what": "globaltimer, each worker's last timed dispatch: to_gpu value seen -> FINISHED store issued",
-        "p50": round(float(np.median(tl[:, 3] - tl[:, 0])) / 1e3, 3),
-        "max": round(float((tl[:, 3] - tl[:, 0]).max()) / 1e3, 3)}}
+    dev_cyc = (tl[:, 7] - tl[:, 5]).astype(np.float64)
+    extras = {"device_handling": {
+        "what": "clock64 cycles, each worker's last timed dispatch: to_gpu value seen -> FINISHED store issued",
+        "p50_cycles": float(np.median(dev_cyc)), "max_cycles": float(dev_cyc.max()),
+        "p50_us_at_max_clock": round(float(np.median(dev_cyc)) / SM_MAX_GHZ / 1e3, 4)}}
     # full-148-worker dispatch
     full = host.full_mask(n)
     _, fdone, fcyc = session.bench_roundtrip([full], 0, args.full_rounds)
@@ -493,6 +526,11 @@ def run_lk_arm(args, world, rank, local):
         session.wait(m)
     e2e_dt = (time.perf_counter_ns() - t0) / 1e9
     e2e_value = e2e_rounds / e2e_dt
+
+    # configs[0] shape on the GPU: 4 workers round robin, int32 vector add of 64 Ki
+    # elements per task (the CPU reference's workload), trigger->done per task
+    if rank == 0 and not args.no_payload:
+        extras["config0_on_gpu"] = measure_config0(session, args.config0_rounds)
 
     payload = {}
     if not args.no_payload and rank == 0:
@@ -576,10 +614,10 @@ def run_lk_arm(args, world, rank, local):
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 1), "unit": "tasks/s",
-                "h2d_bytes_per_step": 8 * R, "d2h_bytes_per_step": 24 * R,
-                "note": "Python API session.trigger+session.wait per task (ctypes -> liblk.so); "
-                        "host<->device traffic is the mailbox words themselves (WORK+ack down, "
-                        "WORKING/FINISHED/NOP status cells up)"},
+                "h2d_bytes_per_step": 2 * 8 * cfg.poll_replicas * R, "d2h_bytes_per_step": 3 * 8 * R,
+                "note": "Python API session.trigger+session.wait per task (ctypes -> liblk.so), "
+                        f"{e2e_rounds} tasks; host<->device traffic per task is the mailbox cells "
+                        "themselves: WORK + ack down (8 B x replicas each), WORKING/FINISHED/NOP up (8 B each)"},
         "gpu_launches": 1,
         "gpu_launch_note": "one persistent kernel resident across the timed region; tasks are "
                            "dispatched by mailbox words, not launches",
@@ -612,6 +650,7 @@ def main():
     ap.add_argument("--no-payload", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-interference", action="store_true")
+    ap.add_argument("--config0-rounds", type=int, default=20_000)
     ap.add_argument("--lat-workers", type=int, default=16, help="latency partition size (configs[3])")
     ap.add_argument("--interf-rounds", type=int, default=100_000)
     ap.add_argument("--stream-mib", type=int, default=512, help="hbm_stream src (= dst) MiB")
