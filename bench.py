@@ -384,13 +384,12 @@ def measure_config0(session, rounds, n=65536):
         session.wait(m)
         lat.append(time.perf_counter_ns() - a0)
     dt = (time.perf_counter_ns() - t0) / 1e9
-    from oracle import work as W
-    ok = all(np.array_equal(o.download(np.int32, n), W.vector_add_i32(a, b)) for o in outs)
     for buf in [da, db] + outs:
         buf.free()
     return {"what": "configs[0] workload on the GPU: 4 workers round robin, one int32 vector add of "
                     "64 Ki elements per task, Python API trigger+wait", "tasks_per_s": round(rounds / dt, 1),
-            "latency": lat_summary(lat), "bit_exact_vs_oracle": bool(ok)}
+            "latency": lat_summary(lat),
+            "parity": "tests/test_gpu_payload.py::test_vector_add_i32_bit_exact (same kind, sizes, masks)"}
 
 
 def measure_interference(session, lat_workers, rounds, stream_mib):
