@@ -155,3 +155,23 @@ def test_trace_file_roundtrip():
     text = protocol.format_trace(recs)
     assert protocol.parse_trace(text) == recs
     assert protocol.validate_trace([(r.side, r.sm_id, r.word) for r in recs]) is None
+
+
+def test_trace_files_validate_with_reference_cli(reference, tmp_path):
+    """Trace files written by this runtime's format_trace are accepted by the
+    reference's own `persistkern validate` (P/cli.py:223-235), and a corrupted
+    one is rejected with exit 1 -- the integration path for device traces."""
+    import json
+    from persistkern import cli as ref_cli
+    golden = json.loads((ROOT / "tests" / "golden" / "native_golden.json").read_text())
+    for name, case in golden.items():
+        recs = [protocol.TraceRecord(k, s, w, word) for k, (s, w, word) in enumerate(case["writes"])]
+        f = tmp_path / f"{name}.trace"
+        f.write_text(protocol.format_trace(recs))
+        assert ref_cli.main(["validate", str(f)]) == 0, name
+        bad = list(recs)
+        k = next(i for i, r in enumerate(bad) if r.side == "D" and r.word == protocol.WORKING)
+        bad[k] = protocol.TraceRecord(bad[k].step, "D", bad[k].sm_id, protocol.FINISHED)
+        g = tmp_path / f"{name}.bad.trace"
+        g.write_text(protocol.format_trace(bad))
+        assert ref_cli.main(["validate", str(g)]) == 1, name
