@@ -469,8 +469,14 @@ def run_lk_arm(args, world, rank, local):
 
     device = local
     pinned = 0
+    pinned_core = None
     try:
         pinned = native.pin_host_thread(device)
+        # one core of the GPU-local set, the highest-numbered one (core 0 takes
+        # most housekeeping interrupts): no migrations under the spin loop
+        local_cores = sorted(os.sched_getaffinity(0))
+        pinned_core = local_cores[-1 - (local % max(1, len(local_cores)))]
+        os.sched_setaffinity(0, {pinned_core})
     except Exception:
         pinned = 0
     cfg = native.NativeConfig(num_workers=args.workers, device=device, spin_strategy=native.PURE_SPIN,
@@ -600,7 +606,7 @@ def run_lk_arm(args, world, rank, local):
                    "cell_stride": cfg.cell_stride, "poll_backoff_ns": cfg.poll_backoff_ns,
                    "poll_mode": cfg.poll_mode, "poll_replicas": cfg.poll_replicas,
                    "poll_spacing_ns": cfg.poll_spacing_ns, "payload_path": "tma" if cfg.tma_payload else "lsu",
-                   "host_cores_pinned": pinned, "l2": "n/a for the empty task (no payload); payload "
+                   "host_cores_local": pinned, "host_core": pinned_core, "l2": "n/a for the empty task (no payload); payload "
                    "GB/s rotate buffers over >= 4x L2",
                    "timing": "host CLOCK_MONOTONIC per round; max over ranks"},
         "latency_us": {"trigger_to_done": lk, "round_trip_with_ack": lat_summary(cyc_all),

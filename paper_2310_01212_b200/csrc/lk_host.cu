@@ -283,26 +283,43 @@ static int kernel_status(lk_session* s) {
   return 1;
 }
 
+// Host spin with the reference's timeout contract (native.py:233-248).  The
+// clock is read every 256 spins and started lazily, and the slow checks
+// (worker error words, cudaStreamQuery on the kernel -- a driver call of
+// several microseconds) run only once a wait has lasted 200 us, so a normal
+// microsecond-scale round trip never pays for them.
 struct Spinner {
+  static constexpr uint64_t kSlowEveryNs = 200000;
   const lk_session* s;
-  uint64_t deadline;
-  uint32_t spins = 0;
-  uint32_t checks = 0;
-  explicit Spinner(const lk_session* ss) : s(ss) { deadline = now_ns() + ss->cfg.wait_timeout_ns; }
-  // returns false on timeout
-  inline bool step() {
+  uint64_t t0 = 0, next_slow = 0;
+  uint32_t spins = 0, checks = 0;
+  explicit Spinner(const lk_session* ss) : s(ss) {}
+  enum { kGo = 0, kTimeout = 1, kSlowCheck = 2 };
+  inline int step() {
     LK_PAUSE();
     if (s->cfg.spin_strategy == 1 && ++spins >= s->cfg.spin_yield_threshold) {
       spins = 0;
       sched_yield();
     }
-    if ((++checks & 1023u) == 0) return now_ns() <= deadline;
-    return true;
+    if ((++checks & 255u) == 0) {
+      const uint64_t t = now_ns();
+      if (!t0) {
+        t0 = t;
+        next_slow = t + kSlowEveryNs;
+        return kGo;
+      }
+      if (t - t0 > s->cfg.wait_timeout_ns) return kTimeout;
+      if (t >= next_slow) {
+        next_slow = t + kSlowEveryNs;
+        return kSlowCheck;
+      }
+    }
+    return kGo;
   }
 };
 
-// Spin until word(i) == want for every id; checks worker errors and the
-// kernel on the slow path.  Returns LK_OK, LK_E_HANG or LK_E_WORKER_DIED.
+// Spin until word(i) == want for every id.  Returns LK_OK, LK_E_HANG or
+// LK_E_WORKER_DIED.
 static int spin_words(lk_session* s, const std::vector<uint32_t>& ids, uint32_t want, const char* what) {
   Spinner sp(s);
   size_t j = 0;
@@ -311,13 +328,14 @@ static int spin_words(lk_session* s, const std::vector<uint32_t>& ids, uint32_t 
       ++j;
       continue;
     }
-    if (!sp.step()) {
+    const int st = sp.step();
+    if (st == Spinner::kTimeout) {
       int rc = check_workers(s);
       if (rc) return rc;
       return fail(LK_E_HANG, "%s made no progress within %.3fs (workers %s)", what,
                   double(s->cfg.wait_timeout_ns) / 1e9, ids_str(ids).c_str());
     }
-    if ((sp.checks & 0xFFFFu) == 0) {
+    if (st == Spinner::kSlowCheck) {
       int rc = check_workers(s);
       if (rc) return rc;
       if (kernel_status(s) != 0) return fail(LK_E_WORKER_DIED, "persistent kernel is no longer running");
