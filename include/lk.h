@@ -104,13 +104,15 @@ typedef struct lk_config {
   uint32_t record_trace;         /* native.py:51 */
   uint32_t trace_capacity;       /* device records per worker; 0 = 65536 */
   uint32_t poll_backoff_ns;      /* device __nanosleep between idle polls (0 = none) */
-  uint32_t cell_stride;          /* bytes between mailbox cells: 8..128 (power of 2); 0 = 128 */
+  uint32_t cell_stride;          /* bytes between to_gpu cells / replicas: 8..128 (power of 2); 0 = 128 */
   uint32_t num_slots;            /* descriptor table entries; 0 = 1024 */
   uint64_t wait_timeout_ns;      /* wait_timeout_s (native.py:52) */
   uint32_t flags;                /* LK_CF_* */
   uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 1 */
   uint32_t poll_spacing_ns;      /* stagger between replica loads / sweeps; 0 = 300 */
   uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default) or LK_POLL_GATEWAY */
+  uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 128 */
+  uint32_t reserved;
 } lk_config;
 
 /* How to_gpu words reach the workers.  DIRECT: every worker polls its own

@@ -126,11 +126,11 @@ struct lk_session {
   std::mutex post_mu;
   std::vector<uint32_t> all_ids;
   bool gateway = false;
-  volatile unsigned long long* status = nullptr;  // stride cell_u64
+  volatile unsigned long long* status = nullptr;  // stride status_u64
   volatile unsigned long long* err = nullptr;
   volatile uint32_t* err_any = nullptr;
   volatile uint32_t* smid = nullptr;
-  uint32_t cell_u64 = 16, replicas = 4;
+  uint32_t cell_u64 = 16, status_u64 = 16, replicas = 4;
 
   // device block
   uint8_t* dev_block = nullptr;
@@ -169,8 +169,8 @@ struct lk_session {
   // scratch
   std::vector<uint32_t> ids;
 
-  inline uint32_t word(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64]); }
-  inline uint32_t phase(uint32_t i) const { return uint32_t(status[uint64_t(i) * cell_u64] >> 32); }
+  inline uint32_t word(uint32_t i) const { return uint32_t(status[uint64_t(i) * status_u64]); }
+  inline uint32_t phase(uint32_t i) const { return uint32_t(status[uint64_t(i) * status_u64] >> 32); }
   // One logical to_gpu write: {word, seq} into every replica (seq = this
   // worker's host write index; the device acts only on newer seqs, so the
   // replicas, written one after another, can never step it backwards).
@@ -357,6 +357,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.cell_stride != 8 && cfg.cell_stride != 16 && cfg.cell_stride != 32 && cfg.cell_stride != 64 &&
       cfg.cell_stride != 128)
     return fail(LK_E_CONFIG, "cell_stride must be 8, 16, 32, 64 or 128");
+  if (cfg.status_stride == 0) cfg.status_stride = 128;
+  if (cfg.status_stride != 16 && cfg.status_stride != 32 && cfg.status_stride != 64 && cfg.status_stride != 128)
+    return fail(LK_E_CONFIG, "status_stride must be 16, 32, 64 or 128");
   if (cfg.poll_mode > LK_POLL_GATEWAY) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
   if (cfg.poll_replicas == 0) cfg.poll_replicas = 1;
   if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)
@@ -391,6 +394,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->threads = cfg.threads_per_worker;
   s->device = cfg.device;
   s->cell_u64 = cfg.cell_stride / 8;
+  s->status_u64 = cfg.status_stride / 8;
   s->replicas = cfg.poll_replicas;
   s->gateway = cfg.poll_mode == LK_POLL_GATEWAY;
   s->last_word.assign(s->nw, LK_NOP);
@@ -426,7 +430,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   auto al = [](size_t x) { return (x + 4095) & ~size_t(4095); };
   const size_t tob = s->gateway ? al(size_t(s->replicas) * s->ring_entries * 64 + 128)
                                 : al(size_t(s->nw) * s->replicas * cfg.cell_stride);
-  const size_t cells = al(size_t(s->nw) * cfg.cell_stride);
+  const size_t cells = al(size_t(s->nw) * cfg.status_stride);
   const size_t err_words = (size_t(s->nw) + 15) / 16 * 16;   // err[] then err_any on its own line
   const size_t errb = al(err_words * 8 + 128), smidb = al(size_t(s->nw) * 4);
   const size_t host_bytes = tob + cells + errb + smidb;
@@ -445,7 +449,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     for (uint32_t k = 0; k < s->replicas; ++k) {
       if (!s->gateway) s->to_gpu[(uint64_t(i) * s->replicas + k) * s->cell_u64] = LK_NOP;   // {NOP, seq 0}
     }
-    s->status[uint64_t(i) * s->cell_u64] = uint64_t(LK_NOP) | (uint64_t(LK_PHASE_BOOTING) << 32);
+    s->status[uint64_t(i) * s->status_u64] = uint64_t(LK_NOP) | (uint64_t(LK_PHASE_BOOTING) << 32);
     s->smid[i] = 0xFFFFFFFFu;
   }
 
@@ -509,6 +513,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.trace = s->d_trace;
   a.trace_cnt = s->d_tcnt;
   a.cell_u64 = s->cell_u64;
+  a.status_u64 = s->status_u64;
   a.replicas = s->replicas;
   a.spacing_ns = cfg.poll_spacing_ns;
   a.num_slots = cfg.num_slots;
@@ -793,7 +798,7 @@ extern "C" int lk_read_cells(lk_session* s, uint32_t* to_gpu, uint32_t* from_gpu
   if (!s) return fail(LK_E_USAGE, "null session");
   const uint32_t m = std::min(n, s->nw);
   for (uint32_t i = 0; i < m; ++i) {
-    const unsigned long long st = s->status[uint64_t(i) * s->cell_u64];
+    const unsigned long long st = s->status[uint64_t(i) * s->status_u64];
     if (to_gpu) to_gpu[i] = s->to_gpu_word(i);
     if (from_gpu) from_gpu[i] = uint32_t(st);
     if (phase) phase[i] = uint32_t(st >> 32);

@@ -18,7 +18,7 @@ struct lk_dev_trace {
 struct lk_dev_args {
   const unsigned long long* to_gpu;  // host-mapped; worker i replica k at to_gpu[(i*replicas + k)*cell_u64]:
                                      // word | seq<<32 (seq = host write index, monotone per worker)
-  unsigned long long* status;      // host-mapped, cell i at status[i*cell_u64]: word | phase<<32
+  unsigned long long* status;      // host-mapped, cell i at status[i*status_u64]: word | phase<<32
   unsigned long long* err;         // host-mapped, err[i] = code | word<<32
   uint32_t* err_any;               // host-mapped, set to 1 after any err[i] is written
   uint32_t* smid;                  // host-mapped, smid[i]
@@ -40,7 +40,8 @@ struct lk_dev_args {
   uint32_t use_tma;                // payload tiles through the TMA bulk ring in dynamic smem
   lk_dev_trace* trace;             // device, num_workers * trace_cap
   uint32_t* trace_cnt;             // device, num_workers
-  uint32_t cell_u64;               // cell stride in u64 (to_gpu replicas and status)
+  uint32_t cell_u64;               // to_gpu cell stride in u64 (DIRECT cells and replicas)
+  uint32_t status_u64;             // from_gpu status cell stride in u64
   uint32_t replicas;               // to_gpu replicas per worker: 1, 2, 4 or 8
   uint32_t spacing_ns;             // stagger between replica loads
   uint32_t num_slots;

@@ -469,7 +469,7 @@ __device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elec
     __threadfence();
   }
   const unsigned long long v = uint64_t(word) | (uint64_t(e.st.phase) << 32);
-  unsigned long long* cell = a.status + uint64_t(wid) * a.cell_u64;
+  unsigned long long* cell = a.status + uint64_t(wid) * a.status_u64;
   if (release) st_release_sys(cell, v); else st_relaxed_sys(cell, v);
   e.pub = word;
 }
@@ -508,7 +508,7 @@ __device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool ti
 
 __device__ __forceinline__ void publish_fast(const lk_dev_args& a, uint32_t wid, uint32_t word,
                                              uint32_t phase) {
-  st_relaxed_sys(a.status + uint64_t(wid) * a.cell_u64, uint64_t(word) | (uint64_t(phase) << 32));
+  st_relaxed_sys(a.status + uint64_t(wid) * a.status_u64, uint64_t(word) | (uint64_t(phase) << 32));
 }
 
 // The two transitions every empty-task round trip makes, settled in place

@@ -57,7 +57,8 @@ class NativeConfig:
     device: int = 0
     threads_per_worker: int = 512
     poll_backoff_ns: int = 0
-    cell_stride: int = 128
+    cell_stride: int = 128          # bytes between to_gpu cells
+    status_stride: int = 128        # bytes between from_gpu status cells
     poll_mode: str = "direct"       # "direct": each worker polls its host cell; "gateway": one warp
                                     # polls all host cells and forwards through device memory
     poll_replicas: int = 1          # to_gpu replicas polled per worker (gateway: doorbell sweeps)
@@ -92,6 +93,7 @@ class NativeConfig:
         c.trace_capacity = self.trace_capacity
         c.poll_backoff_ns = self.poll_backoff_ns
         c.cell_stride = self.cell_stride
+        c.status_stride = self.status_stride
         c.num_slots = self.num_slots
         c.poll_replicas = self.poll_replicas
         c.poll_spacing_ns = self.poll_spacing_ns

@@ -28,21 +28,14 @@ def run(label, rounds=20000, mode="rr", **kw):
     t = s.last_timeline().astype(np.int64)
     s.dispose()
     s.close()
-    dev = np.median(t[:, 3] - t[:, 0]) / 1e3
+    dev = np.median(t[:, 7] - t[:, 5])
     print(f"{label:40s} done p50 {pct(done,50):6.2f} p99 {pct(done,99):6.2f} p99.9 {pct(done,99.9):6.2f} "
-          f"| cycle p50 {pct(cyc,50):6.2f} p99.9 {pct(cyc,99.9):6.2f} | dev {dev:5.2f}", flush=True)
+          f"| cycle p50 {pct(cyc,50):6.2f} p99.9 {pct(cyc,99.9):6.2f} | dev {dev:5.0f} cyc", flush=True)
 
 
 native.pin_host_thread(0)
 pp = native.pingpong(0, 20000)
 print("pingpong p50 %.2f p99.9 %.2f" % (pct(pp[100:], 50), pct(pp[100:], 99.9)))
-for k, d in ((1, 300), (2, 150), (2, 300), (2, 500), (4, 150), (4, 300)):
-    run(f"gateway K={k} d={d}", poll_mode="gateway", poll_replicas=k, poll_spacing_ns=d)
-run("gateway K=2 d=300 backoff=100", poll_mode="gateway", poll_replicas=2, poll_spacing_ns=300,
-    poll_backoff_ns=100)
-run("direct K=1", poll_mode="direct", poll_replicas=1)
-run("direct K=2 d=300", poll_mode="direct", poll_replicas=2, poll_spacing_ns=300)
-for mode in ("gateway", "direct"):
-    run(f"1 worker {mode}", num_workers=1, poll_mode=mode)
-    run(f"16 workers {mode}", num_workers=16, poll_mode=mode)
-    run(f"148 full-mask {mode}", mode="full", rounds=5000, poll_mode=mode)
+for cs, ss in ((128, 128), (32, 128), (128, 32), (32, 32), (64, 64), (32, 64), (128, 64), (128, 16)):
+    run(f"148 rr direct cell={cs} status={ss}", cell_stride=cs, status_stride=ss)
+    run(f"148 full-mask direct cell={cs} status={ss}", mode="full", rounds=5000, cell_stride=cs, status_stride=ss)
