@@ -27,7 +27,7 @@ from . import _lib, protocol
 from .device import WorkDescriptor, as_work
 from .errors import HangDetected, UsageError
 from .host import (PHASE_COPYIN, PHASE_COPYOUT, PHASE_DISPOSE, PHASE_INIT, PHASE_LAUNCH,
-                   PHASE_TRIGGER, PHASE_WAIT, PhaseTiming, _check_mask, full_mask)
+                   PHASE_TRIGGER, PHASE_WAIT, PhaseTiming, _check_mask, full_mask, sms_in_mask)
 
 log = logging.getLogger(__name__)
 
@@ -241,6 +241,12 @@ class NativeSession:
         if self.disposed:
             raise UsageError("session already disposed")
 
+    def _check(self, mask: int) -> None:
+        # host._check_mask's rules (host.py:76-81) without building the id list:
+        # a 148-bit mask would otherwise cost ~30 us of Python per call
+        if mask <= 0 or mask >> self.num_workers:
+            _check_mask(mask, self.num_workers)   # raises with the reference's message
+
     def _mask(self, mask: int) -> bytes:
         return mask.to_bytes(8 * self.nwords, "little")
 
@@ -265,7 +271,7 @@ class NativeSession:
     def trigger(self, mask: int, work: WorkDescriptor) -> PhaseTiming:
         """Dispatch: one word write per masked worker, no kernel launch."""
         self._require_live()
-        _check_mask(mask, self.num_workers)
+        self._check(mask)
         work = as_work(work)
         key = mask if work.multi_worker else 0
         if self._staged.get(work.slot) == (work, key) and self.descriptors.get(work.slot) is work:
@@ -284,9 +290,10 @@ class NativeSession:
     def wait(self, mask: int) -> PhaseTiming:
         """Spin (in C) until every masked worker published FINISHED, then ack."""
         self._require_live()
-        sm_ids = _check_mask(mask, self.num_workers)
+        self._check(mask)
         rc = self._lib.lk_wait(self._h, self._mask(mask), self.nwords, C.byref(self._u64))
-        _lib.check(rc, sm_ids=sm_ids)
+        if rc:
+            _lib.raise_for(rc, sm_ids=tuple(sms_in_mask(mask)))
         timing = PhaseTiming(PHASE_WAIT, self._u64.value, mask)
         self.timings.append(timing)
         return timing
