@@ -386,6 +386,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.num_workers == 0) cfg.num_workers = nsm;
   if (cfg.num_workers > nsm)
     return fail(LK_E_CONFIG, "num_workers %u exceeds the %u SMs (one worker per SM)", cfg.num_workers, nsm);
+  if (cfg.num_workers > 256) return fail(LK_E_CONFIG, "at most 256 workers (4 mask words)");
 
   auto* s = new lk_session();
   s->cfg = cfg;

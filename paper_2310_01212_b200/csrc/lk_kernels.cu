@@ -519,9 +519,21 @@ __device__ __forceinline__ void publish_fast(const lk_dev_args& a, uint32_t wid,
 //   FINISHED x NOP -> publish NOP, IDLE; re-stepping NOP in IDLE is a no-op.
 // Exactly lk_worker_step + lk_complete_work for these cases (protocol.py:151-206);
 // anything else -- and every case while a trace is recorded -- takes settle().
-__device__ __forceinline__ bool fast_step(const lk_dev_args& a, uint32_t wid, Elected& e) {
-  if (a.record_trace | (a.flags & LK_CF_FENCE_ALWAYS)) return false;
+enum FastResult : uint32_t { kFastNone = 0, kFastSettled = 1, kFastBegin = 2 };
+
+__device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  if (a.record_trace | (a.flags & LK_CF_FENCE_ALWAYS)) return kFastNone;
   const uint32_t w = e.cur;
+  if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && !(e.hint & LK_HINT_EMPTY) &&
+      w - LK_WORK_BASE < a.num_slots) {
+    // IDLE x WORK(s) of any other kind: publish WORKING and begin at once; the
+    // word stays dirty so it is re-stepped after completion, as in settle().
+    publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
+    e.st = lk_wstate{LK_PHASE_WORKING, w - LK_WORK_BASE};
+    e.pub = LK_WORKING;
+    e.dirty = true;
+    return kFastBegin;
+  }
   if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && (e.hint & LK_HINT_EMPTY) &&
       w - LK_WORK_BASE < a.num_slots) {
     const uint64_t c_begin = clock64();
@@ -534,16 +546,16 @@ __device__ __forceinline__ bool fast_step(const lk_dev_args& a, uint32_t wid, El
     unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
     tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
     if (a.flags & LK_CF_TIMELINE) { tl[0] = e.t_seen; tl[4] = e.t_fwd; }
-    return true;
+    return kFastSettled;
   }
   if (e.st.phase == LK_PHASE_FINISHED && w == LK_NOP) {
     publish_fast(a, wid, LK_NOP, LK_PHASE_IDLE);
     e.st.phase = LK_PHASE_IDLE;
     e.pub = LK_NOP;
     e.dirty = false;
-    return true;
+    return kFastSettled;
   }
-  return false;
+  return kFastNone;
 }
 
 // Step the current word to a fixed point, exactly as the reference worker
@@ -595,7 +607,9 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (accept(e, v[k], timeline)) {
-          fresh = !fast_step(a, wid, e);   // fast path settled it: keep polling
+          const uint32_t f = fast_step(a, wid, e);
+          if (f == kFastBegin) return LK_ACT_BEGIN;
+          fresh = f == kFastNone;          // settled in place: keep polling
           if (fresh) break;
           v[k] = ld_cell(base + k * step, acquire);
           continue;
@@ -620,7 +634,9 @@ __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t 
     for (;;) {
       if (accept(e, ld_relaxed_gpu64(mb), timeline)) {
         if (timeline) e.t_fwd = ld_relaxed_gpu64(mb + 1);
-        if (!fast_step(a, wid, e)) break;
+        const uint32_t f = fast_step(a, wid, e);
+        if (f == kFastBegin) return LK_ACT_BEGIN;
+        if (f == kFastNone) break;
         continue;
       }
       if (a.backoff_ns) __nanosleep(a.backoff_ns);
@@ -788,12 +804,18 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
           write_timeline(a, wid, e, t_b, t_b, c_begin_e, clock64(), tl);
           continue;
         }
+        // descriptor and the slot's trigger mask in one L2 round trip
         lk_desc d;
+        unsigned long long mk[4] = {0ull, 0ull, 0ull, 0ull};
         {
           const uint4* src = reinterpret_cast<const uint4*>(a.desc + slot);
           uint4* dst = reinterpret_cast<uint4*>(&d);
+          const unsigned long long* m = a.slot_mask + uint64_t(slot) * a.nwords;
 #pragma unroll
           for (int k = 0; k < 4; ++k) dst[k] = ld_cg4(src + k);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (uint32_t(k) < a.nwords) mk[k] = ld_cg64(m + k);
         }
         if (d.kind >= LK_KIND_COUNT) { report_error(a, wid, e, LK_WERR_BAD_KIND, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
         if (single_thread_kind(d.kind)) {
@@ -808,11 +830,11 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
           continue;
         }
         // payload item: rank/count from the slot's trigger mask
-        const unsigned long long* m = a.slot_mask + uint64_t(slot) * a.nwords;
         uint32_t count = 0, rank = 0;
         const uint32_t mw = wid >> 6;
-        for (uint32_t k = 0; k < a.nwords; ++k) {
-          const unsigned long long bits = ld_cg64(m + k);
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+          const unsigned long long bits = mk[k];
           count += __popcll(bits);
           if (k < mw) rank += __popcll(bits);
           else if (k == mw) rank += __popcll(bits & ((1ull << (wid & 63)) - 1ull));
