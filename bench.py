@@ -28,6 +28,7 @@ to the GPU's NUMA-local cores; "replicas only", no collective on the path.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -537,18 +538,28 @@ def run_lk_arm(args, world, rank, local):
     if rank == 0 and not args.no_payload:
         extras["config0_on_gpu"] = measure_config0(session, args.config0_rounds)
 
-    payload = {}
-    if not args.no_payload and rank == 0:
-        payload["saxpy_f32"] = measure_payload(session, "saxpy_f32", args.payload_mib, args.payload_reps,
-                                               4 * L2_BYTES)
-        payload["block_reduce_f32"] = measure_payload(session, "block_reduce_f32", args.payload_mib,
-                                                      args.payload_reps, 4 * L2_BYTES)
     if not args.no_interference and rank == 0 and n >= args.lat_workers + 8:
         extras["interference"] = measure_interference(session, args.lat_workers, args.interf_rounds,
                                                       args.stream_mib)
     smids = session.smid_map
     session.dispose()
     session.close()
+
+    # configs[2]: payload items dispatched to every worker.  Multi-worker
+    # dispatch runs on a GATEWAY-mode session (one ring event reaches all 148
+    # workers within ~0.5 us; direct polling spreads their start over ~2 us,
+    # which the span -- and so the GB/s -- would include at small sizes).
+    payload = {}
+    if not args.no_payload and rank == 0:
+        pcfg = dataclasses.replace(cfg, poll_mode=args.payload_poll_mode)
+        psession, _ = native.NativeSession.start(pcfg)
+        payload["poll_mode"] = args.payload_poll_mode
+        payload["saxpy_f32"] = measure_payload(psession, "saxpy_f32", args.payload_mib, args.payload_reps,
+                                               4 * L2_BYTES)
+        payload["block_reduce_f32"] = measure_payload(psession, "block_reduce_f32", args.payload_mib,
+                                                      args.payload_reps, 4 * L2_BYTES)
+        psession.dispose()
+        psession.close()
 
     # conventional launch+sync baseline, same host thread
     base = {}
@@ -646,6 +657,7 @@ def main():
     ap.add_argument("--replicas", type=int, default=1)
     ap.add_argument("--spacing-ns", type=int, default=300)
     ap.add_argument("--lsu-payload", action="store_true", help="payload via 128-bit LSU loads, not the TMA ring")
+    ap.add_argument("--payload-poll-mode", choices=["gateway", "direct"], default="gateway")
     ap.add_argument("--full-rounds", type=int, default=100_000)
     ap.add_argument("--e2e-rounds", type=int, default=100_000)
     ap.add_argument("--base-rounds", type=int, default=100_000)

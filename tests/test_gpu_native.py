@@ -427,3 +427,30 @@ def test_baseline_launch_wait_contract():
 def test_pingpong_floor_runs():
     rt = native.pingpong(0, 200)
     assert (rt > 0).all()
+
+
+def test_scenario_backend_rows():
+    """backend.run_b200 on a Scenario-shaped object (P/bench.py:51-116): the
+    rows _run_native_lk/_run_native_baseline produce, plus the baseline's
+    Dispose row the reference's native runner omits."""
+    from paper_2310_01212_b200 import backend
+
+    class Scn:
+        reps = 20
+        def cluster_count(self):
+            return 4
+        def mask(self):
+            return 0b1111
+        def work(self):
+            return WorkDescriptor(slot=0, iterations=64)
+        def models(self):
+            return [host.MODEL_LK, host.MODEL_BASELINE]
+
+    rows = backend.run_b200(Scn())
+    got = {(r.model, r.phase): r for r in rows}
+    for key in [("LK", "Init"), ("LK", "Trigger"), ("LK", "Wait"), ("LK", "Dispose"),
+                ("BASE", "Alloc"), ("BASE", "Launch"), ("BASE", "Wait"), ("BASE", "Dispose")]:
+        assert key in got, key
+    assert got[("LK", "Trigger")].samples == 20 and got[("BASE", "Launch")].samples == 20
+    assert all(r.best <= r.avg <= r.worst for r in rows)
+    assert "b200" in backend.rows_csv(rows)

@@ -10,7 +10,9 @@ from paper_2310_01212_b200 import host, native  # noqa: E402
 from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
 
 native.pin_host_thread(0)
-s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN))
+mode = sys.argv[1] if len(sys.argv) > 1 else "direct"
+s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, poll_mode=mode))
+print("poll mode", mode)
 n = s.num_workers
 full = host.full_mask(n)
 s.register(WorkDescriptor(slot=0, kind="empty"))
