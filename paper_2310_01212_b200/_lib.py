@@ -89,7 +89,7 @@ class lk_config(C.Structure):
         ("poll_spacing_ns", C.c_uint32),
         ("poll_mode", C.c_uint32),
         ("status_stride", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("ring_stages", C.c_uint32),
     ]
 
 

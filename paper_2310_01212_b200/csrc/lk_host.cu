@@ -362,6 +362,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     return fail(LK_E_CONFIG, "status_stride must be 16, 32, 64 or 128");
   if (cfg.poll_mode > LK_POLL_GATEWAY) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
   if (cfg.poll_replicas == 0) cfg.poll_replicas = 1;
+  if (cfg.ring_stages == 0) cfg.ring_stages = 12;
+  if (cfg.ring_stages < 2 || cfg.ring_stages > lk_ring_max_stages())
+    return fail(LK_E_CONFIG, "ring_stages must be 2..%u", lk_ring_max_stages());
   if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)
     return fail(LK_E_CONFIG, "poll_replicas must be 1, 2, 4 or 8");
   if (cfg.poll_mode == LK_POLL_GATEWAY && cfg.poll_replicas == 8)
@@ -485,11 +488,11 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "stream: %s", cudaGetErrorString(ce)));
 
   // --- one CTA per SM: dynamic smem above half the SM's capacity
-  s->smem = size_t(prop.sharedMemPerMultiprocessor) / 2 + 8192;
-  if (s->smem > size_t(prop.sharedMemPerBlockOptin) - 1024) s->smem = size_t(prop.sharedMemPerBlockOptin) - 1024;
   const bool use_tma = !(cfg.flags & LK_CF_LSU_PAYLOAD);
-  if (use_tma && s->smem < lk_ring_bytes())
-    return cleanup(fail(LK_E_INIT, "payload ring needs %zu B of shared memory, have %zu", lk_ring_bytes(), s->smem));
+  s->smem = std::max(size_t(prop.sharedMemPerMultiprocessor) / 2 + 8192, use_tma ? lk_ring_bytes(cfg.ring_stages) : 0);
+  if (s->smem > size_t(prop.sharedMemPerBlockOptin) - 1024)
+    return cleanup(fail(LK_E_INIT, "payload ring needs %zu B of shared memory, the device offers %zu",
+                        s->smem, size_t(prop.sharedMemPerBlockOptin) - 1024));
   ce = lk_preload_kernels();
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "kernel load: %s", cudaGetErrorString(ce)));
   ce = lk_persistent_configure(s->smem);
@@ -533,6 +536,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.wthreads = s->threads;
   a.poll_mode = cfg.poll_mode;
   a.use_tma = use_tma ? 1 : 0;
+  a.ring_stages = cfg.ring_stages;
   ce = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(ce)));
 

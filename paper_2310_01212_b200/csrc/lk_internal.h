@@ -38,6 +38,7 @@ struct lk_dev_args {
   uint32_t wthreads;               // worker threads per CTA (the gateway warp comes after)
   uint32_t poll_mode;              // LK_POLL_*
   uint32_t use_tma;                // payload tiles through the TMA bulk ring in dynamic smem
+  uint32_t ring_stages;            // TMA ring depth (16-KiB stages)
   lk_dev_trace* trace;             // device, num_workers * trace_cap
   uint32_t* trace_cnt;             // device, num_workers
   uint32_t cell_u64;               // to_gpu cell stride in u64 (DIRECT cells and replicas)
@@ -63,6 +64,7 @@ cudaError_t lk_launch_clocksync(const uint32_t* flag, unsigned long long* echo, 
 cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_per_sm);
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads,
                            uint32_t* reduce_ctr, cudaStream_t st, int use_tma);
-size_t lk_ring_bytes();
+size_t lk_ring_bytes(uint32_t stages);
+uint32_t lk_ring_max_stages();
 cudaError_t lk_launch_pingpong(volatile uint32_t* flag, volatile uint32_t* echo,
                                uint64_t rounds, cudaStream_t st);

@@ -113,21 +113,23 @@ __device__ __forceinline__ void st4(uint4* p, uint4 v) {
 // ---------------------------------------------------------------- TMA bulk ring
 // Payload tiles stream HBM -> shared memory with cp.async.bulk (the TMA
 // engine's 1-D bulk copy: no tensor map, no register staging), completion
-// counted on an mbarrier by transaction bytes.  kStages tiles of kStageBytes
-// are in flight per SM (96 KiB: ~14 MiB across 148 SMs, far above the
-// ~4.5 MiB Little's law asks for at ~6.5 TB/s x ~700 ns), issued by one
-// elected thread while every worker thread consumes.  The ring persists
-// across dispatches: `g` counts tiles consumed since the barriers were
-// initialised (identical in every thread), so stage = g % kStages and the
-// mbarrier phase parity = (g / kStages) & 1.
+// counted on an mbarrier by transaction bytes.  Up to `stages` tiles of
+// kStageBytes are in flight per SM (12 x 16 KiB = 192 KiB by default: at
+// ~44 GB/s per SM and a loaded HBM latency of 1.5-2 us Little's law asks for
+// ~66-88 KiB per SM, and the producer refills a stage only after every warp
+// released it), issued by one elected thread while every worker thread
+// consumes.  The ring persists across dispatches: `g` counts tiles consumed
+// since the barriers were initialised (identical in every thread), so
+// stage = g % stages and the mbarrier phase parity = (g / stages) & 1.
 constexpr uint32_t kStageBytes = 16384;
-constexpr uint32_t kStages = 6;
-constexpr uint32_t kRingBytes = kStageBytes * kStages;
+constexpr uint32_t kMaxStages = 12;
+constexpr uint32_t kDefaultStages = 12;
 
 struct Ring {
-  uint8_t* buf;       // kStages x kStageBytes, 128-B aligned, dynamic shared memory
-  uint64_t* full;     // kStages mbarriers: 1 arrival (expect_tx) + tx bytes
-  uint64_t* empty;    // kStages mbarriers: T arrivals (every consumer)
+  uint8_t* buf;       // stages x kStageBytes, 128-B aligned, dynamic shared memory
+  uint64_t* full;     // stages mbarriers: 1 arrival (expect_tx) + tx bytes
+  uint64_t* empty;    // stages mbarriers: one arrival per consumer warp
+  uint32_t stages;    // <= kMaxStages
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -169,7 +171,7 @@ __device__ __forceinline__ uint4 lds4(const uint8_t* p) {
 // Called by every worker thread once, before the first dispatch.
 __device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
   if (threadIdx.x == 0) {
-    for (uint32_t k = 0; k < kStages; ++k) {
+    for (uint32_t k = 0; k < r.stages; ++k) {
       mbar_init(r.full + k, 1);
       mbar_init(r.empty + k, T / 32);   // one arrival per consumer warp
     }
@@ -185,18 +187,18 @@ __device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
 template <class Load, class Use>
 __device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntiles, const Load& load,
                                             const Use& use) {
-  const uint32_t c0 = g;
+  const uint32_t c0 = g, S = r.stages;
   auto fill = [&](uint32_t i) {
-    const uint32_t f = c0 + i, st = f % kStages;
-    mbar_wait(r.empty + st, ((f / kStages) & 1u) ^ 1u);   // previous use of this stage released
+    const uint32_t f = c0 + i, st = f % S;
+    mbar_wait(r.empty + st, ((f / S) & 1u) ^ 1u);   // previous use of this stage released
     load(i, r.buf + st * kStageBytes, r.full + st);
   };
   if (threadIdx.x == 0)
-    for (uint32_t i = 0; i < ntiles && i < kStages - 1; ++i) fill(i);
+    for (uint32_t i = 0; i < ntiles && i < S - 1; ++i) fill(i);
   for (uint32_t i = 0; i < ntiles; ++i) {
-    if (threadIdx.x == 0 && i + kStages - 1 < ntiles) fill(i + kStages - 1);
-    const uint32_t c = c0 + i, st = c % kStages;
-    mbar_wait(r.full + st, (c / kStages) & 1u);
+    if (threadIdx.x == 0 && i + S - 1 < ntiles) fill(i + S - 1);
+    const uint32_t c = c0 + i, st = c % S;
+    mbar_wait(r.full + st, (c / S) & 1u);
     use(i, r.buf + st * kStageBytes);
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(r.empty + st);
@@ -756,7 +758,7 @@ struct PersistSmem {
   lk_desc desc;
   uint32_t cmd, rank, count, slot;
   ReduceSmem red;
-  uint64_t full[kStages], empty[kStages];
+  uint64_t full[kMaxStages], empty[kMaxStages];
 };
 
 __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const __grid_constant__ lk_dev_args a) {
@@ -768,7 +770,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     return;
   }
   extern __shared__ __align__(128) uint8_t dyn_smem[];
-  Ring ring{dyn_smem, sm.full, sm.empty};
+  Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages};
   Ring* rp = a.use_tma ? &ring : nullptr;
   uint32_t g = 0;
   if (rp) ring_init(ring, T);
@@ -875,13 +877,13 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
 // ---------------------------------------------------------------- baseline
 __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, uint32_t* ctr, int use_tma) {
   __shared__ ReduceSmem rs;
-  __shared__ uint64_t full[kStages], empty[kStages];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   if (single_thread_kind(d.kind)) {
     if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
     return;
   }
-  Ring ring{dyn_smem, full, empty};
+  Ring ring{dyn_smem, full, empty, kDefaultStages};
   uint32_t g = 0;
   if (use_tma) ring_init(ring, blockDim.x);
   run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, use_tma ? &ring : nullptr, g);
@@ -923,7 +925,8 @@ cudaError_t lk_preload_kernels() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, lk_work_kernel);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(lk_work_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRingBytes));
+    e = cudaFuncSetAttribute(lk_work_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kDefaultStages * kStageBytes));
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_pingpong_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_clocksync_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_persistent_kernel);
@@ -947,11 +950,12 @@ cudaError_t lk_launch_persistent(const lk_dev_args& a, uint32_t grid, uint32_t t
 
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads, uint32_t* reduce_ctr,
                            cudaStream_t st, int use_tma) {
-  lk_work_kernel<<<grid, threads, use_tma ? kRingBytes : 0, st>>>(d, reduce_ctr, use_tma);
+  lk_work_kernel<<<grid, threads, use_tma ? kDefaultStages * kStageBytes : 0, st>>>(d, reduce_ctr, use_tma);
   return cudaGetLastError();
 }
 
-size_t lk_ring_bytes() { return kRingBytes; }
+size_t lk_ring_bytes(uint32_t stages) { return size_t(stages ? stages : kDefaultStages) * kStageBytes; }
+uint32_t lk_ring_max_stages() { return kMaxStages; }
 
 cudaError_t lk_launch_pingpong(volatile uint32_t* flag, volatile uint32_t* echo, uint64_t rounds,
                                cudaStream_t st) {

@@ -68,6 +68,7 @@ class NativeConfig:
     acquire_poll: bool = False
     fence_always: bool = False
     tma_payload: bool = True        # payload tiles via the TMA bulk ring (False: 128-bit LSU loads)
+    ring_stages: int = 12           # TMA ring depth, 16-KiB stages (2..12)
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
 
     def __post_init__(self) -> None:
@@ -94,6 +95,7 @@ class NativeConfig:
         c.poll_backoff_ns = self.poll_backoff_ns
         c.cell_stride = self.cell_stride
         c.status_stride = self.status_stride
+        c.ring_stages = self.ring_stages
         c.num_slots = self.num_slots
         c.poll_replicas = self.poll_replicas
         c.poll_spacing_ns = self.poll_spacing_ns
