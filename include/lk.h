@@ -112,7 +112,7 @@ typedef struct lk_config {
   uint32_t poll_spacing_ns;      /* stagger between replica loads / sweeps; 0 = 300 */
   uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default) or LK_POLL_GATEWAY */
   uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 128 */
-  uint32_t ring_stages;          /* TMA payload ring depth in 16-KiB stages, 2..12; 0 = 12 */
+  uint32_t ring_stages;          /* TMA payload ring depth in 16-KiB stages, 2..12; 0 = 6 */
 } lk_config;
 
 /* How to_gpu words reach the workers.  DIRECT: every worker polls its own

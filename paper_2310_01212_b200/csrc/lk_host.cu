@@ -362,7 +362,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     return fail(LK_E_CONFIG, "status_stride must be 16, 32, 64 or 128");
   if (cfg.poll_mode > LK_POLL_GATEWAY) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
   if (cfg.poll_replicas == 0) cfg.poll_replicas = 1;
-  if (cfg.ring_stages == 0) cfg.ring_stages = 12;
+  if (cfg.ring_stages == 0) cfg.ring_stages = 6;
   if (cfg.ring_stages < 2 || cfg.ring_stages > lk_ring_max_stages())
     return fail(LK_E_CONFIG, "ring_stages must be 2..%u", lk_ring_max_stages());
   if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)

@@ -114,16 +114,16 @@ __device__ __forceinline__ void st4(uint4* p, uint4 v) {
 // Payload tiles stream HBM -> shared memory with cp.async.bulk (the TMA
 // engine's 1-D bulk copy: no tensor map, no register staging), completion
 // counted on an mbarrier by transaction bytes.  Up to `stages` tiles of
-// kStageBytes are in flight per SM (12 x 16 KiB = 192 KiB by default: at
-// ~44 GB/s per SM and a loaded HBM latency of 1.5-2 us Little's law asks for
-// ~66-88 KiB per SM, and the producer refills a stage only after every warp
-// released it), issued by one elected thread while every worker thread
-// consumes.  The ring persists across dispatches: `g` counts tiles consumed
+// kStageBytes are in flight per SM (6 x 16 KiB = 96 KiB by default: at
+// ~44 GB/s per SM and a loaded HBM latency of ~1.5 us Little's law asks for
+// ~66 KiB per SM; 4-12 stages measured within noise of each other,
+// tools/sweep_ring.py), issued by one elected thread while every worker
+// thread consumes.  The ring persists across dispatches: `g` counts tiles consumed
 // since the barriers were initialised (identical in every thread), so
 // stage = g % stages and the mbarrier phase parity = (g / stages) & 1.
 constexpr uint32_t kStageBytes = 16384;
 constexpr uint32_t kMaxStages = 12;
-constexpr uint32_t kDefaultStages = 12;
+constexpr uint32_t kDefaultStages = 6;
 
 struct Ring {
   uint8_t* buf;       // stages x kStageBytes, 128-B aligned, dynamic shared memory

@@ -68,7 +68,7 @@ class NativeConfig:
     acquire_poll: bool = False
     fence_always: bool = False
     tma_payload: bool = True        # payload tiles via the TMA bulk ring (False: 128-bit LSU loads)
-    ring_stages: int = 12           # TMA ring depth, 16-KiB stages (2..12)
+    ring_stages: int = 6            # TMA ring depth, 16-KiB stages (2..12)
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
 
     def __post_init__(self) -> None:
