@@ -168,12 +168,14 @@ __device__ __forceinline__ uint4 lds4(const uint8_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t ring_consumer_warps(uint32_t T) { return T >= 64 ? T / 32 - 1 : 1; }
+
 // Called by every worker thread once, before the first dispatch.
 __device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
   if (threadIdx.x == 0) {
     for (uint32_t k = 0; k < r.stages; ++k) {
       mbar_init(r.full + k, 1);
-      mbar_init(r.empty + k, T / 32);   // one arrival per consumer warp
+      mbar_init(r.empty + k, ring_consumer_warps(T));   // one arrival per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -184,8 +186,13 @@ __device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
 // kStages-1 tiles ahead; `load(i, stage_ptr, bar)` issues tile i's bulk copies
 // (after arming the barrier with its byte count), `use(i, stage_ptr)` consumes
 // it in every thread, and each warp releases the stage with one arrival.
+// Warp 0 is the producer: its lane 0 issues every tile, running ahead until
+// a stage it needs is still held, and never consumes (so a refill is never
+// delayed by the producer's own share of a tile).  Warps 1.. consume;
+// `use(i, stage, ci, nc)` gets the consumer's index and count.
+
 template <class Load, class Use>
-__device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntiles, const Load& load,
+__device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntiles, uint32_t T, const Load& load,
                                             const Use& use) {
   const uint32_t c0 = g, S = r.stages;
   auto fill = [&](uint32_t i) {
@@ -193,15 +200,22 @@ __device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntile
     mbar_wait(r.empty + st, ((f / S) & 1u) ^ 1u);   // previous use of this stage released
     load(i, r.buf + st * kStageBytes, r.full + st);
   };
-  if (threadIdx.x == 0)
-    for (uint32_t i = 0; i < ntiles && i < S - 1; ++i) fill(i);
-  for (uint32_t i = 0; i < ntiles; ++i) {
-    if (threadIdx.x == 0 && i + S - 1 < ntiles) fill(i + S - 1);
-    const uint32_t c = c0 + i, st = c % S;
-    mbar_wait(r.full + st, (c / S) & 1u);
-    use(i, r.buf + st * kStageBytes);
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(r.empty + st);
+  const bool split = T >= 64;
+  const uint32_t ci = split ? threadIdx.x - 32 : threadIdx.x, nc = split ? T - 32 : T;
+  if (split && threadIdx.x < 32) {
+    if (threadIdx.x == 0)
+      for (uint32_t i = 0; i < ntiles; ++i) fill(i);
+  } else {
+    if (!split && threadIdx.x == 0)
+      for (uint32_t i = 0; i < ntiles && i < S - 1; ++i) fill(i);
+    for (uint32_t i = 0; i < ntiles; ++i) {
+      if (!split && threadIdx.x == 0 && i + S - 1 < ntiles) fill(i + S - 1);
+      const uint32_t c = c0 + i, st = c % S;
+      mbar_wait(r.full + st, (c / S) & 1u);
+      use(i, r.buf + st * kStageBytes, ci, nc);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(r.empty + st);
+    }
   }
   g = c0 + ntiles;
 }
@@ -279,7 +293,7 @@ __device__ __forceinline__ void map_tma(const lk_desc& d, Part p, const Op& op, 
   const uint64_t nv = ve > vb ? ve - vb : 0;
   const uint32_t ntiles = uint32_t((nv + kTileV - 1) / kTileV);
   ring_stream(
-      r, g, ntiles,
+      r, g, ntiles, T,
       [&](uint32_t i, uint8_t* stage, uint64_t* bar) {
         const uint64_t v0 = vb + uint64_t(i) * kTileV;
         const uint32_t bytes = uint32_t(min(uint64_t(kTileV), ve - v0)) * 16u;
@@ -287,10 +301,10 @@ __device__ __forceinline__ void map_tma(const lk_desc& d, Part p, const Op& op, 
         bulk_g2s(stage, a4 + v0, bytes, bar);
         if (kTwo) bulk_g2s(stage + kStageBytes / 2, c4 + v0, bytes, bar);
       },
-      [&](uint32_t i, const uint8_t* stage) {
+      [&](uint32_t i, const uint8_t* stage, uint32_t ci, uint32_t nc) {
         const uint64_t v0 = vb + uint64_t(i) * kTileV;
         const uint32_t nvt = uint32_t(min(uint64_t(kTileV), ve - v0));
-        for (uint32_t v = t; v < nvt; v += T) {
+        for (uint32_t v = ci; v < nvt; v += nc) {
           const uint4 x = lds4(stage + 16 * v);
           const uint4 y = kTwo ? lds4(stage + kStageBytes / 2 + 16 * v) : x;
           st4(o4 + v0 + v, vop(op, x, y));
@@ -335,16 +349,16 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
     const uint64_t nv = ve > vb ? ve - vb : 0;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     ring_stream(
-        *ring, g, uint32_t((nv + kTileV - 1) / kTileV),
+        *ring, g, uint32_t((nv + kTileV - 1) / kTileV), T,
         [&](uint32_t i, uint8_t* stage, uint64_t* bar) {
           const uint64_t v0 = vb + uint64_t(i) * kTileV;
           const uint32_t bytes = uint32_t(min(uint64_t(kTileV), ve - v0)) * 16u;
           mbar_expect_tx(bar, bytes);
           bulk_g2s(stage, x4 + v0, bytes, bar);
         },
-        [&](uint32_t i, const uint8_t* stage) {
+        [&](uint32_t i, const uint8_t* stage, uint32_t ci, uint32_t nc) {
           const uint32_t nvt = uint32_t(min(uint64_t(kTileV), ve - (vb + uint64_t(i) * kTileV)));
-          for (uint32_t v = t; v < nvt; v += T) {
+          for (uint32_t v = ci; v < nvt; v += nc) {
             const uint4 r = lds4(stage + 16 * v);
             s.x += __uint_as_float(r.x); s.y += __uint_as_float(r.y);
             s.z += __uint_as_float(r.z); s.w += __uint_as_float(r.w);
