@@ -525,13 +525,16 @@ def run_lk_arm(args, world, rank, local):
 
     # e2e through the Python API (reference-facing plugin), host buffers = mailbox words
     e2e_rounds = args.e2e_rounds
+    barrier(world)
     t0 = time.perf_counter_ns()
     for k in range(e2e_rounds):
         m = rr_masks[k % n]
         session.trigger(m, empty)
         session.wait(m)
     e2e_dt = (time.perf_counter_ns() - t0) / 1e9
-    e2e_value = e2e_rounds / e2e_dt
+    barrier(world)
+    e2e_t, e2e_units = gather_max_sum(world, e2e_dt, e2e_rounds)
+    e2e_value = e2e_units / e2e_t          # whole job: all ranks' tasks / slowest rank
 
     # configs[0] shape on the GPU: 4 workers round robin, int32 vector add of 64 Ki
     # elements per task (the CPU reference's workload), trigger->done per task
