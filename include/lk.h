@@ -110,7 +110,7 @@ typedef struct lk_config {
   uint32_t flags;                /* LK_CF_* */
   uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 1 */
   uint32_t poll_spacing_ns;      /* stagger between replica loads / sweeps; 0 = 300 */
-  uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default) or LK_POLL_GATEWAY */
+  uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default), LK_POLL_GATEWAY or LK_POLL_HYBRID */
   uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 128 */
   uint32_t ring_stages;          /* TMA payload ring depth in 16-KiB stages, 2..12; 0 = 6 */
 } lk_config;
@@ -122,6 +122,12 @@ typedef struct lk_config {
  * measured slower on the B200 hosts, kept as an option). */
 #define LK_POLL_DIRECT  0u
 #define LK_POLL_GATEWAY 1u
+/* HYBRID: writes to at most LK_HYBRID_DIRECT_MAX workers go to their direct
+ * cells, wider ones (full-mask triggers, acks, EXIT) as one ring event; each
+ * CTA runs a host-cell poller warp and a mailbox poller warp that forward into
+ * shared memory, where the protocol thread watches both. */
+#define LK_POLL_HYBRID  2u
+#define LK_HYBRID_DIRECT_MAX 8u
 
 #define LK_CF_ACQUIRE_POLL   1u  /* poll with ld.acquire.sys instead of ld.relaxed.sys */
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */

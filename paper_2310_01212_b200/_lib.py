@@ -42,6 +42,7 @@ CF_LSU_PAYLOAD = 4
 CF_TIMELINE = 8
 POLL_DIRECT = 0
 POLL_GATEWAY = 1
+POLL_HYBRID = 2
 HINT_EMPTY = 1
 
 WERR_NAMES = {

@@ -125,7 +125,10 @@ struct lk_session {
   std::vector<uint32_t> last_word;            // GATEWAY: shadow of each worker's to_gpu value
   std::mutex post_mu;
   std::vector<uint32_t> all_ids;
-  bool gateway = false;
+  bool gateway = false;                       // event ring in use (GATEWAY or HYBRID)
+  bool hybrid = false;
+  uint32_t dreps = 1;                         // replicas of each direct cell (HYBRID: 1)
+  std::vector<uint32_t> host_dseq;            // writes that went to each worker's direct cell
   volatile unsigned long long* status = nullptr;  // stride status_u64
   volatile unsigned long long* err = nullptr;
   volatile uint32_t* err_any = nullptr;
@@ -174,20 +177,24 @@ struct lk_session {
   // One logical to_gpu write: {word, seq} into every replica (seq = this
   // worker's host write index; the device acts only on newer seqs, so the
   // replicas, written one after another, can never step it backwards).
-  // DIRECT: one worker's cell value {word:32, seq:24, hint:8} (lk_kernels.cu: accept).
+  // DIRECT: one worker's cell value {word:32, seq:24, hint:8} (lk_kernels.cu:
+  // accept).  seq counts the writes made through this cell (all of them in
+  // DIRECT mode; in HYBRID the rest travel as ring events).
   inline void host_write(uint32_t i, uint32_t w, uint32_t hint = 0) {
     const uint32_t sq = ++host_seq[i];
+    const uint32_t dq = ++host_dseq[i];
+    last_word[i] = w;
     if (cfg.record_trace) host_log[i].push_back(HostRec{sq, w, now_ns()});
-    const unsigned long long v = uint64_t(w) | (uint64_t(sq & 0xFFFFFFu) << 32) | (uint64_t(hint & 0xFFu) << 56);
-    unsigned long long* c = to_gpu + uint64_t(i) * replicas * cell_u64;
-    for (uint32_t k = 0; k < replicas; ++k) __atomic_store_n(c + k * cell_u64, v, __ATOMIC_RELEASE);
+    const unsigned long long v = uint64_t(w) | (uint64_t(dq & 0xFFFFFFu) << 32) | (uint64_t(hint & 0xFFu) << 56);
+    unsigned long long* c = to_gpu + uint64_t(i) * dreps * cell_u64;
+    for (uint32_t k = 0; k < dreps; ++k) __atomic_store_n(c + k * cell_u64, v, __ATOMIC_RELEASE);
   }
   // One logical write of `w` to every worker in ids (ascending), i.e. the
   // reference's `for i in sm_ids: _host_write(i, word)` (native.py:224-225).
   // GATEWAY: a single ring event carries the word and the worker mask.
   // Returns false if the ring stayed full past the timeout.
   bool post(const std::vector<uint32_t>& ids, uint32_t w, uint32_t hint = 0) {
-    if (!gateway) {
+    if (!gateway || (hybrid && ids.size() <= LK_HYBRID_DIRECT_MAX)) {
       for (uint32_t i : ids) host_write(i, w, hint);
       return true;
     }
@@ -217,8 +224,8 @@ struct lk_session {
     return true;
   }
   inline uint32_t to_gpu_word(uint32_t i) const {
-    if (gateway) return last_word[i];
-    return uint32_t(__atomic_load_n(to_gpu + uint64_t(i) * replicas * cell_u64, __ATOMIC_ACQUIRE));
+    if (gateway) return last_word[i];   // (HYBRID: whichever channel wrote last)
+    return uint32_t(__atomic_load_n(to_gpu + uint64_t(i) * dreps * cell_u64, __ATOMIC_ACQUIRE));
   }
 };
 
@@ -360,7 +367,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.status_stride == 0) cfg.status_stride = 128;
   if (cfg.status_stride != 16 && cfg.status_stride != 32 && cfg.status_stride != 64 && cfg.status_stride != 128)
     return fail(LK_E_CONFIG, "status_stride must be 16, 32, 64 or 128");
-  if (cfg.poll_mode > LK_POLL_GATEWAY) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
+  if (cfg.poll_mode > LK_POLL_HYBRID) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
+  if (cfg.poll_mode == LK_POLL_HYBRID && cfg.poll_replicas > 2)
+    return fail(LK_E_CONFIG, "hybrid mode takes 1 or 2 event-ring replicas");
   if (cfg.poll_replicas == 0) cfg.poll_replicas = 1;
   if (cfg.ring_stages == 0) cfg.ring_stages = 6;
   if (cfg.ring_stages < 2 || cfg.ring_stages > lk_ring_max_stages())
@@ -371,8 +380,8 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     return fail(LK_E_CONFIG, "gateway mode takes 1, 2 or 4 event-ring replicas");
   if (cfg.poll_spacing_ns == 0) cfg.poll_spacing_ns = 300;
   if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 512;
-  if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 608)
-    return fail(LK_E_CONFIG, "threads_per_worker must be a multiple of 32 and <= 608");
+  if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 544)
+    return fail(LK_E_CONFIG, "threads_per_worker must be a multiple of 32 and <= 544");
   if (cfg.num_slots == 0) cfg.num_slots = 1024;
   if (cfg.trace_capacity == 0) cfg.trace_capacity = 65536;
   if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
@@ -400,7 +409,10 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->cell_u64 = cfg.cell_stride / 8;
   s->status_u64 = cfg.status_stride / 8;
   s->replicas = cfg.poll_replicas;
-  s->gateway = cfg.poll_mode == LK_POLL_GATEWAY;
+  s->gateway = cfg.poll_mode == LK_POLL_GATEWAY || cfg.poll_mode == LK_POLL_HYBRID;
+  s->hybrid = cfg.poll_mode == LK_POLL_HYBRID;
+  s->dreps = s->hybrid ? 1 : s->replicas;
+  s->host_dseq.assign(s->nw, 0);
   s->last_word.assign(s->nw, LK_NOP);
   for (uint32_t i = 0; i < s->nw; ++i) s->all_ids.push_back(i);
   if (s->gateway && s->nw > 192) {
@@ -432,8 +444,11 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   // --- pinned mapped mailboxes: to_gpu (DIRECT replicas | GATEWAY doorbell
   // replicas) | status | err | smid, 4 KiB aligned
   auto al = [](size_t x) { return (x + 4095) & ~size_t(4095); };
-  const size_t tob = s->gateway ? al(size_t(s->replicas) * s->ring_entries * 64 + 128)
-                                : al(size_t(s->nw) * s->replicas * cfg.cell_stride);
+  // HYBRID: direct cells (1 replica) first, then the ring replicas + tail line
+  const size_t directb = (!s->gateway || s->hybrid)
+                             ? al(size_t(s->nw) * (s->hybrid ? 1 : s->replicas) * cfg.cell_stride) : 0;
+  const size_t ringb = s->gateway ? al(size_t(s->replicas) * s->ring_entries * 64 + 128) : 0;
+  const size_t tob = directb + ringb;
   const size_t cells = al(size_t(s->nw) * cfg.status_stride);
   const size_t err_words = (size_t(s->nw) + 15) / 16 * 16;   // err[] then err_any on its own line
   const size_t errb = al(err_words * 8 + 128), smidb = al(size_t(s->nw) * 4);
@@ -443,15 +458,16 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(ce)));
   memset(s->host_block, 0, host_bytes);
   s->to_gpu = reinterpret_cast<unsigned long long*>(s->host_block);
-  s->ring = s->to_gpu;
-  s->gw_tail = s->to_gpu + size_t(s->replicas) * s->ring_entries * 8;   // own line after the rings
+  s->ring = s->to_gpu + directb / 8;
+  s->gw_tail = s->ring + size_t(s->replicas) * s->ring_entries * 8;   // own line after the rings
   s->status = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob);
   s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob + cells);
   s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + tob + cells + errb);
   s->err_any = reinterpret_cast<volatile uint32_t*>(s->err + err_words);
   for (uint32_t i = 0; i < s->nw; ++i) {
     for (uint32_t k = 0; k < s->replicas; ++k) {
-      if (!s->gateway) s->to_gpu[(uint64_t(i) * s->replicas + k) * s->cell_u64] = LK_NOP;   // {NOP, seq 0}
+      if (k < s->dreps && (!s->gateway || s->hybrid))
+        s->to_gpu[(uint64_t(i) * s->dreps + k) * s->cell_u64] = LK_NOP;   // {NOP, seq 0}
     }
     s->status[uint64_t(i) * s->status_u64] = uint64_t(LK_NOP) | (uint64_t(LK_PHASE_BOOTING) << 32);
     s->smid[i] = 0xFFFFFFFFu;
@@ -498,7 +514,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   ce = lk_persistent_configure(s->smem);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "smem attr: %s", cudaGetErrorString(ce)));
   int bps = 0;
-  const uint32_t launch_threads = s->threads + 32;   // + the gateway warp (CTA 0; retires elsewhere)
+  // + three warps: host-cell poller and mailbox poller (HYBRID), gateway (CTA 0);
+  // unused ones retire at once
+  const uint32_t launch_threads = s->threads + 96;
   ce = lk_persistent_occupancy(launch_threads, s->smem, &bps);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "occupancy: %s", cudaGetErrorString(ce)));
   if (bps != 1) return cleanup(fail(LK_E_INIT, "expected exactly 1 resident worker per SM, got %d", bps));

@@ -32,8 +32,8 @@
 namespace {
 
 constexpr uint32_t kMaxThreads = 1024;
-// Persistent CTA: up to 608 worker threads + the gateway warp; the bound
-// leaves ~96 registers per thread for the gateway's in-flight sweeps.
+// Persistent CTA: up to 544 worker threads + three extra warps (channel
+// pollers, gateway); the bound leaves ~96 registers per thread.
 constexpr uint32_t kPersistMaxThreads = 640;
 constexpr uint32_t kCmdWork = 1;
 constexpr uint32_t kCmdExit = 2;
@@ -466,6 +466,7 @@ struct Elected {           // thread 0's private protocol state
   uint32_t seq;            // host write index of the current to_gpu word
   uint32_t cur;            // current to_gpu word
   uint32_t hint;           // host hint bits of the current value (LK_HINT_*)
+  uint32_t dseq, rseq;     // HYBRID: writes seen on the direct cell / via the event ring
   uint32_t tcnt;
   bool dirty;              // cur not yet stepped to a fixed point
   uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
@@ -574,6 +575,25 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
   return kFastNone;
 }
 
+// HYBRID: a value from one of two channels, each with its own 24-bit write
+// count (`last`: the direct cell's or the ring's); the host's per-worker write
+// index is their sum.  The host issues a worker's next write only after the
+// device answered the previous one, so at most one channel holds an unseen
+// value and the sum orders them.
+__device__ __forceinline__ bool accept_chan(Elected& e, unsigned long long c, uint32_t& last, bool timeline) {
+  const uint32_t sq = uint32_t(c >> 32) & 0xFFFFFFu;
+  const uint32_t delta = (sq - last) & 0xFFFFFFu;
+  if (delta == 0 || delta >= 0x800000u) return false;
+  last += delta;
+  e.seq = e.dseq + e.rseq;
+  e.cur = uint32_t(c);
+  e.hint = uint32_t(c >> 56);
+  e.dirty = true;
+  e.c_seen = clock64();
+  if (timeline) e.t_seen = globaltimer();
+  return true;
+}
+
 // Step the current word to a fixed point, exactly as the reference worker
 // re-reads a level-triggered cell until it stops making progress
 // (native.py:158-195).  Returns an action, or LK_ACT_NONE once settled.
@@ -661,7 +681,55 @@ __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t 
 }
 
 // Inlined into the worker loop so the protocol state stays in registers.
-__device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e) {
+__device__ __forceinline__ unsigned long long lds_volatile64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_volatile64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(smem_u32(p)), "l"(v) : "memory");
+}
+
+// HYBRID mode, protocol thread: both channels arrive in shared memory (chan[0]
+// from this CTA's host-cell poller warp, chan[1] from its mailbox poller
+// warp), so the thread spins on two ~30-cycle shared loads and never holds a
+// PCIe or L2 load in flight itself.
+__device__ __forceinline__ uint32_t poll_hybrid(const lk_dev_args& a, uint32_t wid, Elected& e,
+                                                const unsigned long long* chan) {
+  const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
+  for (;;) {
+    const uint32_t act = settle(a, wid, e);
+    if (act != LK_ACT_NONE) return act;
+    for (;;) {
+      bool got = accept_chan(e, lds_volatile64(chan), e.dseq, timeline);
+      if (!got) got = accept_chan(e, lds_volatile64(chan + 1), e.rseq, timeline);
+      if (!got) continue;
+      const uint32_t f = fast_step(a, wid, e);
+      if (f == kFastBegin) return LK_ACT_BEGIN;
+      if (f == kFastNone) break;
+    }
+  }
+}
+
+// HYBRID mode, channel pollers (lane 0 of two extra warps per CTA): forward
+// every new value of the host cell (one ld.relaxed.sys in flight) or of the
+// device mailbox (L2) into the CTA's shared-memory channel slot.
+__device__ __noinline__ void chan_poller(const unsigned long long* src, bool sys, unsigned long long* slot,
+                                         const volatile uint32_t* stop) {
+  uint32_t last = 0;
+  while (!*stop) {
+    const unsigned long long v = sys ? ld_cell(src, false) : ld_relaxed_gpu64(src);
+    const uint32_t sq = uint32_t(v >> 32) & 0xFFFFFFu;
+    if (sq != last) {
+      last = sq;
+      sts_volatile64(slot, v);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Elected& e,
+                                         const unsigned long long* chan) {
+  if (a.poll_mode == LK_POLL_HYBRID) return poll_hybrid(a, wid, e, chan);
   if (a.poll_mode == LK_POLL_GATEWAY) return poll_mailbox(a, wid, e);
   switch (a.replicas) {
     case 1: return poll_k<1>(a, wid, e);
@@ -773,14 +841,31 @@ struct PersistSmem {
   uint32_t cmd, rank, count, slot;
   ReduceSmem red;
   uint64_t full[kMaxStages], empty[kMaxStages];
+  unsigned long long chan[2];      // HYBRID: latest direct-cell value, latest mailbox value
+  uint32_t stop;                   // HYBRID: the protocol thread left its loop
 };
 
 __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const __grid_constant__ lk_dev_args a) {
   __shared__ PersistSmem sm;
   const uint32_t wid = blockIdx.x;
   const uint32_t T = a.wthreads;
-  if (threadIdx.x >= T) {           // the extra warp: CTA 0 hosts the gateway, the rest retire
-    if (wid == 0 && a.poll_mode == LK_POLL_GATEWAY) gateway(a);
+  if (threadIdx.x == 0) {
+    sm.chan[0] = 0ull;              // {NOP, count 0}: nothing new on either channel
+    sm.chan[1] = 0ull;
+    sm.stop = 0;
+  }
+  __syncthreads();                  // the only CTA-wide barrier: before the roles split
+  if (threadIdx.x >= T) {           // three extra warps: host-cell poller, mailbox poller, gateway
+    const uint32_t xw = (threadIdx.x - T) >> 5, lane = threadIdx.x & 31;
+    const bool hybrid = a.poll_mode == LK_POLL_HYBRID;
+    if (xw == 0) {
+      if (hybrid && lane == 0)
+        chan_poller(a.to_gpu + uint64_t(wid) * a.cell_u64, true, sm.chan, &sm.stop);   // 1 replica
+    } else if (xw == 1) {
+      if (hybrid && lane == 0) chan_poller(a.dmb + uint64_t(wid) * a.dmb_u64, false, sm.chan + 1, &sm.stop);
+    } else if (wid == 0 && (hybrid || a.poll_mode == LK_POLL_GATEWAY)) {
+      gateway(a);
+    }
     return;
   }
   extern __shared__ __align__(128) uint8_t dyn_smem[];
@@ -794,6 +879,8 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.seq = 0;       // the host's initial {NOP, seq 0} value
   e.cur = LK_NOP;
   e.hint = 0;
+  e.dseq = 0;
+  e.rseq = 0;
   e.tcnt = 0;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   e.t_seen = 0;
@@ -805,7 +892,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   for (;;) {
     if (threadIdx.x == 0) {
       for (;;) {
-        const uint32_t act = poll(a, wid, e);
+        const uint32_t act = poll(a, wid, e, sm.chan);
         if (act == LK_ACT_EXIT) { sm.cmd = kCmdExit; break; }
         const uint32_t slot = e.st.slot;
         if (slot >= a.num_slots) { report_error(a, wid, e, LK_WERR_BAD_SLOT, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
@@ -885,7 +972,10 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
       write_timeline(a, wid, e, t_begin, t_end, c_begin, clock64(), true);
     }
   }
-  if (threadIdx.x == 0) atomicAdd(a.exited, 1u);   // lets the gateway retire
+  if (threadIdx.x == 0) {
+    atomicAdd(a.exited, 1u);                      // lets the gateway retire
+    *reinterpret_cast<volatile uint32_t*>(&sm.stop) = 1u;   // and this CTA's channel pollers
+  }
 }
 
 // ---------------------------------------------------------------- baseline

@@ -34,7 +34,7 @@ log = logging.getLogger(__name__)
 PURE_SPIN = "pure_spin"
 SPIN_THEN_YIELD = "spin_then_yield"
 BACKEND = "b200"
-POLL_MODES = {"gateway": _lib.POLL_GATEWAY, "direct": _lib.POLL_DIRECT}
+POLL_MODES = {"direct": _lib.POLL_DIRECT, "gateway": _lib.POLL_GATEWAY, "hybrid": _lib.POLL_HYBRID}
 
 
 @dataclass(frozen=True)

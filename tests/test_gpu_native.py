@@ -306,7 +306,8 @@ def test_criterion_7_random_programs_on_gpu():
     assert_trace_ok(session, program, 8)
 
 
-@pytest.mark.parametrize("mode,replicas", [("direct", 1), ("direct", 4), ("gateway", 1), ("gateway", 4)])
+@pytest.mark.parametrize("mode,replicas", [("direct", 1), ("direct", 4), ("gateway", 1), ("gateway", 4),
+                                           ("hybrid", 1), ("hybrid", 2)])
 def test_poll_modes_random_programs(mode, replicas):
     """Both to_gpu delivery paths (gateway warp + device mailboxes, direct
     PCIe polling) and replica counts run the same random programs with
@@ -324,11 +325,11 @@ def test_poll_modes_random_programs(mode, replicas):
     assert_trace_ok(session, program, 12)
 
 
-@pytest.mark.parametrize("replicas", [1, 2])
-def test_gateway_back_to_back_single_worker_triggers(replicas):
+@pytest.mark.parametrize("mode,replicas", [("gateway", 1), ("gateway", 2), ("hybrid", 1)])
+def test_gateway_back_to_back_single_worker_triggers(mode, replicas):
     """148 separate trigger events queued before any wait, then one ack event
     for the whole mask: the event ring carries them all in order."""
-    session = start(None, trace_capacity=256, poll_mode="gateway", poll_replicas=replicas)
+    session = start(None, trace_capacity=256, poll_mode=mode, poll_replicas=replicas)
     n = session.num_workers
     work = WorkDescriptor(slot=0, kind="empty")
     for rep in range(3):
@@ -341,7 +342,7 @@ def test_gateway_back_to_back_single_worker_triggers(replicas):
     assert_trace_ok(session)
 
 
-@pytest.mark.parametrize("mode", ["direct", "gateway"])
+@pytest.mark.parametrize("mode", ["direct", "gateway", "hybrid"])
 def test_device_timeline_is_ordered(mode):
     session = start(None, timeline=True, poll_mode=mode)
     n = session.num_workers
@@ -454,3 +455,24 @@ def test_scenario_backend_rows():
     assert got[("LK", "Trigger")].samples == 20 and got[("BASE", "Launch")].samples == 20
     assert all(r.best <= r.avg <= r.worst for r in rows)
     assert "b200" in backend.rows_csv(rows)
+
+
+def test_hybrid_mixes_channels_per_worker():
+    """HYBRID: single-worker writes take the direct cell, wide ones the ring;
+    a worker alternating between both keeps one ordered write stream (the
+    golden projection and the replay both hold)."""
+    session = start(12, trace_capacity=4096, poll_mode="hybrid")
+    full = (1 << 12) - 1
+    program = []
+    for k in range(40):
+        if k % 3 == 0:
+            m = full                          # ring event (12 > LK_HYBRID_DIRECT_MAX)
+        elif k % 3 == 1:
+            m = 1 << (k % 12)                 # direct cell
+        else:
+            m = 0b101                         # direct cells (2 workers)
+        session.trigger(m, WorkDescriptor(slot=k % 8, iterations=k % 5))
+        program.append((m, k % 8))
+        session.wait(m)
+    session.dispose()
+    assert_trace_ok(session, program, 12)

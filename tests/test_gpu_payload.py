@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 RTOL_F32_REDUCE = 1e-6
 
 
-@pytest.fixture(scope="module", params=["tma-direct", "lsu-direct", "tma-gateway"])
+@pytest.fixture(scope="module", params=["tma-direct", "lsu-direct", "tma-gateway", "tma-hybrid"])
 def session(request):
     try:   # bring torch's CUDA state AND the kernels the torch test uses up before the
         # persistent kernel is resident: CUDA 12 loads kernels lazily, and a module

@@ -36,6 +36,6 @@ def run(label, rounds=20000, mode="rr", **kw):
 native.pin_host_thread(0)
 pp = native.pingpong(0, 20000)
 print("pingpong p50 %.2f p99.9 %.2f" % (pct(pp[100:], 50), pct(pp[100:], 99.9)))
-for cs, ss in ((128, 128), (32, 128), (128, 32), (32, 32), (64, 64), (32, 64), (128, 64), (128, 16)):
-    run(f"148 rr direct cell={cs} status={ss}", cell_stride=cs, status_stride=ss)
-    run(f"148 full-mask direct cell={cs} status={ss}", mode="full", rounds=5000, cell_stride=cs, status_stride=ss)
+for mode in ("direct", "gateway", "hybrid"):
+    run(f"148 rr {mode}", poll_mode=mode)
+    run(f"148 full-mask {mode}", mode="full", rounds=5000, poll_mode=mode)
