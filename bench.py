@@ -541,9 +541,6 @@ def run_lk_arm(args, world, rank, local):
     if rank == 0 and not args.no_payload:
         extras["config0_on_gpu"] = measure_config0(session, args.config0_rounds)
 
-    if not args.no_interference and rank == 0 and n >= args.lat_workers + 8:
-        extras["interference"] = measure_interference(session, args.lat_workers, args.interf_rounds,
-                                                      args.stream_mib)
     smids = session.smid_map
     session.dispose()
     session.close()
@@ -563,6 +560,19 @@ def run_lk_arm(args, world, rank, local):
                                                       args.payload_reps, 4 * L2_BYTES)
         psession.dispose()
         psession.close()
+
+    # configs[3]: latency partition beside an HBM-streaming partition, on a
+    # HYBRID session: the latency workers' single-worker writes use their
+    # direct cells, the 132-worker stream triggers travel as one ring event
+    # each (one host store instead of 132, and no extra PCIe polling).
+    if not args.no_interference and rank == 0 and n >= args.lat_workers + 8:
+        icfg = dataclasses.replace(cfg, poll_mode=args.interference_poll_mode)
+        isession, _ = native.NativeSession.start(icfg)
+        extras["interference"] = measure_interference(isession, args.lat_workers, args.interf_rounds,
+                                                      args.stream_mib)
+        extras["interference"]["poll_mode"] = args.interference_poll_mode
+        isession.dispose()
+        isession.close()
 
     # conventional launch+sync baseline, same host thread
     base = {}
@@ -656,11 +666,12 @@ def main():
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--backoff-ns", type=int, default=0)
     ap.add_argument("--cell-stride", type=int, default=128)
-    ap.add_argument("--poll-mode", choices=["gateway", "direct"], default="direct")
+    ap.add_argument("--poll-mode", choices=["gateway", "direct", "hybrid"], default="direct")
     ap.add_argument("--replicas", type=int, default=1)
     ap.add_argument("--spacing-ns", type=int, default=300)
     ap.add_argument("--lsu-payload", action="store_true", help="payload via 128-bit LSU loads, not the TMA ring")
-    ap.add_argument("--payload-poll-mode", choices=["gateway", "direct"], default="gateway")
+    ap.add_argument("--payload-poll-mode", choices=["gateway", "direct", "hybrid"], default="gateway")
+    ap.add_argument("--interference-poll-mode", choices=["gateway", "direct", "hybrid"], default="hybrid")
     ap.add_argument("--full-rounds", type=int, default=100_000)
     ap.add_argument("--e2e-rounds", type=int, default=100_000)
     ap.add_argument("--base-rounds", type=int, default=100_000)
