@@ -407,6 +407,7 @@ def measure_interference(session, lat_workers, rounds, stream_mib):
     src, dst = DeviceBuffer(4 * elems), DeviceBuffer(4 * elems)
     sw = WorkDescriptor(slot=900, kind="hbm_stream", data_in_ref=src, data_out_ref=dst, iterations=1)
     session.register(sw, stream_mask)
+    session.register(WorkDescriptor(slot=0, kind="empty"))
     session.bench_roundtrip(lat_masks, 0, 5000)
     _, solo, _ = session.bench_roundtrip(lat_masks, 0, rounds)
 
