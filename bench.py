@@ -393,6 +393,9 @@ def measure_config0(session, rounds, n=65536):
             "parity": "tests/test_gpu_payload.py::test_vector_add_i32_bit_exact (same kind, sizes, masks)"}
 
 
+_LOCAL_CORES: list = []
+
+
 def measure_interference(session, lat_workers, rounds, stream_mib):
     """configs[3]: a latency partition (workers [0, lat_workers), closed-loop
     empty tasks round-robin, driven from C) measured solo, then while the
@@ -414,7 +417,19 @@ def measure_interference(session, lat_workers, rounds, stream_mib):
     stop = threading.Event()
     stream_stats = {"dispatches": 0, "ns": 0, "spans_ns": []}
 
+    # the streaming partition's host thread gets its own core: threads inherit
+    # the creator's affinity, and two spinning threads on one core would turn
+    # the latency partition's tail into scheduler time slices
+    mine = sorted(os.sched_getaffinity(0))
+    local = sorted(_LOCAL_CORES or mine)
+    others = [c for c in local if c not in mine] or [c for c in range(os.cpu_count() or 1) if c not in mine]
+
     def streamer():
+        if others:
+            try:
+                os.sched_setaffinity(0, {others[-1]})
+            except OSError:
+                pass
         t0 = time.perf_counter_ns()
         while not stop.is_set():
             session.trigger(stream_mask, sw)
@@ -477,6 +492,7 @@ def run_lk_arm(args, world, rank, local):
         # one core of the GPU-local set, the highest-numbered one (core 0 takes
         # most housekeeping interrupts): no migrations under the spin loop
         local_cores = sorted(os.sched_getaffinity(0))
+        _LOCAL_CORES[:] = local_cores
         pinned_core = local_cores[-1 - (local % max(1, len(local_cores)))]
         os.sched_setaffinity(0, {pinned_core})
     except Exception:
