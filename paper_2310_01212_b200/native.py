@@ -118,6 +118,17 @@ def pin_host_thread(device: int) -> int:
 _LAZY_WARNED = False
 
 
+def _timing(phase: str, ns: int, mask: int) -> PhaseTiming:
+    """PhaseTiming for a validated phase/mask without re-running __post_init__
+    (the checks hold by construction here: ns >= 0, mask > 0)."""
+    t = _new(PhaseTiming)
+    t.__dict__.update(phase=phase, cycles=ns, sm_mask=mask)
+    return t
+
+
+_new = object.__new__
+
+
 def _warn_lazy_loading() -> None:
     """CUDA 12 loads kernel modules lazily on first launch, and a module load
     while the persistent kernel is resident can wait on it forever.  liblk.so
@@ -160,6 +171,8 @@ class NativeSession:
         self._staged: dict[int, tuple] = {}
         self._threads = [_WorkerHandle(self, i) for i in range(num_workers)]
         self._u64 = C.c_uint64()
+        self._u64_ref = C.byref(self._u64)
+        self._mask_cache: dict[int, bytes] = {}
         self._cells = (C.c_uint32 * num_workers)()
         self._cells2 = (C.c_uint32 * num_workers)()
         self._cells3 = (C.c_uint32 * num_workers)()
@@ -250,7 +263,12 @@ class NativeSession:
             _check_mask(mask, self.num_workers)   # raises with the reference's message
 
     def _mask(self, mask: int) -> bytes:
-        return mask.to_bytes(8 * self.nwords, "little")
+        b = self._mask_cache.get(mask)
+        if b is None:
+            if len(self._mask_cache) > 4096:
+                self._mask_cache.clear()
+            b = self._mask_cache[mask] = mask.to_bytes(8 * self.nwords, "little")
+        return b
 
     def register(self, work: WorkDescriptor, mask: int = 0) -> int:
         """Stage ``work`` in its device slot (a no-op when already staged).
@@ -261,7 +279,7 @@ class NativeSession:
         t0 = time.perf_counter_ns()
         work = as_work(work)
         key = mask if work.multi_worker else 0
-        if self._staged.get(work.slot) == (work, key) and self.descriptors.get(work.slot) is work:
+        if self._is_staged(work, key):
             return 0   # same descriptor object already staged with this mask
         d = work.to_c()
         rc = self._lib.lk_register_desc(self._h, work.slot, C.byref(d), self._mask(key), self.nwords)
@@ -276,27 +294,34 @@ class NativeSession:
         self._check(mask)
         work = as_work(work)
         key = mask if work.multi_worker else 0
-        if self._staged.get(work.slot) == (work, key) and self.descriptors.get(work.slot) is work:
+        if self._is_staged(work, key):
             d = None   # this descriptor object is already staged for this worker set
         else:
             d = C.byref(work.to_c())
-        rc = self._lib.lk_trigger(self._h, self._mask(mask), self.nwords, work.slot, d, C.byref(self._u64))
-        _lib.check(rc)
+        rc = self._lib.lk_trigger(self._h, self._mask(mask), self.nwords, work.slot, d, self._u64_ref)
+        if rc:
+            _lib.raise_for(rc)
         if d is not None:
             self.descriptors[work.slot] = work
             self._staged[work.slot] = (work, key)
-        timing = PhaseTiming(PHASE_TRIGGER, self._u64.value, mask)
+        timing = _timing(PHASE_TRIGGER, self._u64.value, mask)
         self.timings.append(timing)
         return timing
+
+    def _is_staged(self, work: WorkDescriptor, key: int) -> bool:
+        # identity, not dataclass equality: two descriptors with equal fields
+        # may point at different buffers (their refs are compare=False)
+        st = self._staged.get(work.slot)
+        return st is not None and st[0] is work and st[1] == key
 
     def wait(self, mask: int) -> PhaseTiming:
         """Spin (in C) until every masked worker published FINISHED, then ack."""
         self._require_live()
         self._check(mask)
-        rc = self._lib.lk_wait(self._h, self._mask(mask), self.nwords, C.byref(self._u64))
+        rc = self._lib.lk_wait(self._h, self._mask(mask), self.nwords, self._u64_ref)
         if rc:
             _lib.raise_for(rc, sm_ids=tuple(sms_in_mask(mask)))
-        timing = PhaseTiming(PHASE_WAIT, self._u64.value, mask)
+        timing = _timing(PHASE_WAIT, self._u64.value, mask)
         self.timings.append(timing)
         return timing
 
