@@ -396,6 +396,35 @@ def measure_config0(session, rounds, n=65536):
 _LOCAL_CORES: list = []
 
 
+def measure_multi_driver(session, drivers, rounds):
+    n = session.num_workers
+    groups = [list(range(g, n, drivers)) for g in range(drivers)]
+    res = [None] * drivers
+    mine = sorted(os.sched_getaffinity(0))
+    cores = [c for c in sorted(_LOCAL_CORES or mine) if c not in mine] or mine
+
+    def drive(g):
+        try:
+            os.sched_setaffinity(0, {cores[g % len(cores)]})
+        except OSError:
+            pass
+        _, done, cyc = session.bench_roundtrip([1 << i for i in groups[g]], 0, rounds)
+        res[g] = (done, cyc)
+
+    ths = [threading.Thread(target=drive, args=(g,)) for g in range(drivers)]
+    t0 = time.perf_counter_ns()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = (time.perf_counter_ns() - t0) / 1e9
+    done = np.concatenate([r[0] for r in res])
+    return {"drivers": drivers, "workers_per_driver": len(groups[0]), "rounds_per_driver": rounds,
+            "aggregate_tasks_per_s": round(drivers * rounds / dt, 1), "trigger_to_done": lat_summary(done),
+            "note": "each host thread on its own GPU-local core runs lk_bench_roundtrip over a disjoint "
+                    "worker group (round robin) of one session"}
+
+
 def measure_interference(session, lat_workers, rounds, stream_mib):
     """configs[3]: a latency partition (workers [0, lat_workers), closed-loop
     empty tasks round-robin, driven from C) measured solo, then while the
@@ -539,6 +568,11 @@ def run_lk_arm(args, world, rank, local):
     _, fdone, fcyc = session.bench_roundtrip([full], 0, args.full_rounds)
     extras["full_mask"] = {"trigger_to_done": lat_summary(fdone), "round_trip": lat_summary(fcyc),
                            "tasks_per_s": round(args.full_rounds / (fcyc.sum() / 1e9), 1)}
+
+    # several host threads, each a closed loop over its own worker group (one
+    # session; disjoint workers): aggregate tasks/s a B200 sustains
+    if rank == 0 and args.drivers > 1:
+        extras["multi_driver"] = measure_multi_driver(session, args.drivers, args.driver_rounds)
 
     # e2e through the Python API (reference-facing plugin), host buffers = mailbox words
     e2e_rounds = args.e2e_rounds
@@ -699,6 +733,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-interference", action="store_true")
     ap.add_argument("--config0-rounds", type=int, default=20_000)
+    ap.add_argument("--drivers", type=int, default=4, help="host threads for the multi-driver throughput extra")
+    ap.add_argument("--driver-rounds", type=int, default=100_000)
     ap.add_argument("--lat-workers", type=int, default=16, help="latency partition size (configs[3])")
     ap.add_argument("--interf-rounds", type=int, default=100_000)
     ap.add_argument("--stream-mib", type=int, default=512, help="hbm_stream src (= dst) MiB")
