@@ -403,12 +403,16 @@ def measure_multi_driver(session, drivers, rounds):
     mine = sorted(os.sched_getaffinity(0))
     cores = [c for c in sorted(_LOCAL_CORES or mine) if c not in mine] or mine
 
+    from paper_2310_01212_b200.device import WorkDescriptor
+    for g in range(drivers):   # one slot per driver: a slot is locked while un-waited (native.py:215-217)
+        session.register(WorkDescriptor(slot=800 + g, kind="empty"))
+
     def drive(g):
         try:
             os.sched_setaffinity(0, {cores[g % len(cores)]})
         except OSError:
             pass
-        _, done, cyc = session.bench_roundtrip([1 << i for i in groups[g]], 0, rounds)
+        _, done, cyc = session.bench_roundtrip([1 << i for i in groups[g]], 800 + g, rounds)
         res[g] = (done, cyc)
 
     ths = [threading.Thread(target=drive, args=(g,)) for g in range(drivers)]
