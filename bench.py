@@ -396,6 +396,27 @@ def measure_config0(session, rounds, n=65536):
 _LOCAL_CORES: list = []
 
 
+def measure_small_transfer(device, reps):
+    from paper_2310_01212_b200.device import DeviceBuffer
+    buf = DeviceBuffer(4096, device)
+    h = np.zeros(1, dtype=np.uint32)
+    up, down = [], []
+    for k in range(reps + 100):
+        h[0] = k
+        t0 = time.perf_counter_ns()
+        buf.upload(h)
+        t1 = time.perf_counter_ns()
+        h[:] = buf.download(np.uint32, 1)
+        t2 = time.perf_counter_ns()
+        if k >= 100:
+            up.append(t1 - t0)
+            down.append(t2 - t1)
+    buf.free()
+    return {"h2d_4B_memcpy": lat_summary(up), "d2h_4B_memcpy": lat_summary(down),
+            "note": "cudaMemcpyAsync + stream sync of 4 bytes through the Python API (DeviceBuffer "
+                    "upload/download); compare the mailbox word round trip in latency_us"}
+
+
 def measure_multi_driver(session, drivers, rounds):
     n = session.num_workers
     groups = [list(range(g, n, drivers)) for g in range(drivers)]
@@ -572,6 +593,12 @@ def run_lk_arm(args, world, rank, local):
     _, fdone, fcyc = session.bench_roundtrip([full], 0, args.full_rounds)
     extras["full_mask"] = {"trigger_to_done": lat_summary(fdone), "round_trip": lat_summary(fcyc),
                            "tasks_per_s": round(args.full_rounds / (fcyc.sum() / 1e9), 1)}
+
+    # the small-transfer case the paper's pathology is about (PAPER:160-162,
+    # P/link.py:84-122): a 4-byte cudaMemcpy each way (stream-synchronous)
+    # next to the mailbox word round trip above
+    if rank == 0:
+        extras["small_transfer"] = measure_small_transfer(device, 2000)
 
     # several host threads, each a closed loop over its own worker group (one
     # session; disjoint workers): aggregate tasks/s a B200 sustains
