@@ -396,6 +396,43 @@ def measure_config0(session, rounds, n=65536):
 _LOCAL_CORES: list = []
 
 
+def measure_table2(device, reps=100, iterations=20_000):
+    """The paper's Table II scenarios (P/bench.py:358-373: table2-single-sm,
+    table2-full-gpu; busy_loop work of 20,000 iterations, 100 reps) on B200
+    hardware through backend.run_b200: LK Init/Trigger/Wait/Dispose vs the
+    launch+sync baseline's Alloc/Launch/Wait/Dispose, in ns (avg / worst)."""
+    from paper_2310_01212_b200 import backend, host
+    from paper_2310_01212_b200.device import WorkDescriptor
+
+    class Scn:
+        def __init__(self, scope, n):
+            self.reps, self.scope, self.n = reps, scope, n
+
+        def cluster_count(self):
+            return self.n
+
+        def mask(self):
+            return 1 if self.scope == "single_sm" else host.full_mask(self.n)
+
+        def work(self):
+            return WorkDescriptor(slot=0, iterations=iterations)
+
+        def models(self):
+            return [host.MODEL_LK, host.MODEL_BASELINE]
+
+    from paper_2310_01212_b200 import _lib
+    import ctypes as C
+    nsm = C.c_int()
+    _lib.check(_lib.load().lk_sm_count(device, C.byref(nsm)))
+    out = {}
+    for scope in ("single_sm", "full_gpu"):
+        rows = backend.run_b200(Scn(scope, nsm.value), device=device)
+        out[f"table2-{scope.replace('_', '-')}"] = {f"{r.model}/{r.phase}": {"avg_ns": round(r.avg, 1),
+                                                                           "worst_ns": r.worst}
+                                                   for r in rows}
+    return out
+
+
 def measure_small_transfer(device, reps):
     from paper_2310_01212_b200.device import DeviceBuffer
     buf = DeviceBuffer(4096, device)
@@ -691,6 +728,9 @@ def run_lk_arm(args, world, rank, local):
         except Exception as exc:  # pragma: no cover
             extras["standalone_saxpy_kernel"] = {"error": str(exc)}
 
+    if rank == 0 and not args.no_table2:
+        extras["table2_b200"] = measure_table2(device)
+
     cpu = None
     if not args.no_cpu_baseline:
         cv, clat, ckind = cpu_baseline_config0(budget_s=args.cpu_budget_s)
@@ -764,6 +804,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-interference", action="store_true")
     ap.add_argument("--config0-rounds", type=int, default=20_000)
+    ap.add_argument("--no-table2", action="store_true")
     ap.add_argument("--drivers", type=int, default=4, help="host threads for the multi-driver throughput extra")
     ap.add_argument("--driver-rounds", type=int, default=100_000)
     ap.add_argument("--lat-workers", type=int, default=16, help="latency partition size (configs[3])")
