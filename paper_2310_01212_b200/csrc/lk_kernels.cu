@@ -422,8 +422,18 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
   }
 }
 
-__device__ __forceinline__ void busy_loop(uint64_t iterations) {
-  for (uint64_t i = 0; i < iterations; ++i) asm volatile("" : "+l"(i));
+// native.py:63-67 counts to `iterations`.  Each iteration here reads %clock
+// (a special-register read ptxas may neither fold nor hoist) and folds it into
+// a value the caller keeps live, so the trip count is really executed -- an
+// empty asm body in the loop lets ptxas compute the count and drop the loop.
+__device__ __noinline__ uint32_t busy_loop(uint64_t iterations) {
+  uint32_t acc = 0;
+  for (uint64_t i = 0; i < iterations; ++i) {
+    uint32_t c;
+    asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
+    acc ^= c;
+  }
+  return acc;
 }
 
 __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
@@ -843,6 +853,7 @@ struct PersistSmem {
   uint64_t full[kMaxStages], empty[kMaxStages];
   unsigned long long chan[2];      // HYBRID: latest direct-cell value, latest mailbox value
   uint32_t stop;                   // HYBRID: the protocol thread left its loop
+  uint32_t sink;                   // keeps busy_loop's result live
 };
 
 __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const __grid_constant__ lk_dev_args a) {
@@ -925,7 +936,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
           const bool tl = (a.flags & LK_CF_TIMELINE) != 0;
           c_begin = clock64();
           t_begin = tl ? globaltimer() : 0;
-          if (d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
+          if (d.kind == LK_KIND_BUSY_LOOP) sm.sink = busy_loop(d.iterations);
           const uint64_t t_end = tl ? globaltimer() : 0;
           const lk_step_out o = lk_complete_work(e.st);
           publish(a, wid, e, o.publish, (a.flags & LK_CF_FENCE_ALWAYS) != 0);
@@ -984,7 +995,7 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   if (single_thread_kind(d.kind)) {
-    if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) busy_loop(d.iterations);
+    if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) rs.last = busy_loop(d.iterations);
     return;
   }
   Ring ring{dyn_smem, full, empty, kDefaultStages};

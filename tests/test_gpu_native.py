@@ -476,3 +476,18 @@ def test_hybrid_mixes_channels_per_worker():
         session.wait(m)
     session.dispose()
     assert_trace_ok(session, program, 12)
+
+
+def test_busy_loop_really_counts():
+    """busy_loop(n) executes n iterations (native.py:63-67): the device cycles
+    between work begin and FINISHED grow with n, at least one per iteration."""
+    session = start(1)
+    cyc = {}
+    for n in (0, 100_000, 1_000_000):
+        session.trigger(1, WorkDescriptor(slot=3, iterations=n))
+        session.wait(1)
+        t = session.last_timeline().astype(np.int64)
+        cyc[n] = int(t[0, 7] - t[0, 6])
+    session.dispose()
+    assert cyc[1_000_000] >= 1_000_000 and cyc[100_000] >= 100_000, cyc
+    assert cyc[1_000_000] > 5 * cyc[100_000] > 5 * cyc[0], cyc
