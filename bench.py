@@ -396,6 +396,21 @@ def measure_config0(session, rounds, n=65536):
 _LOCAL_CORES: list = []
 
 
+def measure_lazy(cfg, masks, rounds):
+    from paper_2310_01212_b200 import native
+    from paper_2310_01212_b200.device import WorkDescriptor
+    ls, _ = native.NativeSession.start(dataclasses.replace(cfg, lazy_ack=True))
+    ls.register(WorkDescriptor(slot=0, kind="empty"))
+    ls.bench_roundtrip(masks, 0, 5000)
+    _, done, cyc = ls.bench_roundtrip(masks, 0, rounds)
+    ls.dispose()
+    ls.close()
+    return {"tasks_per_s": round(rounds / (cyc.sum() / 1e9), 1), "trigger_to_done": lat_summary(done),
+            "round_trip": lat_summary(cyc),
+            "note": "NativeConfig(lazy_ack=True): the NOP ack's consumption is awaited by the worker's "
+                    "next trigger instead of inside wait(); protocol and traces unchanged"}
+
+
 def measure_table2(device, reps=100, iterations=20_000):
     """The paper's Table II scenarios (P/bench.py:358-373: table2-single-sm,
     table2-full-gpu; busy_loop work of 20,000 iterations, 100 reps) on B200
@@ -637,6 +652,11 @@ def run_lk_arm(args, world, rank, local):
     if rank == 0:
         extras["small_transfer"] = measure_small_transfer(device, 2000)
 
+    # lazy ack (opt-in): wait() returns once the ack is written; the round
+    # robin's next worker is another one, so the ack's consumption overlaps
+    if rank == 0 and not args.no_lazy:
+        extras["lazy_ack"] = measure_lazy(cfg, rr_masks, args.lazy_rounds)
+
     # several host threads, each a closed loop over its own worker group (one
     # session; disjoint workers): aggregate tasks/s a B200 sustains
     if rank == 0 and args.drivers > 1:
@@ -805,6 +825,8 @@ def main():
     ap.add_argument("--no-interference", action="store_true")
     ap.add_argument("--config0-rounds", type=int, default=20_000)
     ap.add_argument("--no-table2", action="store_true")
+    ap.add_argument("--no-lazy", action="store_true")
+    ap.add_argument("--lazy-rounds", type=int, default=200_000)
     ap.add_argument("--drivers", type=int, default=4, help="host threads for the multi-driver throughput extra")
     ap.add_argument("--driver-rounds", type=int, default=100_000)
     ap.add_argument("--lat-workers", type=int, default=16, help="latency partition size (configs[3])")

@@ -133,6 +133,8 @@ typedef struct lk_config {
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
 #define LK_CF_LSU_PAYLOAD    4u  /* payload items with 128-bit LSU loads instead of the TMA bulk ring */
 #define LK_CF_TIMELINE       8u  /* GATEWAY: stamp forward times into the device timeline (+1 L2 load per value) */
+#define LK_CF_LAZY_ACK      16u  /* lk_wait returns once the NOP ack is written; the next trigger or
+                                    dispose touching that worker waits for its republished NOP */
 
 /* One linearized protocol write; replaces TraceRecord (protocol.py:253-261). */
 typedef struct lk_trace_rec {
@@ -184,7 +186,8 @@ int lk_trigger(lk_session* s, const uint64_t* mask, uint32_t nwords,
 
 /* NativeSession.wait (native.py:250-275): spin until every masked worker
  * published FINISHED (*finished_ns = call start -> that observation), write
- * NOP acks ascending, spin until every masked worker republished NOP. */
+ * NOP acks ascending, spin until every masked worker republished NOP (with
+ * LK_CF_LAZY_ACK that last spin moves to the next trigger of the worker). */
 int lk_wait(lk_session* s, const uint64_t* mask, uint32_t nwords,
             uint64_t* finished_ns);
 

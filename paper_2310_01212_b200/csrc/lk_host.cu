@@ -155,6 +155,9 @@ struct lk_session {
   std::vector<uint8_t> slot_busy;
   std::vector<uint32_t> inflight;
   std::vector<uint64_t> scratch;                          // nwords, under mu
+  // LK_CF_LAZY_ACK: workers whose NOP ack was written but whose republished
+  // NOP has not been seen yet; the next trigger/dispose touching them waits
+  std::vector<uint64_t> ack_pending;                      // nwords, under mu
   std::vector<uint8_t> registered;                        // per slot
   std::vector<lk_desc> reg_desc;                          // host copy per slot
   std::vector<std::vector<uint64_t>> reg_mask;            // per slot (nwords)
@@ -425,6 +428,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->slot_busy.assign(cfg.num_slots, 0);
   s->inflight.reserve(64);
   s->scratch.assign(s->nwords, 0);
+  s->ack_pending.assign(s->nwords, 0);
   s->reg_desc.resize(cfg.num_slots);
   s->reg_mask.resize(cfg.num_slots);
   s->host_seq.assign(s->nw, 0);
@@ -619,6 +623,21 @@ static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* d, const ui
 // Checks in the reference's order (native.py:210-220): live, mask, busy
 // workers, slot lock, idle cells; then stage the descriptor (when given) and
 // write the WORK word to every masked worker, ascending.
+// LK_CF_LAZY_ACK: before a worker is written again, its ack must have been
+// consumed (the reference's wait spins for it, native.py:263-265; lazily it is
+// spun for here instead).  Caller holds s->mu.
+static int settle_acks(lk_session* s, const std::vector<uint32_t>& ids) {
+  static thread_local std::vector<uint32_t> due;
+  due.clear();
+  for (uint32_t i : ids)
+    if (s->ack_pending[i >> 6] >> (i & 63) & 1) due.push_back(i);
+  if (due.empty()) return LK_OK;
+  int rc = spin_words(s, due, LK_NOP, "wait for ack consumption");
+  if (rc) return rc;
+  for (uint32_t i : due) s->ack_pending[i >> 6] &= ~(1ull << (i & 63));
+  return LK_OK;
+}
+
 static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, uint32_t slot,
                           const lk_desc* d, std::vector<uint32_t>& ids, uint64_t* elapsed_ns,
                           uint64_t t_call) {
@@ -633,6 +652,8 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
     return fail(LK_E_USAGE, "descriptor slot %u still referenced by an un-waited dispatch", slot);
   if (slot >= s->cfg.num_slots)
     return fail(LK_E_USAGE, "slot %u outside the %u-entry descriptor table", slot, s->cfg.num_slots);
+  rc = settle_acks(s, ids);
+  if (rc) return rc;
   for (uint32_t i : ids) {
     const uint32_t w = s->word(i);
     if (w != LK_NOP) return fail(LK_E_BUSY, "worker %u not idle (from_gpu=%u)", i, w);
@@ -688,14 +709,19 @@ static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::
   const uint64_t finished_at = now_ns();
   for (uint32_t i : ids) s->host_times[3 * i + 2] = finished_at;
   if (!s->post(ids, LK_NOP)) return fail(LK_E_HANG, "event ring full: gateway not consuming");
-  rc = spin_words(s, ids, LK_NOP, "wait for ack consumption");
-  if (rc) return rc;
+  const bool lazy = (s->cfg.flags & LK_CF_LAZY_ACK) != 0;
+  if (!lazy) {
+    rc = spin_words(s, ids, LK_NOP, "wait for ack consumption");
+    if (rc) return rc;
+  }
   {
     std::lock_guard<std::mutex> g(s->mu);
     std::vector<uint64_t>& m = s->scratch;
     std::fill(m.begin(), m.end(), 0);
     for (uint32_t i : ids) m[i >> 6] |= 1ull << (i & 63);
     for (uint32_t k = 0; k < s->nwords; ++k) s->pending[k] &= ~m[k];
+    if (lazy)
+      for (uint32_t k = 0; k < s->nwords; ++k) s->ack_pending[k] |= m[k];
     // a slot is freed only once every worker it was triggered on was waited (native.py:266-272)
     for (size_t j = 0; j < s->inflight.size();) {
       const uint32_t slot = s->inflight[j];
@@ -763,6 +789,8 @@ extern "C" int lk_dispose(lk_session* s, uint64_t* elapsed_ns) {
     if (s->pending[i >> 6] >> (i & 63) & 1) busy.push_back(i);
   if (!busy.empty()) return fail(LK_E_DISPOSE_BUSY, "worker(s) %s still working", ids_str(busy).c_str());
   const uint64_t t0 = now_ns();
+  rc = settle_acks(s, s->all_ids);
+  if (rc) return rc;
   if (!s->post(s->all_ids, LK_EXIT)) return fail(LK_E_HANG, "event ring full: gateway not consuming");
   const uint64_t deadline = t0 + s->cfg.wait_timeout_ns;
   for (;;) {

@@ -70,6 +70,8 @@ class NativeConfig:
     tma_payload: bool = True        # payload tiles via the TMA bulk ring (False: 128-bit LSU loads)
     ring_stages: int = 6            # TMA ring depth, 16-KiB stages (2..12)
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
+    lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
+                                    # awaited by the next trigger/dispose of that worker
 
     def __post_init__(self) -> None:
         if self.num_workers is not None and self.num_workers < 1:
@@ -104,7 +106,8 @@ class NativeConfig:
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)
-                   | (_lib.CF_TIMELINE if self.timeline else 0))
+                   | (_lib.CF_TIMELINE if self.timeline else 0)
+                   | (_lib.CF_LAZY_ACK if self.lazy_ack else 0))
         return c
 
 

@@ -491,3 +491,31 @@ def test_busy_loop_really_counts():
     session.dispose()
     assert cyc[1_000_000] >= 1_000_000 and cyc[100_000] >= 100_000, cyc
     assert cyc[1_000_000] > 5 * cyc[100_000] > 5 * cyc[0], cyc
+
+
+@pytest.mark.parametrize("mode", ["direct", "hybrid"])
+def test_lazy_ack_keeps_the_protocol(mode):
+    """lazy_ack: wait() returns once the ack is written; the next trigger of
+    that worker waits for the republished NOP.  Every trace still validates
+    and projects to D0 D4 (H[16+slot] D2 D1 H4 D4)* H8."""
+    rng = random.Random(5)
+    session = start(6, trace_capacity=4096, poll_mode=mode, lazy_ack=True)
+    program = []
+    for k in range(120):
+        m = host.mask_of(rng.sample(range(6), rng.randint(1, 6)))
+        session.trigger(m, WorkDescriptor(slot=k % 4, iterations=rng.randrange(50)))
+        program.append((m, k % 4))
+        session.wait(m)
+    session.dispose()
+    assert_trace_ok(session, program, 6)
+
+
+def test_lazy_ack_c_loop_roundtrips():
+    session = start(None, trace_capacity=2048, lazy_ack=True)
+    n = session.num_workers
+    session.register(WorkDescriptor(slot=0, kind="empty"))
+    masks = [1 << i for i in range(n)]
+    _, done, cyc = session.bench_roundtrip(masks, 0, 4 * n)
+    assert (cyc >= done).all()
+    session.dispose()
+    assert_trace_ok(session, [(masks[k % n], 0) for k in range(4 * n)], n)
