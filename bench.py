@@ -652,11 +652,6 @@ def run_lk_arm(args, world, rank, local):
     if rank == 0:
         extras["small_transfer"] = measure_small_transfer(device, 2000)
 
-    # lazy ack (opt-in): wait() returns once the ack is written; the round
-    # robin's next worker is another one, so the ack's consumption overlaps
-    if rank == 0 and not args.no_lazy:
-        extras["lazy_ack"] = measure_lazy(cfg, rr_masks, args.lazy_rounds)
-
     # several host threads, each a closed loop over its own worker group (one
     # session; disjoint workers): aggregate tasks/s a B200 sustains
     if rank == 0 and args.drivers > 1:
@@ -683,6 +678,13 @@ def run_lk_arm(args, world, rank, local):
     smids = session.smid_map
     session.dispose()
     session.close()
+
+    # lazy ack (opt-in): wait() returns once the ack is written; the round
+    # robin's next worker is another one, so the ack's consumption overlaps.
+    # (Each extra session starts after the previous one is disposed: a live
+    # session owns every SM.)
+    if rank == 0 and not args.no_lazy:
+        extras["lazy_ack"] = measure_lazy(cfg, rr_masks, args.lazy_rounds)
 
     # configs[2]: payload items dispatched to every worker.  Multi-worker
     # dispatch runs on a GATEWAY-mode session (one ring event reaches all 148
