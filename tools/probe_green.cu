@@ -8,6 +8,7 @@
 #include <string.h>
 #include <time.h>
 #include <unistd.h>
+#include <stdlib.h>
 
 #define CK(x) do { CUresult r_ = (x); if (r_ != CUDA_SUCCESS) { const char* m; cuGetErrorString(r_, &m); \
   printf("%s -> %d %s (line %d)\n", #x, int(r_), m, __LINE__); return 1; } } while (0)
@@ -57,11 +58,15 @@ int main() {
   RK(cudaFuncSetAttribute(spinner, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
   unsigned nA = part[0].sm.smCount;
   void* args[] = {&stop, &smA};
-  cudaError_t le = cudaLaunchCooperativeKernel((void*)spinner, dim3(nA), dim3(512), args, 120 * 1024, sA);
-  printf("cooperative launch of %u blocks in partition A: %s\n", nA, cudaGetErrorString(le));
+  const bool coop = getenv("NOCOOP") == nullptr;
+  cudaError_t le = coop ? cudaLaunchCooperativeKernel((void*)spinner, dim3(nA), dim3(512), args, 120 * 1024, sA)
+                        : cudaLaunchKernel((void*)spinner, dim3(nA), dim3(512), args, 120 * 1024, sA);
+  printf("%s launch of %u blocks in partition A: %s\n", coop ? "cooperative" : "plain", nA, cudaGetErrorString(le));
   usleep(100000);
   // B: ordinary kernel in partition B while A spins
-  CK(cuCtxSetCurrent(cB));
+  const bool inPrimary = getenv("BPRIMARY") != nullptr;
+  CK(cuCtxSetCurrent(inPrimary ? primary : cB));
+  printf("B runs in the %s context\n", inPrimary ? "primary" : "green B");
   cudaStream_t sB; RK(cudaStreamCreateWithFlags(&sB, cudaStreamNonBlocking));
   cudaEvent_t e0, e1; RK(cudaEventCreate(&e0)); RK(cudaEventCreate(&e1));
   RK(cudaEventRecord(e0, sB));
@@ -74,7 +79,7 @@ int main() {
   float ms = 0; if (done) { cudaEventElapsedTime(&ms, e0, e1); printf("B: 10 x 64 MiB read+write in %.3f ms -> %.0f GB/s\n", ms, 10 * 2 * 64.0 * 1048576 / (ms * 1e6)); }
   *(volatile uint32_t*)stop = 1;
   CK(cuCtxSetCurrent(cA)); RK(cudaStreamSynchronize(sA));
-  CK(cuCtxSetCurrent(cB)); RK(cudaStreamSynchronize(sB));
+  CK(cuCtxSetCurrent(inPrimary ? primary : cB)); RK(cudaStreamSynchronize(sB));
   // SM sets
   unsigned overlap = 0; bool inA[256] = {false};
   for (unsigned i = 0; i < nA; ++i) inA[smA[i] & 255] = true;
