@@ -50,7 +50,9 @@ int main() {
   uint32_t *stop, *smA, *smB;
   RK(cudaHostAlloc(&stop, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(stop, 0, 4096);
-  RK(cudaMallocManaged(&smA, 4096 * 4)); RK(cudaMallocManaged(&smB, 4096 * 4));
+  // plain device memory: managed memory would make the driver serialise B behind A
+  RK(cudaMalloc(&smA, 4096 * 4)); RK(cudaMalloc(&smB, 4096 * 4));
+  static uint32_t hA[4096], hB[4096];
   float* x; RK(cudaMalloc(&x, size_t(64) << 20));
   // A: spinner in partition A, one block per partition SM, cooperative
   CK(cuCtxSetCurrent(cA));
@@ -81,6 +83,9 @@ int main() {
   CK(cuCtxSetCurrent(cA)); RK(cudaStreamSynchronize(sA));
   CK(cuCtxSetCurrent(inPrimary ? primary : cB)); RK(cudaStreamSynchronize(sB));
   // SM sets
+  CK(cuCtxSetCurrent(primary));
+  RK(cudaMemcpy(hA, smA, sizeof hA, cudaMemcpyDeviceToHost)); RK(cudaMemcpy(hB, smB, sizeof hB, cudaMemcpyDeviceToHost));
+  smA = hA; smB = hB;
   unsigned overlap = 0; bool inA[256] = {false};
   for (unsigned i = 0; i < nA; ++i) inA[smA[i] & 255] = true;
   for (int i = 0; i < 1024; ++i) if (inA[smB[i] & 255]) ++overlap;
