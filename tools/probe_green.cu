@@ -54,6 +54,14 @@ int main() {
   RK(cudaMalloc(&smA, 4096 * 4)); RK(cudaMalloc(&smB, 4096 * 4));
   static uint32_t hA[4096], hB[4096];
   float* x; RK(cudaMalloc(&x, size_t(64) << 20));
+  // load every kernel in every context first: a lazy module load while the
+  // spinner is resident would wait for it (the same trap as liblk's preload)
+  cudaFuncAttributes fa;
+  for (CUcontext c : {primary, cA, cB}) {
+    CK(cuCtxSetCurrent(c));
+    RK(cudaFuncGetAttributes(&fa, spinner));
+    RK(cudaFuncGetAttributes(&fa, worker));
+  }
   // A: spinner in partition A, one block per partition SM, cooperative
   CK(cuCtxSetCurrent(cA));
   cudaStream_t sA; RK(cudaStreamCreateWithFlags(&sA, cudaStreamNonBlocking));
