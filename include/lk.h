@@ -113,6 +113,11 @@ typedef struct lk_config {
   uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default), LK_POLL_GATEWAY or LK_POLL_HYBRID */
   uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 128 */
   uint32_t ring_stages;          /* TMA payload ring depth in 16-KiB stages, 2..12; 0 = 6 */
+  uint32_t sm_partition;         /* 0: the persistent kernel spans the GPU.  N: it runs in a green
+                                    context of >= N SMs (driver granularity: multiples of 8), one
+                                    worker per partition SM; the remaining SMs form a second green
+                                    context for ordinary kernels (lk_baseline_create_in) */
+  uint32_t reserved;
 } lk_config;
 
 /* How to_gpu words reach the workers.  DIRECT: every worker polls its own
@@ -280,6 +285,12 @@ int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_t grid,
  * path, which also fits beside a resident LK session. */
 int lk_baseline_set_tma(lk_baseline* b, int on);
 int lk_baseline_destroy(lk_baseline* b);
+/* The baseline's launches go to the SMs a partitioned session left free
+ * (lk_config.sm_partition), so they run beside the resident LK kernel.
+ * Replaces nothing in the reference: its workers are host threads. */
+int lk_baseline_create_in(lk_session* s, uint32_t threads, lk_baseline** out);
+/* SMs of the session's partition and of the rest (0, 0 when unpartitioned). */
+int lk_partition_info(lk_session* s, uint32_t* lk_sms, uint32_t* rest_sms);
 
 /* ---- host helpers ----------------------------------------------------------- */
 /* Pin the calling thread to the CPU cores local to the GPU's NUMA node

@@ -92,6 +92,8 @@ class lk_config(C.Structure):
         ("poll_mode", C.c_uint32),
         ("status_stride", C.c_uint32),
         ("ring_stages", C.c_uint32),
+        ("sm_partition", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -152,6 +154,8 @@ SIGNATURES = {
     "lk_baseline_time_kernel": (I32, [P, C.POINTER(lk_desc), U32, U32, C.POINTER(C.c_float)]),
     "lk_baseline_destroy": (I32, [P]),
     "lk_baseline_set_tma": (I32, [P, I32]),
+    "lk_baseline_create_in": (I32, [P, U32, C.POINTER(P)]),
+    "lk_partition_info": (I32, [P, PU32, PU32]),
     "lk_pin_thread_near": (I32, [I32, PU32]),
     "lk_device_count": (I32, [C.POINTER(C.c_int)]),
     "lk_sm_count": (I32, [I32, C.POINTER(C.c_int)]),

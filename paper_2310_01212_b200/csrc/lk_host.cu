@@ -9,6 +9,7 @@
 // mask / busy / slot lock / idle (208-231), writes 16+slot ascending; wait spins
 // to FINISHED, acks with NOP ascending and spins to NOP (250-275); dispose
 // refuses while pending, writes EXIT, joins (277-295).
+#include <cuda.h>            // driver types only: entry points come from cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 #include <errno.h>
 #include <pthread.h>
@@ -62,6 +63,103 @@ static inline uint64_t now_ns() {
   return uint64_t(ts.tv_sec) * 1000000000ull + uint64_t(ts.tv_nsec);
 }
 
+// ------------------------------------------------------------------ driver entry points
+// Green contexts (SM partitions) are driver-API only.  liblk.so does not link
+// libcuda: the functions are fetched through the runtime, so the library still
+// loads (and its CPU tests run) on machines without a driver.
+struct Drv {
+  decltype(&cuDeviceGet) DeviceGet = nullptr;
+  decltype(&cuDeviceGetDevResource) DeviceGetDevResource = nullptr;
+  decltype(&cuDevSmResourceSplitByCount) DevSmResourceSplitByCount = nullptr;
+  decltype(&cuDevResourceGenerateDesc) DevResourceGenerateDesc = nullptr;
+  decltype(&cuGreenCtxCreate) GreenCtxCreate = nullptr;
+  decltype(&cuGreenCtxDestroy) GreenCtxDestroy = nullptr;
+  decltype(&cuCtxFromGreenCtx) CtxFromGreenCtx = nullptr;
+  decltype(&cuCtxPushCurrent) CtxPushCurrent = nullptr;
+  decltype(&cuCtxPopCurrent) CtxPopCurrent = nullptr;
+  bool ok = false;
+};
+
+static Drv* drv() {
+  static Drv d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    bool ok = true;
+    auto get = [&](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess || !*fn)
+        ok = false;
+    };
+    get("cuDeviceGet", reinterpret_cast<void**>(&d.DeviceGet));
+    get("cuDeviceGetDevResource", reinterpret_cast<void**>(&d.DeviceGetDevResource));
+    get("cuDevSmResourceSplitByCount", reinterpret_cast<void**>(&d.DevSmResourceSplitByCount));
+    get("cuDevResourceGenerateDesc", reinterpret_cast<void**>(&d.DevResourceGenerateDesc));
+    get("cuGreenCtxCreate", reinterpret_cast<void**>(&d.GreenCtxCreate));
+    get("cuGreenCtxDestroy", reinterpret_cast<void**>(&d.GreenCtxDestroy));
+    get("cuCtxFromGreenCtx", reinterpret_cast<void**>(&d.CtxFromGreenCtx));
+    get("cuCtxPushCurrent", reinterpret_cast<void**>(&d.CtxPushCurrent));
+    get("cuCtxPopCurrent", reinterpret_cast<void**>(&d.CtxPopCurrent));
+    d.ok = ok;
+  });
+  return &d;
+}
+
+// Makes a (green) context current for a scope; no-op for nullptr.
+struct CtxScope {
+  CUcontext c;
+  explicit CtxScope(CUcontext ctx) : c(ctx) {
+    if (c) drv()->CtxPushCurrent(c);
+  }
+  ~CtxScope() {
+    if (c) {
+      CUcontext prev;
+      drv()->CtxPopCurrent(&prev);
+    }
+  }
+};
+
+// An SM partition: green context A (>= `sms` SMs, rounded up by the driver to
+// its granularity, 8 on sm_90+) for the persistent kernel, and green context B
+// holding every remaining SM for ordinary kernels that run beside it.
+struct Partition {
+  CUgreenCtx ga = nullptr, gb = nullptr;
+  CUcontext ca = nullptr, cb = nullptr;
+  uint32_t a_sms = 0, b_sms = 0;
+};
+
+static int make_partition(int device, uint32_t sms, Partition* p) {
+  Drv* d = drv();
+  if (!d->ok) return fail(LK_E_INIT, "green-context driver entry points unavailable");
+  CUdevice dev;
+  CUresult r = d->DeviceGet(&dev, device);
+  CUdevResource all, part, rest;
+  unsigned groups = 1;
+  if (r == CUDA_SUCCESS) r = d->DeviceGetDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM);
+  if (r == CUDA_SUCCESS) r = d->DevSmResourceSplitByCount(&part, &groups, &all, &rest, 0, sms);
+  if (r != CUDA_SUCCESS || groups != 1)
+    return fail(LK_E_CONFIG, "cannot split %u SMs off device %d (driver error %d)", sms, device, int(r));
+  CUdevResourceDesc da, db;
+  r = d->DevResourceGenerateDesc(&da, &part, 1);
+  if (r == CUDA_SUCCESS) r = d->GreenCtxCreate(&p->ga, da, dev, CU_GREEN_CTX_DEFAULT_STREAM);
+  if (r == CUDA_SUCCESS) r = d->CtxFromGreenCtx(&p->ca, p->ga);
+  if (r == CUDA_SUCCESS && rest.sm.smCount) {
+    r = d->DevResourceGenerateDesc(&db, &rest, 1);
+    if (r == CUDA_SUCCESS) r = d->GreenCtxCreate(&p->gb, db, dev, CU_GREEN_CTX_DEFAULT_STREAM);
+    if (r == CUDA_SUCCESS) r = d->CtxFromGreenCtx(&p->cb, p->gb);
+  }
+  if (r != CUDA_SUCCESS) return fail(LK_E_INIT, "green context creation failed (driver error %d)", int(r));
+  p->a_sms = part.sm.smCount;
+  p->b_sms = rest.sm.smCount;
+  return LK_OK;
+}
+
+static void free_partition(Partition* p) {
+  if (p->ga) drv()->GreenCtxDestroy(p->ga);
+  if (p->gb) drv()->GreenCtxDestroy(p->gb);
+  *p = Partition{};
+}
+
 // ------------------------------------------------------------------ service stream
 // Allocation, frees and staging copies never touch the legacy stream and never
 // synchronize the device: a resident persistent kernel never "completes", so a
@@ -112,7 +210,8 @@ struct lk_session {
   uint32_t nw = 0, nwords = 0, threads = 0;
   int device = 0;
   size_t smem = 0;
-  cudaStream_t stream = nullptr;   // persistent kernel
+  cudaStream_t stream = nullptr;   // persistent kernel (in part.ca when partitioned)
+  Partition part;                  // sm_partition > 0: green contexts A (LK) and B (the rest)
   cudaStream_t copy_stream = nullptr;
 
   // pinned mapped host block
@@ -283,6 +382,7 @@ static int require_live(lk_session* s) {
 
 static int kernel_status(lk_session* s) {
   if (s->kernel_done) return 1;
+  CtxScope cs(s->part.ca);
   cudaError_t q = cudaStreamQuery(s->stream);
   if (q == cudaErrorNotReady) return 0;
   s->kernel_done = true;
@@ -397,13 +497,24 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   LK_CUDA(cudaGetDeviceProperties(&prop, cfg.device));
   if (!prop.cooperativeLaunch) return fail(LK_E_INIT, "device lacks cooperative launch");
   if (!prop.canMapHostMemory) return fail(LK_E_INIT, "device cannot map host memory");
-  const uint32_t nsm = uint32_t(prop.multiProcessorCount);
+  svc_stream();   // created in the primary context, before any green context is pushed
+  Partition part;
+  uint32_t nsm = uint32_t(prop.multiProcessorCount);
+  if (cfg.sm_partition) {
+    if (cfg.sm_partition >= nsm) return fail(LK_E_CONFIG, "sm_partition %u must be below the %u SMs", cfg.sm_partition, nsm);
+    int prc = make_partition(cfg.device, cfg.sm_partition, &part);
+    if (prc) return prc;
+    nsm = part.a_sms;
+  }
   if (cfg.num_workers == 0) cfg.num_workers = nsm;
-  if (cfg.num_workers > nsm)
+  if (cfg.num_workers > nsm) {
+    free_partition(&part);
     return fail(LK_E_CONFIG, "num_workers %u exceeds the %u SMs (one worker per SM)", cfg.num_workers, nsm);
+  }
   if (cfg.num_workers > 256) return fail(LK_E_CONFIG, "at most 256 workers (4 mask words)");
 
   auto* s = new lk_session();
+  s->part = part;
   s->cfg = cfg;
   s->nw = cfg.num_workers;
   s->nwords = (s->nw + 63) / 64;
@@ -439,8 +550,12 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   auto cleanup = [&](int rc) {
     if (s->host_block) cudaFreeHost(s->host_block);
     if (s->dev_block) dev_free(s->dev_block);
-    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->stream) {
+      CtxScope cs(s->part.ca);
+      cudaStreamDestroy(s->stream);
+    }
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    free_partition(&s->part);
     delete s;
     return rc;
   };
@@ -502,8 +617,6 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->d_trace = traceb ? reinterpret_cast<lk_dev_trace*>(p) : nullptr; p += traceb;
   s->d_tcnt = reinterpret_cast<uint32_t*>(p);
 
-  ce = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
-  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "stream: %s", cudaGetErrorString(ce)));
   ce = cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "stream: %s", cudaGetErrorString(ce)));
 
@@ -513,16 +626,22 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (s->smem > size_t(prop.sharedMemPerBlockOptin) - 1024)
     return cleanup(fail(LK_E_INIT, "payload ring needs %zu B of shared memory, the device offers %zu",
                         s->smem, size_t(prop.sharedMemPerBlockOptin) - 1024));
-  ce = lk_preload_kernels();
-  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "kernel load: %s", cudaGetErrorString(ce)));
-  ce = lk_persistent_configure(s->smem);
-  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "smem attr: %s", cudaGetErrorString(ce)));
+  // Kernel load, attributes, occupancy, the kernel's stream and the launch
+  // happen in the partition's green context when there is one: its streams
+  // run on its SMs only.  (Memory is shared with the primary context.)
   int bps = 0;
   // + three warps: host-cell poller and mailbox poller (HYBRID), gateway (CTA 0);
   // unused ones retire at once
   const uint32_t launch_threads = s->threads + 96;
-  ce = lk_persistent_occupancy(launch_threads, s->smem, &bps);
-  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "occupancy: %s", cudaGetErrorString(ce)));
+  const char* what = "stream";
+  {
+    CtxScope cs(s->part.ca);
+    ce = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) { what = "kernel load"; ce = lk_preload_kernels(); }
+    if (ce == cudaSuccess) { what = "smem attr"; ce = lk_persistent_configure(s->smem); }
+    if (ce == cudaSuccess) { what = "occupancy"; ce = lk_persistent_occupancy(launch_threads, s->smem, &bps); }
+  }
+  if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "%s: %s", what, cudaGetErrorString(ce)));
   if (bps != 1) return cleanup(fail(LK_E_INIT, "expected exactly 1 resident worker per SM, got %d", bps));
 
   lk_dev_args a;
@@ -559,7 +678,10 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.poll_mode = cfg.poll_mode;
   a.use_tma = use_tma ? 1 : 0;
   a.ring_stages = cfg.ring_stages;
-  ce = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);
+  {
+    CtxScope cs(s->part.ca);
+    ce = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);
+  }
   if (ce != cudaSuccess) return cleanup(fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(ce)));
 
   // --- boot: every worker publishes INIT then NOP (native.py:113-118)
@@ -838,9 +960,20 @@ extern "C" int lk_destroy(lk_session* s) {
   }
   cudaFreeHost(s->host_block);
   dev_free(s->dev_block);
-  cudaStreamDestroy(s->stream);
+  {
+    CtxScope cs(s->part.ca);
+    cudaStreamDestroy(s->stream);
+  }
   cudaStreamDestroy(s->copy_stream);
+  free_partition(&s->part);
   delete s;
+  return LK_OK;
+}
+
+extern "C" int lk_partition_info(lk_session* s, uint32_t* lk_sms, uint32_t* rest_sms) {
+  if (!s) return fail(LK_E_USAGE, "null session");
+  if (lk_sms) *lk_sms = s->part.ca ? s->part.a_sms : 0;
+  if (rest_sms) *rest_sms = s->part.ca ? s->part.b_sms : 0;
   return LK_OK;
 }
 
@@ -1105,6 +1238,7 @@ extern "C" int lk_pingpong(int device, uint64_t rounds, uint64_t* rt_ns) {
 
 // ------------------------------------------------------------------ baseline
 struct lk_baseline {
+  CUcontext ctx = nullptr;   // green context B of a partitioned session, else the primary
   int device;
   uint32_t threads;
   cudaStream_t stream;
@@ -1114,21 +1248,35 @@ struct lk_baseline {
   cudaEvent_t e0, e1;
 };
 
+static int baseline_create(int device, uint32_t threads, CUcontext ctx, lk_baseline** out);
+
 extern "C" int lk_baseline_create(int device, uint32_t threads, lk_baseline** out) {
+  return baseline_create(device, threads, nullptr, out);
+}
+
+extern "C" int lk_baseline_create_in(lk_session* s, uint32_t threads, lk_baseline** out) {
+  if (!s || !out) return fail(LK_E_USAGE, "null argument");
+  if (!s->part.cb) return fail(LK_E_USAGE, "session has no SM partition (lk_config.sm_partition)");
+  return baseline_create(s->device, threads, s->part.cb, out);
+}
+
+static int baseline_create(int device, uint32_t threads, CUcontext ctx, lk_baseline** out) {
   if (!out) return fail(LK_E_USAGE, "null argument");
   if (threads == 0) threads = 512;
   if (threads % 32 || threads > 1024) return fail(LK_E_CONFIG, "threads must be a multiple of 32 <= 1024");
   LK_CUDA(cudaSetDevice(device));
   auto* b = new lk_baseline();
+  b->ctx = ctx;
   b->device = device;
   b->threads = threads;
   b->in_flight = false;
   b->use_tma = 1;
-  LK_CUDA(lk_preload_kernels());
-  LK_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
-  LK_CUDA(dev_alloc(reinterpret_cast<void**>(&b->d_ctr), 4));
+  LK_CUDA(dev_alloc(reinterpret_cast<void**>(&b->d_ctr), 4));   // primary context: shared memory
   LK_CUDA(cudaMemsetAsync(b->d_ctr, 0, 4, svc_stream()));
   LK_CUDA(cudaStreamSynchronize(svc_stream()));
+  CtxScope cs(b->ctx);   // kernels, stream and events in the partition's green context
+  LK_CUDA(lk_preload_kernels());
+  LK_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
   LK_CUDA(cudaEventCreate(&b->e0));
   LK_CUDA(cudaEventCreate(&b->e1));
   *out = b;
@@ -1137,6 +1285,7 @@ extern "C" int lk_baseline_create(int device, uint32_t threads, lk_baseline** ou
 
 extern "C" int lk_baseline_launch(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t* launch_ns) {
   if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
+  CtxScope cs(b->ctx);
   if (b->in_flight) return fail(LK_E_USAGE, "previous task not yet joined");
   const uint64_t t0 = now_ns();
   cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
@@ -1149,6 +1298,7 @@ extern "C" int lk_baseline_launch(lk_baseline* b, const lk_desc* d, uint32_t gri
 
 extern "C" int lk_baseline_wait(lk_baseline* b, uint64_t* wait_ns) {
   if (!b) return fail(LK_E_USAGE, "null argument");
+  CtxScope cs(b->ctx);
   if (!b->in_flight) return fail(LK_E_USAGE, "no task in flight");
   const uint64_t t0 = now_ns();
   LK_CUDA(cudaStreamSynchronize(b->stream));
@@ -1160,6 +1310,7 @@ extern "C" int lk_baseline_wait(lk_baseline* b, uint64_t* wait_ns) {
 extern "C" int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t rounds,
                                  uint64_t* launch_ns, uint64_t* total_ns) {
   if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
+  CtxScope cs(b->ctx);
   for (uint64_t k = 0; k < rounds; ++k) {
     const uint64_t t0 = now_ns();
     cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
@@ -1176,6 +1327,7 @@ extern "C" int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid
 extern "C" int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_t grid, uint32_t reps,
                                        float* avg_ms) {
   if (!b || !d || !avg_ms || reps == 0) return fail(LK_E_USAGE, "bad argument");
+  CtxScope cs(b->ctx);
   LK_CUDA(cudaEventRecord(b->e0, b->stream));
   for (uint32_t k = 0; k < reps; ++k) {
     cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
@@ -1197,11 +1349,14 @@ extern "C" int lk_baseline_set_tma(lk_baseline* b, int on) {
 
 extern "C" int lk_baseline_destroy(lk_baseline* b) {
   if (!b) return LK_OK;
-  cudaStreamSynchronize(b->stream);
-  cudaStreamDestroy(b->stream);
+  {
+    CtxScope cs(b->ctx);
+    cudaStreamSynchronize(b->stream);
+    cudaStreamDestroy(b->stream);
+    cudaEventDestroy(b->e0);
+    cudaEventDestroy(b->e1);
+  }
   dev_free(b->d_ctr);
-  cudaEventDestroy(b->e0);
-  cudaEventDestroy(b->e1);
   delete b;
   return LK_OK;
 }

@@ -69,6 +69,8 @@ class NativeConfig:
     fence_always: bool = False
     tma_payload: bool = True        # payload tiles via the TMA bulk ring (False: 128-bit LSU loads)
     ring_stages: int = 6            # TMA ring depth, 16-KiB stages (2..12)
+    sm_partition: int = 0           # N > 0: run in a green context of >= N SMs (multiple of 8), one
+                                    # worker per partition SM; the rest stay free for other kernels
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
@@ -98,6 +100,7 @@ class NativeConfig:
         c.cell_stride = self.cell_stride
         c.status_stride = self.status_stride
         c.ring_stages = self.ring_stages
+        c.sm_partition = self.sm_partition
         c.num_slots = self.num_slots
         c.poll_replicas = self.poll_replicas
         c.poll_spacing_ns = self.poll_spacing_ns
@@ -240,6 +243,14 @@ class NativeSession:
         buf = (C.c_uint64 * self.nwords)()
         _lib.check(self._lib.lk_pending(self._h, buf, self.nwords))
         return int.from_bytes(bytes(buf), "little")
+
+    @property
+    def partition_info(self) -> tuple[int, int]:
+        """(SMs of this session's green-context partition, SMs left for other
+        kernels); (0, 0) when the session spans the GPU."""
+        a, b = C.c_uint32(), C.c_uint32()
+        _lib.check(self._lib.lk_partition_info(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     @property
     def smid_map(self) -> list[int]:
@@ -464,15 +475,23 @@ class LaunchSyncBaseline:
     """cudaLaunchKernel + cudaStreamSynchronize per task (the CUDA "spawn")."""
 
     def __init__(self, device: int = 0, threads_per_worker: int = 512, grid: Optional[int] = None,
-                 tma_payload: bool = True):
+                 tma_payload: bool = True, beside: Optional["NativeSession"] = None):
+        """``beside``: a session started with ``sm_partition``; the baseline's
+        kernels then run on the SMs that session left free, concurrently with it."""
         self._lib = _lib.load()
         self._h = C.c_void_p()
-        _lib.check(self._lib.lk_baseline_create(device, threads_per_worker, C.byref(self._h)))
+        if beside is not None:
+            _lib.check(self._lib.lk_baseline_create_in(beside._h, threads_per_worker, C.byref(self._h)))
+        else:
+            _lib.check(self._lib.lk_baseline_create(device, threads_per_worker, C.byref(self._h)))
         _lib.check(self._lib.lk_baseline_set_tma(self._h, 1 if tma_payload else 0))
         if grid is None:
-            n = C.c_int()
-            _lib.check(self._lib.lk_sm_count(device, C.byref(n)))
-            grid = n.value
+            if beside is not None:
+                grid = beside.partition_info[1]
+            else:
+                n = C.c_int()
+                _lib.check(self._lib.lk_sm_count(device, C.byref(n)))
+                grid = n.value
         self.grid = grid
         self.timings: list[PhaseTiming] = []
         self._u64 = C.c_uint64()

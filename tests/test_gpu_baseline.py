@@ -57,3 +57,36 @@ def test_baseline_time_kernel_reports_positive():
     ms = b.time_kernel(WorkDescriptor(slot=0, kind="saxpy_f32", data_in_ref=(x, y), data_out_ref=y), 3)
     assert 0 < ms < 100
     b.close()
+
+
+def test_baseline_runs_beside_a_partitioned_session():
+    """An sm_partition session leaves the other SMs to ordinary kernels: the
+    baseline launches (and synchronizes) while the persistent kernel is
+    resident, both produce the oracle's results, and the session keeps
+    answering in between."""
+    session, _ = native.NativeSession.start(native.NativeConfig(sm_partition=16, record_trace=True))
+    try:
+        b = native.LaunchSyncBaseline(beside=session)
+        assert b.grid == session.partition_info[1]
+        n = 1 << 20
+        a, c = _i32(n, 0), _i32(n, 1)
+        da, dc, do = DeviceBuffer.from_array(a), DeviceBuffer.from_array(c), DeviceBuffer(4 * n)
+        for k in range(5):
+            b.launch(WorkDescriptor(slot=0, kind="vector_add_i32", data_in_ref=(da, dc), data_out_ref=do))
+            session.trigger(1 << (k % session.num_workers), WorkDescriptor(slot=0, kind="empty"))
+            session.wait(1 << (k % session.num_workers))
+            b.wait()
+        np.testing.assert_array_equal(do.download(np.int32, n), W.vector_add_i32(a, c))
+        x, y = _f32(n, 2), _f32(n, 3)
+        dx, dy = DeviceBuffer.from_array(x), DeviceBuffer.from_array(y)
+        ms = b.time_kernel(WorkDescriptor(slot=0, kind="saxpy_f32", data_in_ref=(dx, dy), data_out_ref=dy,
+                                          alpha=1.5), 1)
+        assert ms > 0
+        np.testing.assert_array_equal(dy.download(np.float32, n).view(np.uint32),
+                                      W.saxpy_f32(1.5, x, y).view(np.uint32))
+        b.close()
+        session.dispose()
+        from oracle import protocol as O
+        assert O.replay([(r.side, r.sm_id, r.word) for r in session.recorded_trace()]).violation is None
+    finally:
+        session.close()

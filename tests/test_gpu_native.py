@@ -519,3 +519,21 @@ def test_lazy_ack_c_loop_roundtrips():
     assert (cyc >= done).all()
     session.dispose()
     assert_trace_ok(session, [(masks[k % n], 0) for k in range(4 * n)], n)
+
+
+def test_sm_partition_session():
+    """sm_partition: the persistent kernel runs in a green context of 16 SMs,
+    one worker per partition SM, and keeps the full protocol."""
+    session = start(None, trace_capacity=2048, sm_partition=16)
+    lk_sms, rest = session.partition_info
+    assert session.num_workers == lk_sms >= 16 and rest > 0
+    assert len(set(session.smid_map)) == session.num_workers
+    rng = random.Random(3)
+    program = []
+    for k in range(60):
+        m = host.mask_of(rng.sample(range(session.num_workers), rng.randint(1, 4)))
+        session.trigger(m, WorkDescriptor(slot=k % 8, iterations=rng.randrange(100)))
+        program.append((m, k % 8))
+        session.wait(m)
+    session.dispose()
+    assert_trace_ok(session, program, session.num_workers)

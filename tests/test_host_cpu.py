@@ -42,7 +42,7 @@ def test_abi_version_and_strerror_without_gpu():
 
 def test_struct_sizes_match_header():
     assert C.sizeof(_lib.lk_desc) == 64
-    assert C.sizeof(_lib.lk_config) == 72
+    assert C.sizeof(_lib.lk_config) == 80
     assert C.sizeof(_lib.lk_trace_rec) == 32
     fields = [f for f, _ in _lib.lk_config._fields_]
     body = re.sub(r"/\*.*?\*/", "", HEADER, flags=re.S)
