@@ -396,6 +396,58 @@ def measure_config0(session, rounds, n=65536):
 _LOCAL_CORES: list = []
 
 
+def measure_interference_green(cfg, lat_sms, rounds, stream_mib):
+    """configs[3] with a hardware partition: the LK session runs in a green
+    context of lat_sms SMs (16); an ordinary hbm_stream kernel (the baseline's
+    work kernel, same TMA copy code) runs back to back on the remaining SMs'
+    green context from a second host thread on its own core."""
+    from paper_2310_01212_b200 import native
+    from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+    gs, _ = native.NativeSession.start(dataclasses.replace(cfg, sm_partition=lat_sms, num_workers=None))
+    masks = [1 << i for i in range(gs.num_workers)]
+    gs.register(WorkDescriptor(slot=0, kind="empty"))
+    gs.bench_roundtrip(masks, 0, 5000)
+    _, solo, _ = gs.bench_roundtrip(masks, 0, rounds)
+    b = native.LaunchSyncBaseline(beside=gs)
+    elems = (stream_mib << 20) // 4
+    src, dst = DeviceBuffer(4 * elems), DeviceBuffer(4 * elems)
+    sw = WorkDescriptor(slot=0, kind="hbm_stream", data_in_ref=src, data_out_ref=dst, iterations=1)
+    b.time_kernel(sw, 1)
+    stop = threading.Event()
+    gbs = []
+    mine = sorted(os.sched_getaffinity(0))
+    others = [c for c in sorted(_LOCAL_CORES or mine) if c not in mine] or mine
+
+    def streamer():
+        try:
+            os.sched_setaffinity(0, {others[-1]})
+        except OSError:
+            pass
+        while not stop.is_set():
+            ms = b.time_kernel(sw, 4)
+            gbs.append(8 * elems * 4 / (ms * 1e6))
+
+    th = threading.Thread(target=streamer, daemon=True)
+    th.start()
+    while len(gbs) < 2:
+        time.sleep(0.001)
+    _, co, _ = gs.bench_roundtrip(masks, 0, rounds)
+    stop.set()
+    th.join()
+    b.close()
+    src.free()
+    dst.free()
+    lk_sms, rest = gs.partition_info
+    gs.dispose()
+    gs.close()
+    return {"latency_partition_sms": lk_sms, "stream_partition_sms": rest,
+            "solo": lat_summary(solo), "co_running": lat_summary(co),
+            "jitter_delta_us": round((pct(co, 99.9) - pct(co, 50)) / 1e3 - (pct(solo, 99.9) - pct(solo, 50)) / 1e3, 3),
+            "stream_gbs_cuda_events": round(statistics.median(gbs), 1), "stream_batches": len(gbs),
+            "note": "green-context SM partitions (cuGreenCtxCreate); the stream partition runs ordinary "
+                    "kernel launches (cudaLaunchKernel + events), not LK workers"}
+
+
 def measure_lazy(cfg, masks, rounds):
     from paper_2310_01212_b200 import native
     from paper_2310_01212_b200.device import WorkDescriptor
@@ -679,6 +731,13 @@ def run_lk_arm(args, world, rank, local):
     session.dispose()
     session.close()
 
+    if rank == 0 and not args.no_interference and not args.no_green:
+        try:
+            extras["interference_green"] = measure_interference_green(cfg, args.lat_workers,
+                                                                      args.interf_rounds, args.stream_mib)
+        except Exception as exc:   # green contexts need driver support; report, don't fail the bench
+            extras["interference_green"] = {"error": str(exc)}
+
     # lazy ack (opt-in): wait() returns once the ack is written; the round
     # robin's next worker is another one, so the ack's consumption overlaps.
     # (Each extra session starts after the previous one is disposed: a live
@@ -828,6 +887,7 @@ def main():
     ap.add_argument("--config0-rounds", type=int, default=20_000)
     ap.add_argument("--no-table2", action="store_true")
     ap.add_argument("--no-lazy", action="store_true")
+    ap.add_argument("--no-green", action="store_true")
     ap.add_argument("--lazy-rounds", type=int, default=200_000)
     ap.add_argument("--drivers", type=int, default=4, help="host threads for the multi-driver throughput extra")
     ap.add_argument("--driver-rounds", type=int, default=100_000)
