@@ -424,8 +424,8 @@ def measure_interference_green(cfg, lat_sms, rounds, stream_mib):
         except OSError:
             pass
         while not stop.is_set():
-            ms = b.time_kernel(sw, 4)
-            gbs.append(8 * elems * 4 / (ms * 1e6))
+            ms = b.time_kernel(sw, 4)            # average ms per launch
+            gbs.append(8 * elems / (ms * 1e6))
 
     th = threading.Thread(target=streamer, daemon=True)
     th.start()
