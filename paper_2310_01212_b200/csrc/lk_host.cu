@@ -933,7 +933,7 @@ extern "C" int lk_dispose(lk_session* s, uint64_t* elapsed_ns) {
 extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
   if (!s) return fail(LK_E_USAGE, "null session");
   std::lock_guard<std::mutex> g(s->mu);
-  if (s->kernel_done) {
+  if (s->kernel_done || kernel_status(s) != 0) {   // already retired (or failed): nothing to tell
     s->disposed = true;
     return LK_OK;
   }
