@@ -262,6 +262,8 @@ struct lk_session {
   std::vector<std::vector<uint64_t>> reg_mask;            // per slot (nwords)
   bool disposed = false;
   bool kernel_done = false;
+  bool claimed = true;             // holds the device's one-session claim until the kernel retired
+  void release_claim();
   uint64_t t_create = 0;
 
   // host half of the last dispatch per worker (lk_last_host_times)
@@ -454,6 +456,28 @@ static int spin_words(lk_session* s, const std::vector<uint32_t>& ids, uint32_t 
   return LK_OK;
 }
 
+// ------------------------------------------------------------------ device claims
+static std::mutex g_claim_mu;
+static void release_device(int dev);
+void lk_session::release_claim() {
+  if (claimed) {
+    release_device(device);
+    claimed = false;
+  }
+}
+static uint8_t g_claimed[64];
+
+static bool claim_device(int dev) {
+  std::lock_guard<std::mutex> g(g_claim_mu);
+  if (dev < 0 || dev >= 64 || g_claimed[dev]) return false;
+  g_claimed[dev] = 1;
+  return true;
+}
+static void release_device(int dev) {
+  std::lock_guard<std::mutex> g(g_claim_mu);
+  if (dev >= 0 && dev < 64) g_claimed[dev] = 0;
+}
+
 // ------------------------------------------------------------------ create
 extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* init_ns) {
   if (!cfg_in || !out) return fail(LK_E_USAGE, "null argument");
@@ -498,20 +522,36 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (!prop.cooperativeLaunch) return fail(LK_E_INIT, "device lacks cooperative launch");
   if (!prop.canMapHostMemory) return fail(LK_E_INIT, "device cannot map host memory");
   svc_stream();   // created in the primary context, before any green context is pushed
-  Partition part;
+  // One live session per device and process: a session's CTAs hold every SM
+  // (or, partitioned, SMs split off the whole device), so a second one could
+  // never become resident -- it would spin in boot, then run unbidden later.
   uint32_t nsm = uint32_t(prop.multiProcessorCount);
+  if (cfg.sm_partition && cfg.sm_partition >= nsm)
+    return fail(LK_E_CONFIG, "sm_partition %u must be below the %u SMs", cfg.sm_partition, nsm);
+  if (!cfg.sm_partition && cfg.num_workers > nsm)
+    return fail(LK_E_CONFIG, "num_workers %u exceeds the %u SMs (one worker per SM)", cfg.num_workers, nsm);
+  if (cfg.num_workers > 256) return fail(LK_E_CONFIG, "at most 256 workers (4 mask words)");
+  if (cfg.poll_mode != LK_POLL_DIRECT && (cfg.num_workers ? cfg.num_workers : nsm) > 192 && !cfg.sm_partition)
+    return fail(LK_E_CONFIG, "gateway/hybrid modes support up to 192 workers (4 x 48-bit event masks)");
+  if (!claim_device(cfg.device))
+    return fail(LK_E_BUSY, "device %d already has a live LK session in this process", cfg.device);
+  // from here on every failure path releases the claim (cleanup, or explicitly)
+  Partition part;
   if (cfg.sm_partition) {
-    if (cfg.sm_partition >= nsm) return fail(LK_E_CONFIG, "sm_partition %u must be below the %u SMs", cfg.sm_partition, nsm);
     int prc = make_partition(cfg.device, cfg.sm_partition, &part);
-    if (prc) return prc;
+    if (prc) {
+      release_device(cfg.device);
+      return prc;
+    }
     nsm = part.a_sms;
   }
   if (cfg.num_workers == 0) cfg.num_workers = nsm;
   if (cfg.num_workers > nsm) {
     free_partition(&part);
-    return fail(LK_E_CONFIG, "num_workers %u exceeds the %u SMs (one worker per SM)", cfg.num_workers, nsm);
+    release_device(cfg.device);
+    return fail(LK_E_CONFIG, "num_workers %u exceeds the partition's %u SMs (one worker per SM)", cfg.num_workers,
+                nsm);
   }
-  if (cfg.num_workers > 256) return fail(LK_E_CONFIG, "at most 256 workers (4 mask words)");
 
   auto* s = new lk_session();
   s->part = part;
@@ -529,10 +569,6 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->host_dseq.assign(s->nw, 0);
   s->last_word.assign(s->nw, LK_NOP);
   for (uint32_t i = 0; i < s->nw; ++i) s->all_ids.push_back(i);
-  if (s->gateway && s->nw > 192) {
-    delete s;
-    return fail(LK_E_CONFIG, "gateway mode supports up to 192 workers (4 x 48-bit event masks)");
-  }
   s->pending.assign(s->nwords, 0);
   s->registered.assign(cfg.num_slots, 0);
   s->slot_pend.assign(size_t(cfg.num_slots) * s->nwords, 0);
@@ -556,6 +592,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     }
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     free_partition(&s->part);
+    release_device(s->device);
     delete s;
     return rc;
   };
@@ -923,6 +960,7 @@ extern "C" int lk_dispose(lk_session* s, uint64_t* elapsed_ns) {
     usleep(20);
   }
   s->disposed = true;
+  s->release_claim();
   if (elapsed_ns) *elapsed_ns = now_ns() - t0;
   return LK_OK;
 }
@@ -935,6 +973,7 @@ extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
   std::lock_guard<std::mutex> g(s->mu);
   if (s->kernel_done || kernel_status(s) != 0) {   // already retired (or failed): nothing to tell
     s->disposed = true;
+    s->release_claim();
     return LK_OK;
   }
   s->post(s->all_ids, LK_EXIT);
@@ -946,6 +985,7 @@ extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
     usleep(50);
   }
   s->disposed = true;
+  s->release_claim();
   return LK_OK;
 }
 
@@ -966,6 +1006,7 @@ extern "C" int lk_destroy(lk_session* s) {
   }
   cudaStreamDestroy(s->copy_stream);
   free_partition(&s->part);
+  s->release_claim();
   delete s;
   return LK_OK;
 }

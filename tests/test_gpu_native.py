@@ -537,3 +537,15 @@ def test_sm_partition_session():
         session.wait(m)
     session.dispose()
     assert_trace_ok(session, program, session.num_workers)
+
+
+def test_second_live_session_on_a_device_is_refused():
+    """A live session holds every SM; a second one on the same device could
+    never become resident, so start() refuses it -- and succeeds again once
+    the first is disposed."""
+    first = start(4)
+    with pytest.raises(BusyTriggerError, match="already has a live LK session"):
+        native.NativeSession.start(native.NativeConfig(num_workers=4))
+    first.dispose()
+    second = start(4)
+    second.dispose()
