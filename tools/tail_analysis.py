@@ -13,6 +13,9 @@ import os  # noqa: E402
 native.pin_host_thread(0)
 cores = sorted(os.sched_getaffinity(0))
 os.sched_setaffinity(0, {cores[-1]})
+if "fifo" in sys.argv:
+    os.sched_setscheduler(0, os.SCHED_FIFO, os.sched_param(50))
+    print("SCHED_FIFO 50")
 s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN))
 n = s.num_workers
 s.register(WorkDescriptor(slot=0, kind="empty"))
