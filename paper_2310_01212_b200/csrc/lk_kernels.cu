@@ -402,15 +402,17 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
       reinterpret_cast<float*>(d.out)[rank] = v;
       uint32_t last = 0;
       if (d.aux) {
-        __threadfence();
-        last = atomicAdd(ctr, 1u) == count - 1;
+        // acq_rel RMW: releases this worker's partial, and the last arrival
+        // acquires every other worker's -- no separate fences
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
+        last = prev == count - 1;
       }
       sm.last = last;
     }
   }
   wsync(T);
   if (sm.last && warp == 0) {
-    __threadfence();
     const uint32_t* partials = reinterpret_cast<const uint32_t*>(d.out);
     double tot = 0.0;
     for (uint32_t r = lane; r < count; r += 32) tot += double(__uint_as_float(ld_cg1(partials + r)));
