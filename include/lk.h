@@ -138,6 +138,8 @@ typedef struct lk_config {
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
 #define LK_CF_LSU_PAYLOAD    4u  /* payload items with 128-bit LSU loads instead of the TMA bulk ring */
 #define LK_CF_TIMELINE       8u  /* GATEWAY: stamp forward times into the device timeline (+1 L2 load per value) */
+#define LK_CF_ACK_WINDOW    32u  /* DIRECT, 1 replica: a worker awaiting its ack samples the cell twice
+                                    (a second load poll_spacing_ns after the first) */
 #define LK_CF_LAZY_ACK      16u  /* lk_wait returns once the NOP ack is written; the next trigger or
                                     dispose touching that worker waits for its republished NOP */
 

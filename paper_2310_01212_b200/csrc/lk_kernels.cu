@@ -671,6 +671,48 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
   }
 }
 
+// DIRECT mode, one cell: one ld.relaxed.sys in flight.  With LK_CF_ACK_WINDOW
+// a worker that just published FINISHED -- and so expects the host's ack
+// within about one link round trip -- issues a second load `spacing_ns` after
+// the first, sampling the cell twice in that window (only the one worker that
+// finished does, so the link does not see the 148 x 2 loads that made
+// replicas slower for everyone).
+__device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  const unsigned long long* cell = a.to_gpu + uint64_t(wid) * a.cell_u64;
+  const bool acquire = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
+  const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
+  const uint64_t gap = (a.flags & LK_CF_ACK_WINDOW) ? uint64_t(a.spacing_ns) * 2 : 0;   // ~cycles at 2 GHz
+  for (;;) {
+    const uint32_t act = settle(a, wid, e);
+    if (act != LK_ACT_NONE) return act;
+    unsigned long long v = ld_cell(cell, acquire), x = 0;
+    bool hx = false;
+    for (;;) {
+      bool got = accept(e, v, timeline);
+      if (!got && hx) {
+        hx = false;
+        got = accept(e, x, timeline);
+      }
+      if (got) {
+        const uint32_t f = fast_step(a, wid, e);
+        if (f == kFastBegin) return LK_ACT_BEGIN;
+        if (f == kFastNone) break;                  // general path
+        v = ld_cell(cell, acquire);
+        if (gap && e.st.phase == LK_PHASE_FINISHED) {
+          const uint64_t c0 = clock64();
+          while (clock64() - c0 < gap) {
+          }
+          x = ld_cell(cell, acquire);
+          hx = true;
+        }
+        continue;
+      }
+      v = ld_cell(cell, acquire);
+      if (a.backoff_ns) __nanosleep(a.backoff_ns);
+    }
+  }
+}
+
 // GATEWAY mode: the worker's to_gpu value arrives in its device mailbox line
 // (written by the gateway warp); poll it in L2, one load in flight.
 __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t wid, Elected& e) {
@@ -744,7 +786,7 @@ __device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Ele
   if (a.poll_mode == LK_POLL_HYBRID) return poll_hybrid(a, wid, e, chan);
   if (a.poll_mode == LK_POLL_GATEWAY) return poll_mailbox(a, wid, e);
   switch (a.replicas) {
-    case 1: return poll_k<1>(a, wid, e);
+    case 1: return poll_direct1(a, wid, e);
     case 2: return poll_k<2>(a, wid, e);
     case 8: return poll_k<8>(a, wid, e);
     default: return poll_k<4>(a, wid, e);

@@ -72,6 +72,7 @@ class NativeConfig:
     sm_partition: int = 0           # N > 0: run in a green context of >= N SMs (multiple of 8), one
                                     # worker per partition SM; the rest stay free for other kernels
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
+    ack_window: bool = False        # direct/1 replica: second load while awaiting the ack
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
 
@@ -110,7 +111,8 @@ class NativeConfig:
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)
                    | (_lib.CF_TIMELINE if self.timeline else 0)
-                   | (_lib.CF_LAZY_ACK if self.lazy_ack else 0))
+                   | (_lib.CF_LAZY_ACK if self.lazy_ack else 0)
+                   | (_lib.CF_ACK_WINDOW if self.ack_window else 0))
         return c
 
 
