@@ -688,12 +688,12 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
     unsigned long long v = ld_cell(cell, acquire), x = 0;
     bool hx = false;
     for (;;) {
-      bool got = accept(e, v, timeline);
-      if (!got && hx) {
+      unsigned long long c = v;
+      if (hx) {        // the second sample counts only when the first was stale
+        if (((uint32_t(v >> 32) - e.seq) & 0xFFFFFFu) == 0) c = x;
         hx = false;
-        got = accept(e, x, timeline);
       }
-      if (got) {
+      if (accept(e, c, timeline)) {
         const uint32_t f = fast_step(a, wid, e);
         if (f == kFastBegin) return LK_ACT_BEGIN;
         if (f == kFastNone) break;                  // general path
