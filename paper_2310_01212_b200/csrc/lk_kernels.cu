@@ -786,7 +786,7 @@ __device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Ele
   if (a.poll_mode == LK_POLL_HYBRID) return poll_hybrid(a, wid, e, chan);
   if (a.poll_mode == LK_POLL_GATEWAY) return poll_mailbox(a, wid, e);
   switch (a.replicas) {
-    case 1: return poll_direct1(a, wid, e);
+    case 1: return (a.flags & LK_CF_ACK_WINDOW) ? poll_direct1(a, wid, e) : poll_k<1>(a, wid, e);
     case 2: return poll_k<2>(a, wid, e);
     case 8: return poll_k<8>(a, wid, e);
     default: return poll_k<4>(a, wid, e);

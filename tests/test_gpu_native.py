@@ -549,3 +549,14 @@ def test_second_live_session_on_a_device_is_refused():
     first.dispose()
     second = start(4)
     second.dispose()
+
+
+def test_ack_window_keeps_the_protocol():
+    session = start(8, trace_capacity=2048, ack_window=True)
+    session.register(WorkDescriptor(slot=0, kind="empty"))
+    masks = [1 << i for i in range(8)]
+    session.bench_roundtrip(masks, 0, 400)
+    session.trigger(0b1010, WorkDescriptor(slot=1, iterations=30))
+    session.wait(0b1010)
+    session.dispose()
+    assert_trace_ok(session, [(masks[k % 8], 0) for k in range(400)] + [(0b1010, 1)], 8)
