@@ -632,7 +632,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   // --- device block: desc | masks | ctr | spans | dmb | exited | trace | tcnt
   const size_t descb = al(size_t(cfg.num_slots) * sizeof(lk_desc));
   const size_t maskb = al(size_t(cfg.num_slots) * s->nwords * 8);
-  const size_t ctrb = al(size_t(cfg.num_slots) * 4);
+  const size_t ctrb = al(size_t(cfg.num_slots) * 16);   // per slot: reduce counter, tile claim, done, spare
   const size_t spanb = al(size_t(s->nw) * 8 * LK_TIMELINE_WORDS);
   const size_t dmbb = al(size_t(s->nw) * 128);
   const size_t exb = al(4);
@@ -1312,8 +1312,8 @@ static int baseline_create(int device, uint32_t threads, CUcontext ctx, lk_basel
   b->threads = threads;
   b->in_flight = false;
   b->use_tma = 1;
-  LK_CUDA(dev_alloc(reinterpret_cast<void**>(&b->d_ctr), 4));   // primary context: shared memory
-  LK_CUDA(cudaMemsetAsync(b->d_ctr, 0, 4, svc_stream()));
+  LK_CUDA(dev_alloc(reinterpret_cast<void**>(&b->d_ctr), 16));   // primary context: shared memory
+  LK_CUDA(cudaMemsetAsync(b->d_ctr, 0, 16, svc_stream()));
   LK_CUDA(cudaStreamSynchronize(svc_stream()));
   CtxScope cs(b->ctx);   // kernels, stream and events in the partition's green context
   LK_CUDA(lk_preload_kernels());

@@ -130,6 +130,8 @@ struct Ring {
   uint64_t* full;     // stages mbarriers: 1 arrival (expect_tx) + tx bytes
   uint64_t* empty;    // stages mbarriers: one arrival per consumer warp
   uint32_t stages;    // <= kMaxStages
+  uint32_t* tile;     // stages: global tile index a stage holds (dynamic schedule), shared memory
+  uint32_t* gshared;  // the ring count after a dynamic stream, for threads that did not count it
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -316,6 +318,98 @@ __device__ __forceinline__ void map_tma(const lk_desc& d, Part p, const Op& op, 
   for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
 }
 
+// map through the TMA ring with a balanced tail (LK_CF_STATIC_TILES off):
+// each worker first streams a static share of 7/8 of the tiles, contiguous
+// by rank; the last 1/8 of the tiles form a pool claimed one at a time with
+// an atomic counter, the next claim issued before the current tile's copies
+// so the atomic's L2 round trip overlaps them.  Whoever finishes its share
+// first takes more of the pool, so a dispatch ends when the *average*
+// worker would, not the slowest one (per-dispatch stragglers are random:
+// tools/straggler.py).  Elementwise maps only: results do not depend on who
+// computes a tile.  ctr[0] = next pool tile, ctr[1] = workers done; the last
+// worker to finish resets both for the slot's next dispatch.
+constexpr uint32_t kTileEnd = 0xFFFFFFFFu;
+
+template <bool kTwo, class Op>
+__device__ __forceinline__ void map_tma_dyn(const lk_desc& d, uint32_t rank, uint32_t count, const Op& op,
+                                            uint32_t T, Ring& r, uint32_t& g, uint32_t* ctr) {
+  const uint4* a4 = reinterpret_cast<const uint4*>(d.in0);
+  const uint4* c4 = reinterpret_cast<const uint4*>(d.in1);
+  uint4* o4 = reinterpret_cast<uint4*>(d.out);
+  constexpr uint32_t kTileV = kTwo ? kStageBytes / 32 : kStageBytes / 16;   // uint4 per input per tile
+  const uint64_t nv = d.n >> 2;                                           // vector part, all workers
+  const uint32_t ntiles = uint32_t((nv + kTileV - 1) / kTileV);
+  const uint32_t share = uint32_t((uint64_t(ntiles) * 7 / 8) / count);     // static tiles per worker
+  const uint32_t pool0 = share * count;                                    // first pool tile
+  const uint32_t c0 = g, S = r.stages;
+  if (threadIdx.x == 0) {
+    uint32_t f = c0;
+    auto fill = [&](uint32_t t) {                                          // t = global tile or kTileEnd
+      const uint32_t st = f % S;
+      mbar_wait(r.empty + st, ((f / S) & 1u) ^ 1u);
+      r.tile[st] = t;
+      if (t == kTileEnd) {
+        mbar_arrive(r.full + st);                                          // wake consumers, no bytes
+      } else {
+        const uint64_t v0 = uint64_t(t) * kTileV;
+        const uint32_t bytes = uint32_t(min(uint64_t(kTileV), nv - v0)) * 16u;
+        mbar_expect_tx(r.full + st, kTwo ? 2 * bytes : bytes);
+        bulk_g2s(r.buf + st * kStageBytes, a4 + v0, bytes, r.full + st);
+        if (kTwo) bulk_g2s(r.buf + st * kStageBytes + kStageBytes / 2, c4 + v0, bytes, r.full + st);
+      }
+      ++f;
+    };
+    for (uint32_t i = 0; i < share; ++i) fill(rank * share + i);
+    uint32_t claim = atomicAdd(ctr, 1u);
+    for (;;) {
+      const uint32_t t = pool0 + claim;
+      if (t >= ntiles) break;
+      const uint32_t next = atomicAdd(ctr, 1u);                           // in flight during fill(t)
+      fill(t);
+      claim = next;
+    }
+    fill(kTileEnd);
+    *r.gshared = f;
+  } else if (threadIdx.x >= 32) {
+    const uint32_t ci = threadIdx.x - 32, nc = T - 32;
+    for (uint32_t c = c0;; ++c) {
+      const uint32_t st = c % S;
+      mbar_wait(r.full + st, (c / S) & 1u);
+      const uint32_t t = r.tile[st];
+      if (t != kTileEnd) {
+        const uint64_t v0 = uint64_t(t) * kTileV;
+        const uint32_t nvt = uint32_t(min(uint64_t(kTileV), nv - v0));
+        const uint8_t* stage = r.buf + st * kStageBytes;
+        for (uint32_t v = ci; v < nvt; v += nc) {
+          const uint4 x = lds4(stage + 16 * v);
+          const uint4 y = kTwo ? lds4(stage + kStageBytes / 2 + 16 * v) : x;
+          st4(o4 + v0 + v, vop(op, x, y));
+        }
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(r.empty + st);
+      if (t == kTileEnd) break;
+    }
+  }
+  wsync(T);                                                                // gshared visible; stream done
+  g = *r.gshared;
+  if (threadIdx.x == 0) {
+    // scalar tail (n % 4 elements) by rank 0; then count this worker done
+    if (rank == 0) {
+      const uint32_t* a = reinterpret_cast<const uint32_t*>(d.in0);
+      const uint32_t* c = reinterpret_cast<const uint32_t*>(d.in1);
+      uint32_t* o = reinterpret_cast<uint32_t*>(d.out);
+      for (uint64_t i = nv << 2; i < d.n; ++i) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
+    }
+    uint32_t prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr + 1) : "memory");
+    if (prev == count - 1) {   // last one out: no worker claims from this slot any more
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -446,23 +540,31 @@ __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
 // ring == nullptr (or misaligned buffers): 128-bit LSU loads; else the TMA ring.
 __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
                                           uint32_t* ctr, ReduceSmem& rs, uint32_t T, Ring* ring,
-                                          uint32_t& g) {
+                                          uint32_t& g, bool dyn = false) {
   const Part p = partition(d.n, rank, count);
   const bool tma = ring != nullptr && !(d.flags & LK_DF_SCALAR);
+  dyn = dyn && tma && T >= 64 && ring->tile != nullptr;
   switch (d.kind) {
     case LK_KIND_VECTOR_ADD_I32:
-      if (tma) map_tma<true>(d, p, OpAddI32{}, T, *ring, g);
+      if (dyn) map_tma_dyn<true>(d, rank, count, OpAddI32{}, T, *ring, g, ctr + 1);
+      else if (tma) map_tma<true>(d, p, OpAddI32{}, T, *ring, g);
       else map_chunk<4, true>(d, p, OpAddI32{}, T);
       break;
     case LK_KIND_SAXPY_F32:
-      if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, *ring, g);
+      if (dyn) map_tma_dyn<true>(d, rank, count, OpSaxpy{d.alpha}, T, *ring, g, ctr + 1);
+      else if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, *ring, g);
       else map_chunk<4, true>(d, p, OpSaxpy{d.alpha}, T);
       break;
     case LK_KIND_HBM_STREAM: {
       const uint64_t passes = d.iterations ? d.iterations : 1;
       for (uint64_t k = 0; k < passes; ++k) {
-        if (tma) map_tma<false>(d, p, OpCopy{}, T, *ring, g);
-        else map_chunk<8, false>(d, p, OpCopy{}, T);
+        if (dyn && passes == 1) {   // multi-pass: a fast worker would claim the next pass early
+          map_tma_dyn<false>(d, rank, count, OpCopy{}, T, *ring, g, ctr + 1);
+        } else if (tma) {
+          map_tma<false>(d, p, OpCopy{}, T, *ring, g);
+        } else {
+          map_chunk<8, false>(d, p, OpCopy{}, T);
+        }
       }
       break;
     }
@@ -895,6 +997,7 @@ struct PersistSmem {
   uint32_t cmd, rank, count, slot;
   ReduceSmem red;
   uint64_t full[kMaxStages], empty[kMaxStages];
+  uint32_t tile[kMaxStages], ring_g;
   unsigned long long chan[2];      // HYBRID: latest direct-cell value, latest mailbox value
   uint32_t stop;                   // HYBRID: the protocol thread left its loop
   uint32_t sink;                   // keeps busy_loop's result live
@@ -924,7 +1027,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     return;
   }
   extern __shared__ __align__(128) uint8_t dyn_smem[];
-  Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages};
+  Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages, sm.tile, &sm.ring_g};
   Ring* rp = a.use_tma ? &ring : nullptr;
   uint32_t g = 0;
   if (rp) ring_init(ring, T);
@@ -1010,7 +1113,8 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     wsync(T);
     if (sm.cmd == kCmdExit) break;
     const lk_desc d = sm.desc;
-    run_multi(d, sm.rank, sm.count, a.reduce_ctr + sm.slot, sm.red, T, rp, g);
+    run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T, rp, g,
+              !(a.flags & LK_CF_STATIC_TILES));
     wsync(T);
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();
@@ -1042,7 +1146,7 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
     if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) rs.last = busy_loop(d.iterations);
     return;
   }
-  Ring ring{dyn_smem, full, empty, kDefaultStages};
+  Ring ring{dyn_smem, full, empty, kDefaultStages, nullptr, nullptr};   // static tiles only
   uint32_t g = 0;
   if (use_tma) ring_init(ring, blockDim.x);
   run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, use_tma ? &ring : nullptr, g);

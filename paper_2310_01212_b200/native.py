@@ -73,6 +73,7 @@ class NativeConfig:
                                     # worker per partition SM; the rest stay free for other kernels
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
     ack_window: bool = False        # direct/1 replica: second load while awaiting the ack
+    dynamic_tiles: bool = True      # payload maps: static 7/8 share + a pool claimed by early finishers
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
 
@@ -112,7 +113,8 @@ class NativeConfig:
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)
                    | (_lib.CF_TIMELINE if self.timeline else 0)
                    | (_lib.CF_LAZY_ACK if self.lazy_ack else 0)
-                   | (_lib.CF_ACK_WINDOW if self.ack_window else 0))
+                   | (_lib.CF_ACK_WINDOW if self.ack_window else 0)
+                   | (0 if self.dynamic_tiles else _lib.CF_STATIC_TILES))
         return c
 
 
