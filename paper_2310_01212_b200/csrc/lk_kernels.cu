@@ -544,6 +544,10 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
   const Part p = partition(d.n, rank, count);
   const bool tma = ring != nullptr && !(d.flags & LK_DF_SCALAR);
   dyn = dyn && tma && T >= 64 && ring->tile != nullptr;
+  if (dyn) {   // the pool's atomics cost ~1 us: only worth it with >= 8 tiles per worker
+    const uint64_t tile_v = (d.kind == LK_KIND_HBM_STREAM) ? kStageBytes / 16 : kStageBytes / 32;
+    dyn = ((d.n >> 2) + tile_v - 1) / tile_v >= 8ull * count;
+  }
   switch (d.kind) {
     case LK_KIND_VECTOR_ADD_I32:
       if (dyn) map_tma_dyn<true>(d, rank, count, OpAddI32{}, T, *ring, g, ctr + 1);
