@@ -42,7 +42,7 @@ CF_LSU_PAYLOAD = 4
 CF_TIMELINE = 8
 CF_LAZY_ACK = 16
 CF_ACK_WINDOW = 32
-CF_STATIC_TILES = 64
+CF_DYNAMIC_TILES = 64
 POLL_DIRECT = 0
 POLL_GATEWAY = 1
 POLL_HYBRID = 2

@@ -318,7 +318,7 @@ __device__ __forceinline__ void map_tma(const lk_desc& d, Part p, const Op& op, 
   for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
 }
 
-// map through the TMA ring with a balanced tail (LK_CF_STATIC_TILES off):
+// map through the TMA ring with a balanced tail (LK_CF_DYNAMIC_TILES):
 // each worker first streams a static share of 7/8 of the tiles, contiguous
 // by rank; the last 1/8 of the tiles form a pool claimed one at a time with
 // an atomic counter, the next claim issued before the current tile's copies
@@ -1118,7 +1118,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     if (sm.cmd == kCmdExit) break;
     const lk_desc d = sm.desc;
     run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T, rp, g,
-              !(a.flags & LK_CF_STATIC_TILES));
+              (a.flags & LK_CF_DYNAMIC_TILES) != 0);
     wsync(T);
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();

@@ -73,7 +73,7 @@ class NativeConfig:
                                     # worker per partition SM; the rest stay free for other kernels
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
     ack_window: bool = False        # direct/1 replica: second load while awaiting the ack
-    dynamic_tiles: bool = True      # payload maps: static 7/8 share + a pool claimed by early finishers
+    dynamic_tiles: bool = False     # payload maps: static 7/8 share + a pool claimed by early finishers
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
 
@@ -114,7 +114,7 @@ class NativeConfig:
                    | (_lib.CF_TIMELINE if self.timeline else 0)
                    | (_lib.CF_LAZY_ACK if self.lazy_ack else 0)
                    | (_lib.CF_ACK_WINDOW if self.ack_window else 0)
-                   | (0 if self.dynamic_tiles else _lib.CF_STATIC_TILES))
+                   | (_lib.CF_DYNAMIC_TILES if self.dynamic_tiles else 0))
         return c
 
 

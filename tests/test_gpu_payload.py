@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 RTOL_F32_REDUCE = 1e-6
 
 
-@pytest.fixture(scope="module", params=["tma-direct", "lsu-direct", "tma-gateway", "tma-hybrid"])
+@pytest.fixture(scope="module", params=["tma-direct", "lsu-direct", "tma-gateway", "tma-hybrid", "dyn-gateway"])
 def session(request):
     try:   # bring torch's CUDA state AND the kernels the torch test uses up before the
         # persistent kernel is resident: CUDA 12 loads kernels lazily, and a module
@@ -34,7 +34,8 @@ def session(request):
         pass
     path, mode = request.param.split("-")
     s, _ = native.NativeSession.start(native.NativeConfig(spin_yield_threshold=200, poll_mode=mode,
-                                                          tma_payload=path == "tma"))
+                                                          tma_payload=path != "lsu",
+                                                          dynamic_tiles=path == "dyn"))
     yield s
     s.close()
 
