@@ -560,3 +560,15 @@ def test_ack_window_keeps_the_protocol():
     session.wait(0b1010)
     session.dispose()
     assert_trace_ok(session, [(masks[k % 8], 0) for k in range(400)] + [(0b1010, 1)], 8)
+
+
+@pytest.mark.slow
+def test_gateway_event_tags_wrap():
+    """More than 2^16 ring events (the torn-read tag is seq & 0xFFFF) and
+    hundreds of ring wraparounds: every round still completes in order."""
+    session = start(16, poll_mode="gateway")
+    session.register(WorkDescriptor(slot=0, kind="empty"))
+    full = (1 << 16) - 1
+    _, done, cyc = session.bench_roundtrip([full], 0, 36_000)   # 2 events per round
+    assert (cyc >= done).all() and len(done) == 36_000
+    session.dispose()
