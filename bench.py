@@ -396,6 +396,27 @@ def measure_config0(session, rounds, n=65536):
 _LOCAL_CORES: list = []
 
 
+def read_only_peak(device):
+    try:
+        import torch
+        x = torch.empty(1 << 28, dtype=torch.float32, device=f"cuda:{device}").uniform_()
+        for _ in range(3):
+            x.sum()
+        best = None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(10):
+            e0.record()
+            x.sum()
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del x
+        return round((1 << 30) / (best * 1e6), 1)
+    except Exception:
+        return None
+
+
 def measure_interference_green(cfg, lat_sms, rounds, stream_mib):
     """configs[3] with a hardware partition: the LK session runs in a green
     context of lat_sms SMs (16); an ordinary hbm_stream kernel (the baseline's
@@ -808,6 +829,15 @@ def run_lk_arm(args, world, rank, local):
             extras["standalone_saxpy_kernel"] = standalone_kernel_gbs(device, "saxpy_f32", max(args.payload_mib))
         except Exception as exc:  # pragma: no cover
             extras["standalone_saxpy_kernel"] = {"error": str(exc)}
+        # the reduction reads only: its ceiling is a read-only stream, measured
+        # here with torch.sum over 1 GiB (CUDA events; no LK session is live)
+        rpk = read_only_peak(device)
+        if rpk and "block_reduce_f32" in payload:
+            rach = payload["block_reduce_f32"][big]["gbs_device"]
+            extras["reduce_roofline"] = {"bound": "hbm (read-only)", "achieved": rach, "peak": rpk,
+                                         "unit": "GB/s", "frac": round(rach / rpk, 4),
+                                         "peak_source": "torch.sum over 1 GiB fp32, best of 10, this box",
+                                         "kernel": f"lk_persistent_kernel block_reduce_f32 {big}"}
 
     if rank == 0 and not args.no_table2:
         extras["table2_b200"] = measure_table2(device)
