@@ -190,6 +190,21 @@ def load() -> C.CDLL:
     return lib
 
 
+_raw = None
+
+
+def raw() -> C.CDLL:
+    """The same library through a second handle whose functions carry no
+    argtypes: for the per-task hot calls (lk_trigger, lk_wait) whose
+    arguments the caller already passes as ctypes-ready objects, skipping
+    ctypes' per-argument conversion (~40% of the call cost)."""
+    global _raw
+    if _raw is None:
+        load()
+        _raw = C.CDLL(str(LIB_PATH))
+    return _raw
+
+
 def last_error() -> str:
     return load().lk_last_error().decode(errors="replace")
 

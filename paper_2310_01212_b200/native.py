@@ -172,6 +172,8 @@ class NativeSession:
     def __init__(self, cfg: NativeConfig, handle: C.c_void_p, num_workers: int):
         self.cfg = cfg
         self._lib = _lib.load()
+        raw = _lib.raw()
+        self._raw_trigger, self._raw_wait = raw.lk_trigger, raw.lk_wait   # hot path: no argtypes
         self._h = handle
         self.num_workers = num_workers
         self.nwords = (num_workers + 63) // 64
@@ -316,7 +318,7 @@ class NativeSession:
             d = None   # this descriptor object is already staged for this worker set
         else:
             d = C.byref(work.to_c())
-        rc = self._lib.lk_trigger(self._h, self._mask(mask), self.nwords, work.slot, d, self._u64_ref)
+        rc = self._raw_trigger(self._h, self._mask(mask), self.nwords, work.slot, d, self._u64_ref)
         if rc:
             _lib.raise_for(rc)
         if d is not None:
@@ -336,7 +338,7 @@ class NativeSession:
         """Spin (in C) until every masked worker published FINISHED, then ack."""
         self._require_live()
         self._check(mask)
-        rc = self._lib.lk_wait(self._h, self._mask(mask), self.nwords, self._u64_ref)
+        rc = self._raw_wait(self._h, self._mask(mask), self.nwords, self._u64_ref)
         if rc:
             _lib.raise_for(rc, sm_ids=tuple(sms_in_mask(mask)))
         timing = _timing(PHASE_WAIT, self._u64.value, mask)
