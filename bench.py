@@ -802,6 +802,17 @@ def run_lk_arm(args, world, rank, local):
         b1.bench(empty, 200, grid)
         launch, total = b1.bench(empty, args.base_rounds, grid)
         base[name] = {"launch": lat_summary(launch), "launch_plus_sync": lat_summary(total)}
+    # the same conventional flow through the Python API (launch() + wait() per
+    # task), the counterpart of the LK arm's e2e
+    n_py = min(args.e2e_rounds, 50_000)
+    for _ in range(200):
+        b1.launch(empty, 1)
+        b1.wait()
+    t0 = time.perf_counter_ns()
+    for _ in range(n_py):
+        b1.launch(empty, 1)
+        b1.wait()
+    base["python_api_tasks_per_s"] = round(n_py / ((time.perf_counter_ns() - t0) / 1e9), 1)
     b1.close()
     pp = native.pingpong(device, args.pp_rounds)
     extras["pingpong_floor"] = lat_summary(pp[100:])
