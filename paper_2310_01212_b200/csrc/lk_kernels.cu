@@ -116,9 +116,8 @@ __device__ __forceinline__ void st4(uint4* p, uint4 v) {
 // counted on an mbarrier by transaction bytes.  Up to `stages` tiles of
 // kStageBytes are in flight per SM (6 x 16 KiB = 96 KiB by default: at
 // ~44 GB/s per SM and a loaded HBM latency of ~1.5 us Little's law asks for
-// ~66 KiB per SM; 4-12 stages measured within noise of each other,
-// tools/sweep_ring.py), issued by one elected thread while every worker
-// thread consumes.  The ring persists across dispatches: `g` counts tiles consumed
+// ~66 KiB per SM; 6 measured best of 4/6/8/12, tools/ab_stages.py), issued
+// by one elected thread while the other warps consume.  The ring persists across dispatches: `g` counts tiles consumed
 // since the barriers were initialised (identical in every thread), so
 // stage = g % stages and the mbarrier phase parity = (g / stages) & 1.
 constexpr uint32_t kStageBytes = 16384;
