@@ -268,6 +268,11 @@ int lk_last_host_times(lk_session* s, uint64_t* t, uint32_t n);
 /* globaltimer - CLOCK_MONOTONIC offset (ns) from `rounds` host<->GPU echoes,
  * taken from the echo with the shortest round trip (*best_rtt_ns). */
 int lk_clock_offset(int device, uint32_t rounds, int64_t* offset_ns, uint64_t* best_rtt_ns);
+/* GPC membership of each SM (the placement side of check_block_mapping,
+ * device.py:102-111): clustered launches of a probe kernel -- a cluster's
+ * CTAs share a GPC -- with the SM ids of each cluster unioned.  Needs every
+ * SM (no session live).  gpc[smid] = dense group id, -1 if never observed. */
+int lk_sm_topology(int device, int32_t* gpc, uint32_t n, uint32_t* ngroups);
 
 /* Raw host<->GPU ping-pong floor: one thread polls a mapped host word and
  * echoes it back; rounds samples of the round trip. */

@@ -148,6 +148,7 @@ SIGNATURES = {
     "lk_last_timeline": (I32, [P, P, U32]),
     "lk_last_host_times": (I32, [P, P, U32]),
     "lk_clock_offset": (I32, [I32, U32, PI64, PU64]),
+    "lk_sm_topology": (I32, [I32, C.POINTER(C.c_int32), U32, PU32]),
     "lk_pingpong": (I32, [I32, U64, P]),
     "lk_baseline_create": (I32, [I32, U32, C.POINTER(P)]),
     "lk_baseline_launch": (I32, [P, C.POINTER(lk_desc), U32, PU64]),

@@ -1089,6 +1089,71 @@ extern "C" int lk_last_host_times(lk_session* s, uint64_t* t, uint32_t n) {
   return LK_OK;
 }
 
+// GPC membership of every SM: clustered launches of a probe kernel (a
+// cluster's CTAs share a GPC) over many grid sizes, SM ids of a cluster
+// unioned.  Run with no session live (it needs every SM).  gpc[smid] = group
+// id (dense, 0..*ngroups-1), or -1 for an SM never observed.
+extern "C" int lk_sm_topology(int device, int32_t* gpc, uint32_t n, uint32_t* ngroups) {
+  if (!gpc || !ngroups) return fail(LK_E_USAGE, "null argument");
+  LK_CUDA(cudaSetDevice(device));
+  int nsm = 0, optin = 0;
+  LK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  LK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  std::vector<int> parent(size_t(nsm) + 1);
+  std::vector<uint8_t> seen(size_t(nsm) + 1, 0);
+  for (int i = 0; i <= nsm; ++i) parent[i] = i;
+  auto find = [&](int x) {
+    while (parent[x] != x) x = parent[x] = parent[parent[x]];
+    return x;
+  };
+  uint32_t* d = nullptr;
+  LK_CUDA(dev_alloc(reinterpret_cast<void**>(&d), 4096 * 4));
+  std::vector<uint32_t> h(4096);
+  cudaStream_t st;
+  LK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const size_t smem = size_t(optin) / 2 + 1024;   // one CTA per SM
+  int rc = LK_OK;
+  for (uint32_t cluster : {8u, 16u, 4u, 2u}) {
+    for (uint32_t k = 1; k * cluster <= uint32_t(nsm) && rc == LK_OK; ++k) {
+      const uint32_t grid = k * cluster;
+      cudaError_t e = lk_launch_topo(d, grid, cluster, smem, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, grid * 4, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (cluster > 8) break;   // non-portable size unsupported: skip it
+        rc = fail(LK_E_CUDA, "topology probe: %s", cudaGetErrorString(e));
+        break;
+      }
+      for (uint32_t c = 0; c < grid; c += cluster) {
+        const int r0 = find(int(std::min<uint32_t>(h[c], uint32_t(nsm))));
+        for (uint32_t j = 0; j < cluster; ++j) {
+          const uint32_t sm = std::min<uint32_t>(h[c + j], uint32_t(nsm));
+          seen[sm] = 1;
+          const int rj = find(int(sm));
+          if (rj != r0) parent[rj] = r0;
+        }
+      }
+    }
+  }
+  cudaStreamDestroy(st);
+  dev_free(d);
+  if (rc) return rc;
+  std::vector<int> id(size_t(nsm) + 1, -1);
+  uint32_t groups = 0;
+  for (uint32_t sm = 0; sm < n; ++sm) {
+    if (sm >= uint32_t(nsm) || !seen[sm]) {
+      gpc[sm] = -1;
+      continue;
+    }
+    const int r = find(int(sm));
+    if (id[r] < 0) id[r] = int(groups++);
+    gpc[sm] = id[r];
+  }
+  *ngroups = groups;
+  return LK_OK;
+}
+
 extern "C" int lk_clock_offset(int device, uint32_t rounds, int64_t* offset_ns, uint64_t* best_rtt_ns) {
   if (!offset_ns || rounds == 0) return fail(LK_E_USAGE, "bad argument");
   LK_CUDA(cudaSetDevice(device));

@@ -1176,7 +1176,35 @@ __global__ void lk_clocksync_kernel(const uint32_t* flag, unsigned long long* ec
   }
 }
 
+// SM topology probe: every CTA of a cluster runs on the same GPC, so the SM
+// ids of one cluster's CTAs belong to one GPC (lk_sm_topology unions them).
+__global__ void lk_topo_kernel(uint32_t* smids) {
+  if (threadIdx.x == 0) smids[blockIdx.x] = smid();
+}
+
 }  // namespace
+
+// One clustered launch of the topology probe: grid blocks in clusters of
+// `cluster` CTAs, one CTA per SM (large dynamic shared memory).
+cudaError_t lk_launch_topo(uint32_t* smids, uint32_t grid, uint32_t cluster, size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaFuncSetAttribute(lk_topo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e == cudaSuccess && cluster > 8)
+    e = cudaFuncSetAttribute(lk_topo_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, lk_topo_kernel, smids);
+}
 
 cudaError_t lk_launch_clocksync(const uint32_t* flag, unsigned long long* echo, uint32_t rounds,
                                 cudaStream_t st) {

@@ -555,6 +555,26 @@ class LaunchSyncBaseline:
 ThreadSpawnBaseline = LaunchSyncBaseline
 
 
+def sm_topology(device: int = 0) -> list[int]:
+    """GPC group of every SM (index = %smid), from clustered probe launches
+    (lk_sm_topology).  Call with no session live.  Combine with a session's
+    ``smid_map`` to place a latency partition on one GPC, or spread it."""
+    n = C.c_int()
+    _lib.check(_lib.load().lk_sm_count(device, C.byref(n)))
+    out = (C.c_int32 * n.value)()
+    groups = C.c_uint32()
+    _lib.check(_lib.load().lk_sm_topology(device, out, n.value, C.byref(groups)))
+    return list(out)
+
+
+def workers_by_gpc(smid_map: list[int], topology: list[int]) -> dict[int, list[int]]:
+    """{gpc: [worker ids]} for a session's workers."""
+    out: dict[int, list[int]] = {}
+    for w, sm in enumerate(smid_map):
+        out.setdefault(topology[sm] if 0 <= sm < len(topology) else -1, []).append(w)
+    return out
+
+
 def clock_offset(device: int = 0, rounds: int = 2000) -> tuple[int, int]:
     """(globaltimer - CLOCK_MONOTONIC ns, best echo round trip ns)."""
     off, rtt = C.c_int64(), C.c_uint64()

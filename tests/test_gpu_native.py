@@ -572,3 +572,18 @@ def test_gateway_event_tags_wrap():
     _, done, cyc = session.bench_roundtrip([full], 0, 36_000)   # 2 events per round
     assert (cyc >= done).all() and len(done) == 36_000
     session.dispose()
+
+
+def test_sm_topology_groups_sms_by_gpc():
+    """lk_sm_topology: clustered probe launches group every SM into GPCs
+    (B200: 148 SMs in ~8 GPCs of <= 20); a session's workers map onto them."""
+    topo = native.sm_topology(0)
+    assert len(topo) >= 148 and all(g >= 0 for g in topo)
+    sizes = {}
+    for g in topo:
+        sizes[g] = sizes.get(g, 0) + 1
+    assert 2 <= len(sizes) <= 32 and max(sizes.values()) <= 32, sizes
+    session = start(None)
+    by = native.workers_by_gpc(session.smid_map, topo)
+    session.dispose()
+    assert sum(len(v) for v in by.values()) == session.num_workers and -1 not in by
