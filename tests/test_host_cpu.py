@@ -175,3 +175,25 @@ def test_trace_files_validate_with_reference_cli(reference, tmp_path):
         g = tmp_path / f"{name}.bad.trace"
         g.write_text(protocol.format_trace(bad))
         assert ref_cli.main(["validate", str(g)]) == 1, name
+
+
+def test_fast_phase_timing_equals_validated_one():
+    from paper_2310_01212_b200 import native
+    t = native._timing(host.PHASE_WAIT, 123, 0b101)
+    assert t == host.PhaseTiming(host.PHASE_WAIT, 123, 0b101)
+    assert hash(t) == hash(host.PhaseTiming(host.PHASE_WAIT, 123, 0b101))
+    assert repr(t) == repr(host.PhaseTiming(host.PHASE_WAIT, 123, 0b101))
+
+
+def test_workers_by_gpc_groups_workers():
+    from paper_2310_01212_b200 import native
+    topo = [0, 0, 1, 1, 2]
+    assert native.workers_by_gpc([4, 0, 3, 1], topo) == {2: [0], 0: [1, 3], 1: [2]}
+    assert native.workers_by_gpc([9], topo) == {-1: [0]}
+
+
+def test_raw_handle_exports_hot_calls():
+    raw = _lib.raw()
+    assert raw.lk_trigger and raw.lk_wait
+    # argtype-free calls on a null session fail cleanly, not crash
+    assert raw.lk_wait(None, b"\x01" + b"\x00" * 7, 1, None) == _lib.LK_E_USAGE
