@@ -318,7 +318,8 @@ class NativeSession:
             d = None   # this descriptor object is already staged for this worker set
         else:
             d = C.byref(work.to_c())
-        rc = self._raw_trigger(self._h, self._mask(mask), self.nwords, work.slot, d, self._u64_ref)
+        trig = self._raw_trigger if work.slot <= 0x7FFFFFFF else self._lib.lk_trigger   # raw: C int args
+        rc = trig(self._h, self._mask(mask), self.nwords, work.slot, d, self._u64_ref)
         if rc:
             _lib.raise_for(rc)
         if d is not None:

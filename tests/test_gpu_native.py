@@ -587,3 +587,14 @@ def test_sm_topology_groups_sms_by_gpc():
     by = native.workers_by_gpc(session.smid_map, topo)
     session.dispose()
     assert sum(len(v) for v in by.values()) == session.num_workers and -1 not in by
+
+
+def test_huge_slot_numbers_are_refused_cleanly():
+    """Slots up to the reference's MAX_SLOT (2^32 - 17) are legal words; ones
+    beyond the device table are a UsageError, not a ctypes overflow."""
+    session = start(1)
+    with pytest.raises(UsageError):
+        session.trigger(1, WorkDescriptor(slot=protocol.MAX_SLOT, iterations=1))
+    session.trigger(1, TINY_WORK)
+    session.wait(1)
+    session.dispose()
