@@ -307,7 +307,7 @@ def run_reference_arm(args, world, rank):
         "latency_us": lat_summary(lat),
         "cpu_baseline": {"value": round(value, 3), "unit": "tasks/s", "cores": cores, "kind": Exe.kind,
                          "sample": f"{rounds} round trips on {workers} Python worker threads "
-                                   f"(GIL-bound; {cores} host threads available)"},
+                                   f"(GIL-bound; {cores} host threads available)", "host": host_info()},
         "e2e": {"value": round(value, 3), "unit": "tasks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -394,6 +394,15 @@ def measure_config0(session, rounds, n=65536):
 
 
 _LOCAL_CORES: list = []
+
+
+def host_info():
+    """The CPU side of the comparison: what the reference
+    executor's Python threads ran on."""
+    import platform
+    return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "python": platform.python_version(), "switchinterval_s": sys.getswitchinterval(),
+            "cpu": platform.processor() or platform.machine()}
 
 
 def read_only_peak(device):
@@ -856,7 +865,7 @@ def run_lk_arm(args, world, rank, local):
     cpu = None
     if not args.no_cpu_baseline:
         cv, clat, ckind = cpu_baseline_config0(budget_s=args.cpu_budget_s)
-        cpu = {"value": round(cv, 2), "unit": "tasks/s", "cores": 1, "kind": ckind,
+        cpu = {"value": round(cv, 2), "unit": "tasks/s", "cores": 1, "kind": ckind, "host": host_info(),
                "sample": f"{len(clat)} round trips of BASELINE config 0 (4 Python worker threads, "
                          "int32 vector add 64 Ki elements via numpy on the worker, spin_yield_threshold "
                          "10000 = reference default); GIL-serialised so ~1 core; p50 "
