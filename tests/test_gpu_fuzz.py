@@ -31,7 +31,7 @@ def _check_trace(session, program):
         assert proj[i] == projection.expected_projection(per[i]), i
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_random_programs(seed):
     rng = random.Random(seed)
     cfg = native.NativeConfig(num_workers=NW, record_trace=True, trace_capacity=8192,
@@ -44,7 +44,7 @@ def test_random_programs(seed):
     try:
         program = []
         slot = 0
-        for step in range(40):
+        for step in range(60):
             # up to three overlapping dispatches on disjoint worker sets, then wait
             free = list(range(NW))
             rng.shuffle(free)
