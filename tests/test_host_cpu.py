@@ -197,3 +197,45 @@ def test_raw_handle_exports_hot_calls():
     assert raw.lk_trigger and raw.lk_wait
     # argtype-free calls on a null session fail cleanly, not crash
     assert raw.lk_wait(None, b"\x01" + b"\x00" * 7, 1, None) == _lib.LK_E_USAGE
+
+
+def _gpu_trace_program(n):
+    """The dispatch program tools/record_gpu_trace.py ran on the B200."""
+    full = (1 << n) - 1
+    return [(full, 1) if k % 100 == 99 else (1 << (k % n), 0) for k in range(1500)]
+
+
+def _gpu_trace_records():
+    import gzip
+    text = gzip.decompress((ROOT / "tests" / "golden" / "gpu_trace_r01.txt.gz").read_bytes()).decode()
+    return text, protocol.parse_trace(text)
+
+
+def test_recorded_b200_trace_replays_clean():
+    """A device trace recorded on a B200 (148 workers, 1500 dispatches, with
+    full-mask saxpy payloads; tools/record_gpu_trace.py) replays clean in the
+    oracle and the native validator, and every worker's projection is the one
+    the handshake fixes for the program that ran."""
+    from oracle import projection
+    from oracle import protocol as O
+    _, recs = _gpu_trace_records()
+    writes = [(r.side, r.sm_id, r.word) for r in recs]
+    n = 148
+    assert max(r.sm_id for r in recs) == n - 1
+    assert O.replay(writes).violation is None
+    assert protocol.validate_trace(writes) is None
+    per = projection.program_slots(_gpu_trace_program(n), n)
+    proj = projection.projections(writes, n)
+    for i in range(n):
+        assert proj[i] == projection.expected_projection(per[i]), i
+
+
+def test_recorded_b200_trace_validates_with_reference_cli(reference, tmp_path):
+    """The same B200 trace file passes the reference's own `persistkern
+    validate` (P/cli.py:223-235) -- device trace capture feeding the
+    reference's validator."""
+    from persistkern import cli as ref_cli
+    text, _ = _gpu_trace_records()
+    f = tmp_path / "b200.trace"
+    f.write_text(text)
+    assert ref_cli.main(["validate", str(f)]) == 0
