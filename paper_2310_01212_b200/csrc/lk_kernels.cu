@@ -507,8 +507,21 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
   wsync(T);
   if (sm.last && warp == 0) {
     const uint32_t* partials = reinterpret_cast<const uint32_t*>(d.out);
+    // the loads of a group are independent, so their L2 round trips overlap
+    // (one at a time they cost ~0.2 us each); the add order per lane is
+    // unchanged: r = lane, lane + 32, ...
     double tot = 0.0;
-    for (uint32_t r = lane; r < count; r += 32) tot += double(__uint_as_float(ld_cg1(partials + r)));
+    for (uint32_t r0 = 0; r0 < count; r0 += 32 * 5) {
+      float v[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const uint32_t r = r0 + 32 * k + lane;
+        v[k] = r < count ? __uint_as_float(ld_cg1(partials + r)) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+        if (r0 + 32 * k + lane < count) tot += double(v[k]);
+    }
     tot = warp_sum(tot);
     if (lane == 0) {
       *reinterpret_cast<double*>(d.aux) = tot;
