@@ -128,6 +128,8 @@ struct Partition {
   uint32_t a_sms = 0, b_sms = 0;
 };
 
+static void free_partition(Partition* p);
+
 static int make_partition(int device, uint32_t sms, Partition* p) {
   Drv* d = drv();
   if (!d->ok) return fail(LK_E_INIT, "green-context driver entry points unavailable");
@@ -148,7 +150,10 @@ static int make_partition(int device, uint32_t sms, Partition* p) {
     if (r == CUDA_SUCCESS) r = d->GreenCtxCreate(&p->gb, db, dev, CU_GREEN_CTX_DEFAULT_STREAM);
     if (r == CUDA_SUCCESS) r = d->CtxFromGreenCtx(&p->cb, p->gb);
   }
-  if (r != CUDA_SUCCESS) return fail(LK_E_INIT, "green context creation failed (driver error %d)", int(r));
+  if (r != CUDA_SUCCESS) {
+    free_partition(p);
+    return fail(LK_E_INIT, "green context creation failed (driver error %d)", int(r));
+  }
   p->a_sms = part.sm.smCount;
   p->b_sms = rest.sm.smCount;
   return LK_OK;
@@ -166,11 +171,13 @@ static void free_partition(Partition* p) {
 // device-wide sync (cudaDeviceSynchronize, cudaFree, cudaMemset) would block
 // forever.  Stream-ordered allocation on a private non-blocking stream does not.
 static std::mutex g_svc_mu;
-static cudaStream_t g_svc[64];
+static constexpr int kMaxDevices = 64;
+static cudaStream_t g_svc[kMaxDevices];
 
 static cudaStream_t svc_stream() {
   int dev = 0;
   cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return nullptr;   // create() refuses such devices first
   std::lock_guard<std::mutex> g(g_svc_mu);
   if (!g_svc[dev]) {
     cudaStreamCreateWithFlags(&g_svc[dev], cudaStreamNonBlocking);
@@ -465,17 +472,17 @@ void lk_session::release_claim() {
     claimed = false;
   }
 }
-static uint8_t g_claimed[64];
+static uint8_t g_claimed[kMaxDevices];
 
 static bool claim_device(int dev) {
   std::lock_guard<std::mutex> g(g_claim_mu);
-  if (dev < 0 || dev >= 64 || g_claimed[dev]) return false;
+  if (dev < 0 || dev >= kMaxDevices || g_claimed[dev]) return false;
   g_claimed[dev] = 1;
   return true;
 }
 static void release_device(int dev) {
   std::lock_guard<std::mutex> g(g_claim_mu);
-  if (dev >= 0 && dev < 64) g_claimed[dev] = 0;
+  if (dev >= 0 && dev < kMaxDevices) g_claimed[dev] = 0;
 }
 
 // ------------------------------------------------------------------ create
@@ -516,6 +523,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   int ndev = 0;
   LK_CUDA(cudaGetDeviceCount(&ndev));
   if (cfg.device < 0 || cfg.device >= ndev) return fail(LK_E_CONFIG, "no CUDA device %d", cfg.device);
+  if (cfg.device >= kMaxDevices) return fail(LK_E_CONFIG, "device %d beyond the %d supported", cfg.device, kMaxDevices);
   LK_CUDA(cudaSetDevice(cfg.device));
   cudaDeviceProp prop;
   LK_CUDA(cudaGetDeviceProperties(&prop, cfg.device));
@@ -722,15 +730,35 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (ce != cudaSuccess) return cleanup(fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(ce)));
 
   // --- boot: every worker publishes INIT then NOP (native.py:113-118)
+  // A failed boot frees the session only once the kernel has retired (the
+  // surviving workers are told EXIT first); a kernel that stays resident can
+  // still touch the mailboxes, so then everything, the device claim included,
+  // is deliberately leaked.
+  auto boot_failed = [&](int rc) {
+    if (kernel_status(s) == 0) {
+      s->post(s->all_ids, LK_EXIT);
+      const uint64_t until = now_ns() + std::min<uint64_t>(cfg.wait_timeout_ns, 2000000000ull);
+      while (kernel_status(s) == 0 && now_ns() < until) usleep(50);
+      if (kernel_status(s) == 0) return rc;
+    }
+    return cleanup(rc);
+  };
   const uint64_t deadline = now_ns() + cfg.wait_timeout_ns;
   for (uint32_t i = 0; i < s->nw;) {
     if (s->word(i) == LK_NOP && s->phase(i) == LK_PHASE_IDLE) { ++i; continue; }
-    if (s->err[i]) return cleanup(fail(LK_E_INIT, "worker %u failed during boot", i));
+    if (s->err[i]) {
+      const int rc = fail(LK_E_INIT, "worker %u failed during boot", i);
+      const std::string msg = g_last_error;
+      boot_failed(rc);
+      g_last_error = msg;
+      return rc;
+    }
     if (now_ns() > deadline) {
-      // the kernel may still run: leak rather than free memory it can touch
-      const int ks = kernel_status(s);
-      if (ks == 0) return fail(LK_E_INIT, "workers failed to reach idle (worker %u)", i);
-      return cleanup(fail(LK_E_INIT, "workers failed to reach idle (worker %u)", i));
+      const int rc = fail(LK_E_INIT, "workers failed to reach idle (worker %u)", i);
+      const std::string msg = g_last_error;
+      boot_failed(rc);
+      g_last_error = msg;
+      return rc;
     }
     LK_PAUSE();
   }
@@ -1166,7 +1194,11 @@ extern "C" int lk_clock_offset(int device, uint32_t rounds, int64_t* offset_ns, 
   cudaStream_t st;
   LK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   cudaError_t ce = lk_launch_clocksync(flag, const_cast<unsigned long long*>(echo), rounds, st);
-  if (ce != cudaSuccess) return fail(LK_E_CUDA, "clocksync launch: %s", cudaGetErrorString(ce));
+  if (ce != cudaSuccess) {
+    cudaStreamDestroy(st);
+    cudaFreeHost(cells);
+    return fail(LK_E_CUDA, "clocksync launch: %s", cudaGetErrorString(ce));
+  }
   uint64_t best = ~0ull;
   int64_t off = 0;
   for (uint32_t r = 1; r <= rounds; ++r) {

@@ -44,11 +44,6 @@ __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -80,11 +75,6 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu32(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_relaxed_gpu64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ ulonglong2 ld_relaxed_sys_v2(const unsigned long long* p) {
-  ulonglong2 v;
-  asm volatile("ld.relaxed.sys.global.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
-  return v;
 }
 // Named barrier 1 over the T worker threads of the CTA (the gateway warp of
 // CTA 0 never joins it).
@@ -928,7 +918,7 @@ __device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Ele
 // posted back to the host (ring flow control).  Exits once every worker has
 // left its loop.
 constexpr uint32_t kRingMaskBits = 48;
-constexpr uint32_t kRingMaxWorkers = 4 * kRingMaskBits;   // 192
+static_assert(4 * kRingMaskBits >= 148, "event masks cover every SM of a B200");   // host: <= 192 workers
 
 template <int K>
 __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
