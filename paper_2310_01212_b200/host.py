@@ -42,6 +42,77 @@ class PhaseTiming:
             raise ValueError(f"{self.phase} timing needs a nonempty sm mask")
 
 
+_new = object.__new__
+
+
+def _materialize(row: tuple) -> PhaseTiming:
+    t = _new(PhaseTiming)
+    d = t.__dict__
+    d["phase"], d["cycles"], d["sm_mask"] = row
+    return t
+
+
+class TimingLog:
+    """``session.timings``: the reference's ``list[PhaseTiming]``
+    (P/native.py:99) as a sequence of PhaseTiming values.
+
+    Rows are kept as plain (phase, cycles, sm_mask) tuples, which the garbage
+    collector stops tracking after its first pass; a list of a million
+    dataclass instances (plus their ``__dict__``s) is re-traversed by every
+    older-generation collection, which cost more than the dispatch itself in
+    long trigger/wait loops (tools/py_overhead.py).  Reading an entry builds
+    an equal PhaseTiming."""
+
+    __slots__ = ("_rows",)
+
+    def __init__(self, items: Iterable[PhaseTiming] = ()) -> None:
+        self._rows: list[tuple] = [(t.phase, t.cycles, t.sm_mask) for t in items]
+
+    def append(self, t: PhaseTiming) -> None:
+        self._rows.append((t.phase, t.cycles, t.sm_mask))
+
+    def extend(self, items: Iterable[PhaseTiming]) -> None:
+        for t in items:
+            self.append(t)
+
+    def clear(self) -> None:
+        self._rows.clear()
+
+    def pop(self, i: int = -1) -> PhaseTiming:
+        return _materialize(self._rows.pop(i))
+
+    def __len__(self) -> int:
+        return len(self._rows)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [_materialize(r) for r in self._rows[i]]
+        return _materialize(self._rows[i])
+
+    def __iter__(self):
+        for r in self._rows:
+            yield _materialize(r)
+
+    def __reversed__(self):
+        for r in reversed(self._rows):
+            yield _materialize(r)
+
+    def __contains__(self, t) -> bool:
+        return isinstance(t, PhaseTiming) and (t.phase, t.cycles, t.sm_mask) in self._rows
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, TimingLog):
+            return self._rows == other._rows
+        if isinstance(other, (list, tuple)):
+            return list(self) == list(other)
+        return NotImplemented
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return repr(list(self))
+
+
 def full_mask(num_sms: int) -> int:
     return (1 << num_sms) - 1
 

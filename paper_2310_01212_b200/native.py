@@ -27,7 +27,7 @@ from . import _lib, protocol
 from .device import WorkDescriptor, as_work
 from .errors import HangDetected, UsageError
 from .host import (PHASE_COPYIN, PHASE_COPYOUT, PHASE_DISPOSE, PHASE_INIT, PHASE_LAUNCH,
-                   PHASE_TRIGGER, PHASE_WAIT, PhaseTiming, _check_mask, full_mask, sms_in_mask)
+                   PHASE_TRIGGER, PHASE_WAIT, PhaseTiming, TimingLog, _check_mask, full_mask, sms_in_mask)
 
 log = logging.getLogger(__name__)
 
@@ -178,7 +178,7 @@ class NativeSession:
         self.num_workers = num_workers
         self.nwords = (num_workers + 63) // 64
         self.disposed = False
-        self.timings: list[PhaseTiming] = []
+        self.timings = TimingLog()   # a list[PhaseTiming] (host.TimingLog)
         self.descriptors: dict[int, WorkDescriptor] = {}
         self._staged: dict[int, tuple] = {}
         self._threads = [_WorkerHandle(self, i) for i in range(num_workers)]
@@ -305,46 +305,68 @@ class NativeSession:
         rc = self._lib.lk_register_desc(self._h, work.slot, C.byref(d), self._mask(key), self.nwords)
         _lib.check(rc)
         self.descriptors[work.slot] = work
-        self._staged[work.slot] = (work, key)
+        self._staged[work.slot] = (work, key, work.multi_worker)
         return time.perf_counter_ns() - t0
 
+    # trigger and wait are the per-task hot path: the helpers (_check, _mask,
+    # _is_staged, _timing) are inlined, which halves the wrapper's cost over
+    # the bare ctypes calls (tools/py_overhead.py).  Semantics are the helpers'.
     def trigger(self, mask: int, work: WorkDescriptor) -> PhaseTiming:
         """Dispatch: one word write per masked worker, no kernel launch."""
-        self._require_live()
-        self._check(mask)
-        work = as_work(work)
-        key = mask if work.multi_worker else 0
-        if self._is_staged(work, key):
+        if self.disposed:
+            raise UsageError("session already disposed")
+        if mask <= 0 or mask >> self.num_workers:
+            _check_mask(mask, self.num_workers)   # raises with the reference's message
+        if type(work) is not WorkDescriptor:
+            work = as_work(work)
+        slot = work.slot
+        # identity, not dataclass equality: two descriptors with equal fields
+        # may point at different buffers (their refs are compare=False)
+        st = self._staged.get(slot)
+        if st is not None and st[0] is work and st[1] == (mask if st[2] else 0):
             d = None   # this descriptor object is already staged for this worker set
         else:
             d = C.byref(work.to_c())
-        trig = self._raw_trigger if work.slot <= 0x7FFFFFFF else self._lib.lk_trigger   # raw: C int args
-        rc = trig(self._h, self._mask(mask), self.nwords, work.slot, d, self._u64_ref)
+        b = self._mask_cache.get(mask)
+        if b is None:
+            b = self._mask(mask)
+        trig = self._raw_trigger if slot <= 0x7FFFFFFF else self._lib.lk_trigger   # raw: C int args
+        rc = trig(self._h, b, self.nwords, slot, d, self._u64_ref)
         if rc:
             _lib.raise_for(rc)
         if d is not None:
-            self.descriptors[work.slot] = work
-            self._staged[work.slot] = (work, key)
-        timing = _timing(PHASE_TRIGGER, self._u64.value, mask)
-        self.timings.append(timing)
-        return timing
+            multi = work.multi_worker
+            self.descriptors[slot] = work
+            self._staged[slot] = (work, mask if multi else 0, multi)
+        row = (PHASE_TRIGGER, self._u64.value, mask)
+        self.timings._rows.append(row)
+        t = _new(PhaseTiming)
+        td = t.__dict__
+        td["phase"], td["cycles"], td["sm_mask"] = row
+        return t
 
     def _is_staged(self, work: WorkDescriptor, key: int) -> bool:
-        # identity, not dataclass equality: two descriptors with equal fields
-        # may point at different buffers (their refs are compare=False)
         st = self._staged.get(work.slot)
         return st is not None and st[0] is work and st[1] == key
 
     def wait(self, mask: int) -> PhaseTiming:
         """Spin (in C) until every masked worker published FINISHED, then ack."""
-        self._require_live()
-        self._check(mask)
-        rc = self._raw_wait(self._h, self._mask(mask), self.nwords, self._u64_ref)
+        if self.disposed:
+            raise UsageError("session already disposed")
+        if mask <= 0 or mask >> self.num_workers:
+            _check_mask(mask, self.num_workers)
+        b = self._mask_cache.get(mask)
+        if b is None:
+            b = self._mask(mask)
+        rc = self._raw_wait(self._h, b, self.nwords, self._u64_ref)
         if rc:
             _lib.raise_for(rc, sm_ids=tuple(sms_in_mask(mask)))
-        timing = _timing(PHASE_WAIT, self._u64.value, mask)
-        self.timings.append(timing)
-        return timing
+        row = (PHASE_WAIT, self._u64.value, mask)
+        self.timings._rows.append(row)
+        t = _new(PhaseTiming)
+        td = t.__dict__
+        td["phase"], td["cycles"], td["sm_mask"] = row
+        return t
 
     def _spin_until(self, cond, what: str, sm_ids) -> int:
         """Python-level poll helper with the reference's timeout contract."""
@@ -500,7 +522,7 @@ class LaunchSyncBaseline:
                 _lib.check(self._lib.lk_sm_count(device, C.byref(n)))
                 grid = n.value
         self.grid = grid
-        self.timings: list[PhaseTiming] = []
+        self.timings = TimingLog()   # a list[PhaseTiming] (host.TimingLog)
         self._u64 = C.c_uint64()
         self._inflight = False
 

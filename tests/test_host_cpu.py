@@ -239,3 +239,24 @@ def test_recorded_b200_trace_validates_with_reference_cli(reference, tmp_path):
     f = tmp_path / "b200.trace"
     f.write_text(text)
     assert ref_cli.main(["validate", str(f)]) == 0
+
+
+def test_timing_log_is_a_list_of_phase_timings():
+    import gc
+    log = host.TimingLog()
+    a = host.PhaseTiming(host.PHASE_TRIGGER, 5, 0b11)
+    b = host.PhaseTiming(host.PHASE_WAIT, 9, 0b11)
+    log.append(a)
+    log.extend([b])
+    assert len(log) == 2 and log == [a, b] and list(log) == [a, b]
+    assert log[0] == a and log[-1] == b and log[:1] == [a] and a in log
+    assert [t.cycles for t in log if t.phase == host.PHASE_WAIT] == [9]
+    assert isinstance(log[1], host.PhaseTiming) and hash(log[1]) == hash(b)
+    assert list(reversed(log)) == [b, a] and repr(log) == repr([a, b])
+    assert log.pop() == b and log == [a]
+    log.clear()
+    assert not log and log == []
+    # rows are untracked by the collector once it has seen them
+    log.append(a)
+    gc.collect()
+    assert not gc.is_tracked(log._rows[0])
