@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import sysconfig
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -21,6 +22,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]
 
 SOURCES = ["lk_kernels.cu", "lk_host.cu", "lk_validate.cpp"]
+# CPython fast path for trigger/wait (csrc/lk_pyfast.c); binds liblk.so's
+# entry points at run time, so it links no CUDA library
+PYFAST = PKG / ("_lkfast" + sysconfig.get_config_var("EXT_SUFFIX"))
 HEADERS = ["lk_internal.h", "lk_protocol.cuh"]
 
 
@@ -32,7 +36,23 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+def build_pyfast(force: bool = False, verbose: bool = False) -> Path:
+    src = CSRC / "lk_pyfast.c"
+    if not force and PYFAST.exists() and PYFAST.stat().st_mtime > max(src.stat().st_mtime,
+                                                                       Path(__file__).stat().st_mtime):
+        return PYFAST
+    tmp = PYFAST.with_suffix(".tmp")
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall", "-Werror",
+           "-I", sysconfig.get_paths()["include"], str(src), "-o", str(tmp)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, PYFAST)
+    return PYFAST
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_pyfast(force, verbose)
     if not force and not _stale():
         return LIB
     objdir = PKG / "build"

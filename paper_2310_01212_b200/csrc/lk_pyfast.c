@@ -1,0 +1,232 @@
+/* lk_pyfast.c -- CPython fast path for NativeSession.trigger / wait.
+ *
+ * The per-task cost of the Python API is the wrapper, not the C ABI: a bare
+ * ctypes trigger+wait pair costs ~0.3 us over the C loop, the Python methods
+ * around it another ~0.7 us (tools/py_overhead.py).  This module performs the
+ * common case of NativeSession.trigger / wait (native.py) in C and calls
+ * lk_trigger / lk_wait (include/lk.h) directly:
+ *   - a mask already validated and cached as its u64 words,
+ *   - a WorkDescriptor object already staged in its slot for this worker set,
+ *   - the timing row appended to session.timings (host.TimingLog rows), and
+ *     an equal PhaseTiming returned.
+ * Anything else returns None and native.py takes its Python path, which
+ * holds the full rules (validation messages, staging, foreign descriptors).
+ * A failing C call returns its LK_E_* code (an int) for native.py to raise.
+ *
+ * The two entry points are passed in as addresses taken from the ctypes
+ * handle of liblk.so, so this module and ctypes share one loaded library
+ * (one set of session claims and one thread-local last error).
+ */
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <stdint.h>
+
+typedef int (*trigger_fn)(void*, const uint64_t*, uint32_t, uint32_t, const void*, uint64_t*);
+typedef int (*wait_fn)(void*, const uint64_t*, uint32_t, uint64_t*);
+
+typedef struct {
+  PyObject_HEAD
+  void* h;
+  uint32_t nwords;
+  trigger_fn trig;
+  wait_fn wait;
+  PyObject* staged;      /* dict slot -> (work, key, multi) */
+  PyObject* mask_cache;  /* dict mask -> bytes (8 * nwords) */
+  PyObject* rows;        /* list of (phase, ns, mask) */
+  PyObject* limit;       /* 1 << num_workers */
+  PyTypeObject* timing_type;
+  PyTypeObject* work_type;
+  PyObject* ph_trigger;
+  PyObject* ph_wait;
+} Fast;
+
+static PyObject* g_zero;
+static PyObject* g_empty;
+static PyObject *s_slot, *s_phase, *s_cycles, *s_sm_mask;
+
+static void fast_dealloc(Fast* f) {
+  Py_XDECREF(f->staged);
+  Py_XDECREF(f->mask_cache);
+  Py_XDECREF(f->rows);
+  Py_XDECREF(f->limit);
+  Py_XDECREF(f->timing_type);
+  Py_XDECREF(f->work_type);
+  Py_XDECREF(f->ph_trigger);
+  Py_XDECREF(f->ph_wait);
+  Py_TYPE(f)->tp_free((PyObject*)f);
+}
+
+static int fast_init(Fast* f, PyObject* args, PyObject* kw) {
+  unsigned long long h, trig, wt;
+  unsigned int nwords;
+  PyObject *staged, *cache, *rows, *limit, *tt, *wtp, *pt, *pw;
+  (void)kw;
+  if (!PyArg_ParseTuple(args, "KIKKO!O!O!O!O!O!UU", &h, &nwords, &trig, &wt, &PyDict_Type, &staged,
+                        &PyDict_Type, &cache, &PyList_Type, &rows, &PyLong_Type, &limit, &PyType_Type, &tt,
+                        &PyType_Type, &wtp, &pt, &pw))
+    return -1;
+  if (!h || !trig || !wt || nwords == 0) {
+    PyErr_SetString(PyExc_ValueError, "null handle or entry point");
+    return -1;
+  }
+  f->h = (void*)(uintptr_t)h;
+  f->nwords = nwords;
+  f->trig = (trigger_fn)(uintptr_t)trig;
+  f->wait = (wait_fn)(uintptr_t)wt;
+  Py_INCREF(staged); Py_XSETREF(f->staged, staged);
+  Py_INCREF(cache); Py_XSETREF(f->mask_cache, cache);
+  Py_INCREF(rows); Py_XSETREF(f->rows, rows);
+  Py_INCREF(limit); Py_XSETREF(f->limit, limit);
+  Py_INCREF(tt); Py_XSETREF(f->timing_type, (PyTypeObject*)tt);
+  Py_INCREF(wtp); Py_XSETREF(f->work_type, (PyTypeObject*)wtp);
+  Py_INCREF(pt); Py_XSETREF(f->ph_trigger, pt);
+  Py_INCREF(pw); Py_XSETREF(f->ph_wait, pw);
+  return 0;
+}
+
+/* The cached u64 words of a valid mask (0 < mask < 1 << num_workers), or NULL
+ * (no exception set) when the Python path must handle it. */
+static const uint64_t* mask_words(Fast* f, PyObject* mask) {
+  if (!PyLong_CheckExact(mask)) return NULL;
+  PyObject* b = PyDict_GetItemWithError(f->mask_cache, mask);   /* borrowed */
+  if (!b) {
+    PyErr_Clear();
+    return NULL;
+  }
+  if (!PyBytes_CheckExact(b) || PyBytes_GET_SIZE(b) != (Py_ssize_t)(8 * f->nwords)) return NULL;
+  int gt = PyObject_RichCompareBool(mask, g_zero, Py_GT);
+  int lt = gt == 1 ? PyObject_RichCompareBool(mask, f->limit, Py_LT) : 0;
+  if (gt != 1 || lt != 1) {
+    PyErr_Clear();
+    return NULL;
+  }
+  return (const uint64_t*)PyBytes_AS_STRING(b);
+}
+
+/* Append (phase, ns, mask) to the timing rows and return an equal PhaseTiming
+ * built like object.__new__ + __dict__ fill (host._materialize). */
+static PyObject* record(Fast* f, PyObject* phase, uint64_t ns, PyObject* mask) {
+  PyObject* cyc = PyLong_FromUnsignedLongLong(ns);
+  if (!cyc) return NULL;
+  PyObject* row = PyTuple_Pack(3, phase, cyc, mask);
+  if (!row) {
+    Py_DECREF(cyc);
+    return NULL;
+  }
+  int rc = PyList_Append(f->rows, row);
+  Py_DECREF(row);
+  if (rc) {
+    Py_DECREF(cyc);
+    return NULL;
+  }
+  PyObject* t = PyBaseObject_Type.tp_new(f->timing_type, g_empty, NULL);
+  if (!t) {
+    Py_DECREF(cyc);
+    return NULL;
+  }
+  PyObject* d = PyObject_GenericGetDict(t, NULL);
+  if (!d || PyDict_SetItem(d, s_phase, phase) || PyDict_SetItem(d, s_cycles, cyc) ||
+      PyDict_SetItem(d, s_sm_mask, mask)) {
+    Py_XDECREF(d);
+    Py_DECREF(cyc);
+    Py_DECREF(t);
+    return NULL;
+  }
+  Py_DECREF(d);
+  Py_DECREF(cyc);
+  return t;
+}
+
+static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 2) {
+    PyErr_SetString(PyExc_TypeError, "trigger(mask, work)");
+    return NULL;
+  }
+  PyObject *mask = args[0], *work = args[1];
+  if (Py_TYPE(work) != f->work_type) Py_RETURN_NONE;
+  const uint64_t* m = mask_words(f, mask);
+  if (!m) Py_RETURN_NONE;
+  PyObject* slot = PyObject_GetAttr(work, s_slot);
+  if (!slot) return NULL;
+  PyObject* st = PyDict_GetItemWithError(f->staged, slot);   /* borrowed */
+  unsigned long sl = PyLong_Check(slot) ? PyLong_AsUnsignedLong(slot) : (unsigned long)-1;
+  Py_DECREF(slot);
+  if (PyErr_Occurred()) {
+    PyErr_Clear();
+    Py_RETURN_NONE;
+  }
+  if (!st || !PyTuple_CheckExact(st) || PyTuple_GET_SIZE(st) != 3 || PyTuple_GET_ITEM(st, 0) != work ||
+      sl > 0xFFFFFFFFul)
+    Py_RETURN_NONE;
+  /* staged for this worker set: key is the mask for payload kinds, else 0 */
+  PyObject* key = PyObject_IsTrue(PyTuple_GET_ITEM(st, 2)) == 1 ? mask : g_zero;
+  int same = PyObject_RichCompareBool(PyTuple_GET_ITEM(st, 1), key, Py_EQ);
+  if (same != 1) {
+    PyErr_Clear();
+    Py_RETURN_NONE;
+  }
+  uint64_t ns = 0;
+  int rc;
+  Py_BEGIN_ALLOW_THREADS
+  rc = f->trig(f->h, m, f->nwords, (uint32_t)sl, NULL, &ns);
+  Py_END_ALLOW_THREADS
+  if (rc) return PyLong_FromLong(rc);
+  return record(f, f->ph_trigger, ns, mask);
+}
+
+static PyObject* fast_wait(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 1) {
+    PyErr_SetString(PyExc_TypeError, "wait(mask)");
+    return NULL;
+  }
+  PyObject* mask = args[0];
+  const uint64_t* m = mask_words(f, mask);
+  if (!m) Py_RETURN_NONE;
+  uint64_t ns = 0;
+  int rc;
+  Py_BEGIN_ALLOW_THREADS
+  rc = f->wait(f->h, m, f->nwords, &ns);
+  Py_END_ALLOW_THREADS
+  if (rc) return PyLong_FromLong(rc);
+  return record(f, f->ph_wait, ns, mask);
+}
+
+static PyMethodDef fast_methods[] = {
+    {"trigger", (PyCFunction)(void (*)(void))fast_trigger, METH_FASTCALL, "trigger(mask, work)"},
+    {"wait", (PyCFunction)(void (*)(void))fast_wait, METH_FASTCALL, "wait(mask)"},
+    {NULL, NULL, 0, NULL}};
+
+static PyTypeObject FastType = {
+    PyVarObject_HEAD_INIT(NULL, 0).tp_name = "paper_2310_01212_b200._lkfast.Fast",
+    .tp_basicsize = sizeof(Fast),
+    .tp_flags = Py_TPFLAGS_DEFAULT,
+    .tp_new = PyType_GenericNew,
+    .tp_init = (initproc)fast_init,
+    .tp_dealloc = (destructor)fast_dealloc,
+    .tp_methods = fast_methods,
+    .tp_doc = "Fast(handle, nwords, lk_trigger, lk_wait, staged, mask_cache, rows, limit, PhaseTiming, "
+              "WorkDescriptor, phase_trigger, phase_wait)",
+};
+
+static struct PyModuleDef moddef = {PyModuleDef_HEAD_INIT, "_lkfast", "CPython fast path for trigger/wait", -1,
+                                    NULL, NULL, NULL, NULL, NULL};
+
+PyMODINIT_FUNC PyInit__lkfast(void) {
+  if (PyType_Ready(&FastType) < 0) return NULL;
+  g_zero = PyLong_FromLong(0);
+  g_empty = PyTuple_New(0);
+  s_slot = PyUnicode_InternFromString("slot");
+  s_phase = PyUnicode_InternFromString("phase");
+  s_cycles = PyUnicode_InternFromString("cycles");
+  s_sm_mask = PyUnicode_InternFromString("sm_mask");
+  if (!g_zero || !g_empty || !s_slot || !s_phase || !s_cycles || !s_sm_mask) return NULL;
+  PyObject* m = PyModule_Create(&moddef);
+  if (!m) return NULL;
+  Py_INCREF(&FastType);
+  if (PyModule_AddObject(m, "Fast", (PyObject*)&FastType) < 0) {
+    Py_DECREF(&FastType);
+    Py_DECREF(m);
+    return NULL;
+  }
+  return m;
+}

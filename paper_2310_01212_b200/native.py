@@ -139,6 +139,21 @@ def _timing(phase: str, ns: int, mask: int) -> PhaseTiming:
 _new = object.__new__
 
 
+def _make_fast(session: "NativeSession", raw):
+    """The CPython fast path (csrc/lk_pyfast.c) bound to this session, or
+    None when the module was not built (the ctypes calls then serve every
+    call; both go to liblk.so)."""
+    try:
+        from . import _lkfast
+    except ImportError:
+        log.debug("_lkfast not built: trigger/wait use ctypes only")
+        return None
+    addr = lambda fn: C.cast(fn, C.c_void_p).value  # noqa: E731
+    return _lkfast.Fast(session._h.value, session.nwords, addr(raw.lk_trigger), addr(raw.lk_wait),
+                        session._staged, session._mask_cache, session._timings._rows,
+                        1 << session.num_workers, PhaseTiming, WorkDescriptor, PHASE_TRIGGER, PHASE_WAIT)
+
+
 def _warn_lazy_loading() -> None:
     """CUDA 12 loads kernel modules lazily on first launch, and a module load
     while the persistent kernel is resident can wait on it forever.  liblk.so
@@ -188,6 +203,8 @@ class NativeSession:
         self._cells = (C.c_uint32 * num_workers)()
         self._cells2 = (C.c_uint32 * num_workers)()
         self._cells3 = (C.c_uint32 * num_workers)()
+        self._raw = raw
+        self._fast = _make_fast(self, raw)
 
     # -- bring-up ----------------------------------------------------------
 
@@ -272,6 +289,19 @@ class NativeSession:
 
     # -- host side -----------------------------------------------------------
 
+    @property
+    def timings(self) -> TimingLog:
+        """Every PhaseTiming of this session, in order (a list, P/native.py:99)."""
+        return self._timings
+
+    @timings.setter
+    def timings(self, v) -> None:
+        # callers may rebind it (session.timings = []): keep the TimingLog
+        # type and point the C fast path at the new rows
+        self._timings = v if isinstance(v, TimingLog) else TimingLog(v)
+        if getattr(self, "_fast", None) is not None:
+            self._fast = _make_fast(self, self._raw)
+
     def _require_live(self) -> None:
         if self.disposed:
             raise UsageError("session already disposed")
@@ -313,6 +343,13 @@ class NativeSession:
     # the bare ctypes calls (tools/py_overhead.py).  Semantics are the helpers'.
     def trigger(self, mask: int, work: WorkDescriptor) -> PhaseTiming:
         """Dispatch: one word write per masked worker, no kernel launch."""
+        f = self._fast
+        if f is not None:   # staged descriptor, cached mask: all in C (csrc/lk_pyfast.c)
+            r = f.trigger(mask, work)
+            if r is not None:
+                if r.__class__ is PhaseTiming:
+                    return r
+                _lib.raise_for(r)
         if self.disposed:
             raise UsageError("session already disposed")
         if mask <= 0 or mask >> self.num_workers:
@@ -339,7 +376,7 @@ class NativeSession:
             self.descriptors[slot] = work
             self._staged[slot] = (work, mask if multi else 0, multi)
         row = (PHASE_TRIGGER, self._u64.value, mask)
-        self.timings._rows.append(row)
+        self._timings._rows.append(row)
         t = _new(PhaseTiming)
         td = t.__dict__
         td["phase"], td["cycles"], td["sm_mask"] = row
@@ -351,6 +388,13 @@ class NativeSession:
 
     def wait(self, mask: int) -> PhaseTiming:
         """Spin (in C) until every masked worker published FINISHED, then ack."""
+        f = self._fast
+        if f is not None:
+            r = f.wait(mask)
+            if r is not None:
+                if r.__class__ is PhaseTiming:
+                    return r
+                _lib.raise_for(r, sm_ids=tuple(sms_in_mask(mask)))
         if self.disposed:
             raise UsageError("session already disposed")
         if mask <= 0 or mask >> self.num_workers:
@@ -362,7 +406,7 @@ class NativeSession:
         if rc:
             _lib.raise_for(rc, sm_ids=tuple(sms_in_mask(mask)))
         row = (PHASE_WAIT, self._u64.value, mask)
-        self.timings._rows.append(row)
+        self._timings._rows.append(row)
         t = _new(PhaseTiming)
         td = t.__dict__
         td["phase"], td["cycles"], td["sm_mask"] = row
@@ -402,6 +446,7 @@ class NativeSession:
         rc = self._lib.lk_dispose(self._h, C.byref(self._u64))
         _lib.check(rc, sm_ids=tuple(range(self.num_workers)))
         self.disposed = True
+        self._fast = None
         timing = PhaseTiming(PHASE_DISPOSE, self._u64.value, full_mask(self.num_workers))
         self.timings.append(timing)
         return timing
@@ -409,11 +454,13 @@ class NativeSession:
     def abort(self, timeout_s: float = 10.0) -> None:
         """Retire the kernel whatever the host state (dead worker, pending work)."""
         if self._h:
+            self._fast = None
             _lib.check(self._lib.lk_abort(self._h, int(timeout_s * 1e9)))
             self.disposed = True
 
     def close(self) -> None:
         """Dispose (or abort) if needed and free the runtime's memory."""
+        self._fast = None
         if self._h:
             if not self.disposed:
                 try:

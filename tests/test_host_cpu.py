@@ -260,3 +260,100 @@ def test_timing_log_is_a_list_of_phase_timings():
     log.append(a)
     gc.collect()
     assert not gc.is_tracked(log._rows[0])
+
+
+_FAKE_LK = r"""
+#include <stdint.h>
+uint64_t last[4]; uint32_t last_slot, calls;
+int fake_trigger(void* h, const uint64_t* m, uint32_t nw, uint32_t slot, const void* d, uint64_t* ns) {
+  for (uint32_t k = 0; k < nw && k < 4; ++k) last[k] = m[k];
+  last_slot = slot; ++calls; *ns = 1000 + slot;
+  return (uintptr_t)h == 7 ? -4 : 0;
+}
+int fake_wait(void* h, const uint64_t* m, uint32_t nw, uint64_t* ns) {
+  for (uint32_t k = 0; k < nw && k < 4; ++k) last[k] = m[k];
+  ++calls; *ns = 77;
+  return (uintptr_t)h == 7 ? -4 : 0;
+}
+"""
+
+
+def _fake_session(tmp_path, handle=1):
+    """A NativeSession shell whose C entry points are fakes (no GPU): drives
+    the CPython fast path (csrc/lk_pyfast.c) and the Python path side by side."""
+    import ctypes as C
+    import shutil
+    import subprocess
+    from paper_2310_01212_b200 import native
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    src = tmp_path / "fake.c"
+    src.write_text(_FAKE_LK)
+    so = tmp_path / "libfake.so"
+    subprocess.run(["gcc", "-O1", "-shared", "-fPIC", str(src), "-o", str(so)], check=True)
+    lib = C.CDLL(str(so))
+    raw = type("Raw", (), {"lk_trigger": lib.fake_trigger, "lk_wait": lib.fake_wait})
+    s = native.NativeSession.__new__(native.NativeSession)
+    s.cfg = native.NativeConfig()
+    s._lib, s._raw = None, raw
+    s._raw_trigger, s._raw_wait = lib.fake_trigger, lib.fake_wait
+    s._h, s.num_workers, s.nwords, s.disposed = C.c_void_p(handle), 148, 3, False
+    s._fast = None
+    s.timings = host.TimingLog()
+    s.descriptors, s._staged, s._mask_cache = {}, {}, {}
+    s._u64 = C.c_uint64()
+    s._u64_ref = C.byref(s._u64)
+    s._fast = native._make_fast(s, raw)
+    assert s._fast is not None, "_lkfast extension not built"
+    return s, lib
+
+
+def test_pyfast_path_matches_python_path(tmp_path):
+    s, lib = _fake_session(tmp_path)
+    calls = C.c_uint32.in_dll(lib, "calls")
+    w = WorkDescriptor(slot=3, kind="empty")
+    s._staged[3] = (w, 0, False)
+    m = (1 << 130) | 1
+    # first use: mask not cached -> Python path (which caches it)
+    t1 = s.trigger(m, w)
+    assert t1 == host.PhaseTiming(host.PHASE_TRIGGER, 1003, m) and calls.value == 1
+    assert s._fast.trigger(m, w) == host.PhaseTiming(host.PHASE_TRIGGER, 1003, m)   # now the C path serves it
+    assert list((C.c_uint64 * 4).in_dll(lib, "last"))[:3] == [1, 0, 1 << 2]
+    assert s._fast.wait(m) == host.PhaseTiming(host.PHASE_WAIT, 77, m)
+    assert s.timings == [t1, t1, host.PhaseTiming(host.PHASE_WAIT, 77, m)]
+    assert isinstance(s.timings[-1], host.PhaseTiming)
+    # the C path declines what the Python path must handle
+    w2 = WorkDescriptor(slot=3, kind="empty")          # equal fields, different object: restage
+    assert s._fast.trigger(m, w2) is None
+    assert s._fast.trigger(m, object()) is None        # not a WorkDescriptor
+    s._mask_cache[0] = bytes(24)
+    s._mask_cache[1 << 148] = bytes(24)
+    assert s._fast.wait(0) is None                     # empty mask: the reference's error message
+    assert s._fast.wait(1 << 148) is None              # wider than the workers
+    assert s._fast.wait(True) is None                  # not an exact int
+    pay = WorkDescriptor(slot=4, kind="empty")
+    s._staged[4] = (pay, m, True)                      # payload staged for mask m only
+    assert s._fast.trigger(m, pay) is not None
+    s._mask(1)
+    assert s._fast.trigger(1, pay) is None             # another worker set: restage
+    # invalid masks still raise the reference's errors through the wrapper
+    with pytest.raises(errors.UsageError):
+        s.wait(0)
+    # rebinding timings keeps both paths appending to the new log
+    s.timings = []
+    s.wait(m)
+    assert len(s.timings) == 1 and s.timings[0].phase == host.PHASE_WAIT
+
+
+def test_pyfast_error_codes_raise(tmp_path):
+    from paper_2310_01212_b200.errors import HangDetected
+    s, _ = _fake_session(tmp_path, handle=7)          # fakes return LK_E_HANG (-4)
+    w = WorkDescriptor(slot=0, kind="empty")
+    s._staged[0] = (w, 0, False)
+    s._mask(1)
+    assert s._fast.trigger(1, w) == _lib.LK_E_HANG
+    with pytest.raises(HangDetected):
+        s.trigger(1, w)
+    with pytest.raises(HangDetected):
+        s.wait(1)
+    assert len(s.timings) == 0
