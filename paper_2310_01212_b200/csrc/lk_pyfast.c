@@ -158,9 +158,12 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
   if (!st || !PyTuple_CheckExact(st) || PyTuple_GET_SIZE(st) != 3 || PyTuple_GET_ITEM(st, 0) != work ||
       sl > 0xFFFFFFFFul)
     Py_RETURN_NONE;
-  /* staged for this worker set: key is the mask for payload kinds, else 0 */
+  /* staged for this worker set: key is the mask for payload kinds, else 0
+   * (the entry is held across the comparisons, which could run Python code) */
+  Py_INCREF(st);
   PyObject* key = PyObject_IsTrue(PyTuple_GET_ITEM(st, 2)) == 1 ? mask : g_zero;
   int same = PyObject_RichCompareBool(PyTuple_GET_ITEM(st, 1), key, Py_EQ);
+  Py_DECREF(st);
   if (same != 1) {
     PyErr_Clear();
     Py_RETURN_NONE;
