@@ -84,9 +84,11 @@ static int fast_init(Fast* f, PyObject* args, PyObject* kw) {
   return 0;
 }
 
-/* The cached u64 words of a valid mask (0 < mask < 1 << num_workers), or NULL
- * (no exception set) when the Python path must handle it. */
-static const uint64_t* mask_words(Fast* f, PyObject* mask) {
+/* The cached u64 words (a new reference to the bytes: another thread may
+ * clear the cache while the GIL is released) of a valid mask
+ * (0 < mask < 1 << num_workers), or NULL (no exception set) when the Python
+ * path must handle it. */
+static PyObject* mask_words(Fast* f, PyObject* mask) {
   if (!PyLong_CheckExact(mask)) return NULL;
   PyObject* b = PyDict_GetItemWithError(f->mask_cache, mask);   /* borrowed */
   if (!b) {
@@ -94,13 +96,15 @@ static const uint64_t* mask_words(Fast* f, PyObject* mask) {
     return NULL;
   }
   if (!PyBytes_CheckExact(b) || PyBytes_GET_SIZE(b) != (Py_ssize_t)(8 * f->nwords)) return NULL;
+  Py_INCREF(b);   /* the comparisons below could run Python code */
   int gt = PyObject_RichCompareBool(mask, g_zero, Py_GT);
   int lt = gt == 1 ? PyObject_RichCompareBool(mask, f->limit, Py_LT) : 0;
   if (gt != 1 || lt != 1) {
     PyErr_Clear();
+    Py_DECREF(b);
     return NULL;
   }
-  return (const uint64_t*)PyBytes_AS_STRING(b);
+  return b;
 }
 
 /* Append (phase, ns, mask) to the timing rows and return an equal PhaseTiming
@@ -144,20 +148,26 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
   }
   PyObject *mask = args[0], *work = args[1];
   if (Py_TYPE(work) != f->work_type) Py_RETURN_NONE;
-  const uint64_t* m = mask_words(f, mask);
-  if (!m) Py_RETURN_NONE;
+  PyObject* mb = mask_words(f, mask);
+  if (!mb) Py_RETURN_NONE;
   PyObject* slot = PyObject_GetAttr(work, s_slot);
-  if (!slot) return NULL;
+  if (!slot) {
+    Py_DECREF(mb);
+    return NULL;
+  }
   PyObject* st = PyDict_GetItemWithError(f->staged, slot);   /* borrowed */
   unsigned long sl = PyLong_Check(slot) ? PyLong_AsUnsignedLong(slot) : (unsigned long)-1;
   Py_DECREF(slot);
   if (PyErr_Occurred()) {
     PyErr_Clear();
+    Py_DECREF(mb);
     Py_RETURN_NONE;
   }
   if (!st || !PyTuple_CheckExact(st) || PyTuple_GET_SIZE(st) != 3 || PyTuple_GET_ITEM(st, 0) != work ||
-      sl > 0xFFFFFFFFul)
+      sl > 0xFFFFFFFFul) {
+    Py_DECREF(mb);
     Py_RETURN_NONE;
+  }
   /* staged for this worker set: key is the mask for payload kinds, else 0
    * (the entry is held across the comparisons, which could run Python code) */
   Py_INCREF(st);
@@ -166,13 +176,16 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
   Py_DECREF(st);
   if (same != 1) {
     PyErr_Clear();
+    Py_DECREF(mb);
     Py_RETURN_NONE;
   }
+  const uint64_t* m = (const uint64_t*)PyBytes_AS_STRING(mb);
   uint64_t ns = 0;
   int rc;
   Py_BEGIN_ALLOW_THREADS
   rc = f->trig(f->h, m, f->nwords, (uint32_t)sl, NULL, &ns);
   Py_END_ALLOW_THREADS
+  Py_DECREF(mb);
   if (rc) return PyLong_FromLong(rc);
   return record(f, f->ph_trigger, ns, mask);
 }
@@ -183,13 +196,15 @@ static PyObject* fast_wait(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
     return NULL;
   }
   PyObject* mask = args[0];
-  const uint64_t* m = mask_words(f, mask);
-  if (!m) Py_RETURN_NONE;
+  PyObject* mb = mask_words(f, mask);
+  if (!mb) Py_RETURN_NONE;
+  const uint64_t* m = (const uint64_t*)PyBytes_AS_STRING(mb);
   uint64_t ns = 0;
   int rc;
   Py_BEGIN_ALLOW_THREADS
   rc = f->wait(f->h, m, f->nwords, &ns);
   Py_END_ALLOW_THREADS
+  Py_DECREF(mb);
   if (rc) return PyLong_FromLong(rc);
   return record(f, f->ph_wait, ns, mask);
 }
