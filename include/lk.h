@@ -117,7 +117,11 @@ typedef struct lk_config {
                                     context of >= N SMs (driver granularity: multiples of 8), one
                                     worker per partition SM; the remaining SMs form a second green
                                     context for ordinary kernels (lk_baseline_create_in) */
-  uint32_t reserved;
+  uint32_t ack_delay_ns;         /* DIRECT, 1 replica: after publishing FINISHED a worker waits this
+                                    long before it polls for the host's NOP ack.  A poll issued at
+                                    once is ordered behind FINISHED on the link, reaches host memory
+                                    before the host can have answered, and costs a wasted round
+                                    trip; 0 = 200 (LK_CF_NO_ACK_DELAY: poll at once) */
 } lk_config;
 
 /* How to_gpu words reach the workers.  DIRECT: every worker polls its own
@@ -144,6 +148,8 @@ typedef struct lk_config {
                                     whoever finishes first (default: fixed contiguous chunks; the pool
                                     measured neutral at 64 MiB and -11% at 16 MiB on an idle GPU, and is
                                     meant for SMs slowed unevenly by co-running work) */
+#define LK_CF_NO_ACK_DELAY 128u  /* DIRECT, 1 replica: poll for the ack right after FINISHED
+                                    (lk_config.ack_delay_ns) */
 #define LK_CF_LAZY_ACK      16u  /* lk_wait returns once the NOP ack is written; the next trigger or
                                     dispose touching that worker waits for its republished NOP */
 
@@ -257,10 +263,13 @@ int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks,
 /* Device-side spans of the last dispatch per worker (globaltimer ns):
  * begin (WORK observed) and end (work done, before FINISHED). */
 int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n);
-/* Device timeline of the last dispatch per worker, 8 words each (t[8*i+k]):
+/* Device timeline of the last dispatch per worker, 12 words each (t[12*i+k]):
  * globaltimer ns at k=0 to_gpu value seen, 1 work begin, 2 work end,
  * 3 FINISHED issued, 4 gateway forward (LK_CF_TIMELINE, else 0); clock64 at
- * 5 value seen, 6 work begin, 7 FINISHED issued. */
+ * 5 value seen, 6 work begin, 7 FINISHED issued.  The ack phase of an empty
+ * task on a DIRECT session with LK_CF_TIMELINE (else 0): 8 globaltimer at
+ * FINISHED issued, 9 globaltimer when the NOP ack was seen, 10 cell loads
+ * issued in between, 11 clock64 when the NOP ack was seen. */
 int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n);
 /* Host side of the same dispatches (CLOCK_MONOTONIC ns, t[3*i+k]): k=0
  * trigger call start, 1 WORK word written, 2 FINISHED observed by wait. */

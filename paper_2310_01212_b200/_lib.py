@@ -43,6 +43,7 @@ CF_TIMELINE = 8
 CF_LAZY_ACK = 16
 CF_ACK_WINDOW = 32
 CF_DYNAMIC_TILES = 64
+CF_NO_ACK_DELAY = 128
 POLL_DIRECT = 0
 POLL_GATEWAY = 1
 POLL_HYBRID = 2
@@ -95,7 +96,7 @@ class lk_config(C.Structure):
         ("status_stride", C.c_uint32),
         ("ring_stages", C.c_uint32),
         ("sm_partition", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("ack_delay_ns", C.c_uint32),
     ]
 
 

@@ -519,6 +519,8 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.num_slots == 0) cfg.num_slots = 1024;
   if (cfg.trace_capacity == 0) cfg.trace_capacity = 65536;
   if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
+  if (cfg.ack_delay_ns == 0) cfg.ack_delay_ns = 200;
+  if (cfg.ack_delay_ns > 100000) return fail(LK_E_CONFIG, "ack_delay_ns must be at most 100000");
 
   int ndev = 0;
   LK_CUDA(cudaGetDeviceCount(&ndev));
@@ -723,6 +725,12 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.poll_mode = cfg.poll_mode;
   a.use_tma = use_tma ? 1 : 0;
   a.ring_stages = cfg.ring_stages;
+  {
+    int khz = 0;   // SM clock: the delay is spun on clock64
+    if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, cfg.device) != cudaSuccess || khz <= 0) khz = 1965000;
+    a.ack_delay_cyc = (cfg.flags & LK_CF_NO_ACK_DELAY) ? 0u
+                                                      : uint32_t(uint64_t(cfg.ack_delay_ns) * uint64_t(khz) / 1000000ull);
+  }
   {
     CtxScope cs(s->part.ca);
     ce = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);

@@ -39,6 +39,7 @@ struct lk_dev_args {
   uint32_t poll_mode;              // LK_POLL_*
   uint32_t use_tma;                // payload tiles through the TMA bulk ring in dynamic smem
   uint32_t ring_stages;            // TMA ring depth (16-KiB stages)
+  uint32_t ack_delay_cyc;          // DIRECT, 1 replica: SM cycles between FINISHED and the first ack poll
   lk_dev_trace* trace;             // device, num_workers * trace_cap
   uint32_t* trace_cnt;             // device, num_workers
   uint32_t cell_u64;               // to_gpu cell stride in u64 (DIRECT cells and replicas)
@@ -60,7 +61,7 @@ cudaError_t lk_persistent_configure(size_t smem);
 cudaError_t lk_preload_kernels();
 cudaError_t lk_launch_clocksync(const uint32_t* flag, unsigned long long* echo, uint32_t rounds,
                                 cudaStream_t st);
-#define LK_TIMELINE_WORDS 8
+#define LK_TIMELINE_WORDS 12
 cudaError_t lk_launch_topo(uint32_t* smids, uint32_t grid, uint32_t cluster, size_t smem, cudaStream_t st);
 cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_per_sm);
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads,

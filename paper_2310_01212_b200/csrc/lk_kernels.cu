@@ -588,6 +588,7 @@ struct Elected {           // thread 0's private protocol state
   uint32_t hint;           // host hint bits of the current value (LK_HINT_*)
   uint32_t dseq, rseq;     // HYBRID: writes seen on the direct cell / via the event ring
   uint32_t tcnt;
+  uint32_t nload;          // LK_CF_TIMELINE, DIRECT: cell loads issued while awaiting the ack
   bool dirty;              // cur not yet stepped to a fixed point
   uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
   uint64_t c_seen;         // clock64 at the same point
@@ -682,11 +683,18 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
     e.dirty = false;
     unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
     tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
-    if (a.flags & LK_CF_TIMELINE) { tl[0] = e.t_seen; tl[4] = e.t_fwd; }
+    if (a.flags & LK_CF_TIMELINE) {
+      tl[0] = e.t_seen; tl[4] = e.t_fwd; tl[8] = globaltimer();
+      e.nload = 0;
+    }
     return kFastSettled;
   }
   if (e.st.phase == LK_PHASE_FINISHED && w == LK_NOP) {
     publish_fast(a, wid, LK_NOP, LK_PHASE_IDLE);
+    if (a.flags & LK_CF_TIMELINE) {
+      unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
+      tl[9] = e.t_seen; tl[10] = e.nload; tl[11] = e.c_seen;
+    }
     e.st.phase = LK_PHASE_IDLE;
     e.pub = LK_NOP;
     e.dirty = false;
@@ -738,6 +746,21 @@ __device__ __forceinline__ uint32_t settle(const lk_dev_args& a, uint32_t wid, E
   return LK_ACT_NONE;
 }
 
+// A worker that has just published FINISHED expects the host's NOP ack about
+// one link round trip later.  A cell load issued at once is ordered behind the
+// FINISHED store on the link (reads do not pass posted writes), so it samples
+// host memory the moment FINISHED lands -- before the host can have seen it
+// and answered -- and the ack waits a whole extra round trip for the next
+// load.  Waiting ack_delay_cyc (~200 ns: the host's detect-and-write time)
+// first makes that one load the one that sees the ack: the empty-task cycle
+// drops from 4.5 to 3.5 us (tools/ab_ack.py, tools/ack_breakdown.py).
+__device__ __forceinline__ void ack_delay(const lk_dev_args& a) {
+  if (!a.ack_delay_cyc) return;
+  const uint64_t c0 = clock64();
+  while (clock64() - c0 < a.ack_delay_cyc) {
+  }
+}
+
 // Spin until the state machine begins work or exits.  The to_gpu cell is K
 // replicas {word, seq} on separate 128-B lines; one ld.relaxed.sys per replica
 // is kept in flight, staggered by spacing_ns, so the host's write is sampled K
@@ -753,6 +776,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
   for (;;) {
     const uint32_t act = settle(a, wid, e);
     if (act != LK_ACT_NONE) return act;
+    if (K == 1 && e.st.phase == LK_PHASE_FINISHED) ack_delay(a);
     unsigned long long v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -767,10 +791,13 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
           if (f == kFastBegin) return LK_ACT_BEGIN;
           fresh = f == kFastNone;          // settled in place: keep polling
           if (fresh) break;
+          if (K == 1 && e.st.phase == LK_PHASE_FINISHED) ack_delay(a);
           v[k] = ld_cell(base + k * step, acquire);
+          if (timeline) ++e.nload;
           continue;
         }
         v[k] = ld_cell(base + k * step, acquire);
+        if (timeline) ++e.nload;
         if (K > 1) __nanosleep(a.spacing_ns);
         else if (a.backoff_ns) __nanosleep(a.backoff_ns);
       }
@@ -805,7 +832,9 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         const uint32_t f = fast_step(a, wid, e);
         if (f == kFastBegin) return LK_ACT_BEGIN;
         if (f == kFastNone) break;                  // general path
+        if (e.st.phase == LK_PHASE_FINISHED) ack_delay(a);
         v = ld_cell(cell, acquire);
+        if (timeline) ++e.nload;
         if (gap && e.st.phase == LK_PHASE_FINISHED) {
           const uint64_t c0 = clock64();
           while (clock64() - c0 < gap) {
@@ -816,6 +845,7 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         continue;
       }
       v = ld_cell(cell, acquire);
+      if (timeline) ++e.nload;
       if (a.backoff_ns) __nanosleep(a.backoff_ns);
     }
   }
@@ -1046,6 +1076,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.dseq = 0;
   e.rseq = 0;
   e.tcnt = 0;
+  e.nload = 0;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   e.t_seen = 0;
   e.c_seen = 0;

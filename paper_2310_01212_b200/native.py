@@ -74,6 +74,7 @@ class NativeConfig:
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
     ack_window: bool = False        # direct/1 replica: second load while awaiting the ack
     dynamic_tiles: bool = False     # payload maps: static 7/8 share + a pool claimed by early finishers
+    ack_delay_ns: int = 200         # direct/1 replica: first poll for the ack this long after FINISHED (0: at once)
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
 
@@ -88,6 +89,8 @@ class NativeConfig:
             raise UsageError("wait_timeout_s must be positive")
         if self.poll_mode not in POLL_MODES:
             raise UsageError(f"unknown poll mode {self.poll_mode!r}")
+        if not 0 <= self.ack_delay_ns <= 100_000:
+            raise UsageError("ack_delay_ns must be in [0, 100000]")
 
     def to_c(self) -> "_lib.lk_config":
         c = _lib.lk_config()
@@ -108,13 +111,15 @@ class NativeConfig:
         c.poll_spacing_ns = self.poll_spacing_ns
         c.poll_mode = POLL_MODES[self.poll_mode]
         c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
+        c.ack_delay_ns = self.ack_delay_ns
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)
                    | (_lib.CF_TIMELINE if self.timeline else 0)
                    | (_lib.CF_LAZY_ACK if self.lazy_ack else 0)
                    | (_lib.CF_ACK_WINDOW if self.ack_window else 0)
-                   | (_lib.CF_DYNAMIC_TILES if self.dynamic_tiles else 0))
+                   | (_lib.CF_DYNAMIC_TILES if self.dynamic_tiles else 0)
+                   | (0 if self.ack_delay_ns else _lib.CF_NO_ACK_DELAY))
         return c
 
 
@@ -523,7 +528,7 @@ class NativeSession:
         """(num_workers, 8) record of each worker's last dispatch: globaltimer ns
         at value seen, work begin, work end, FINISHED issued, gateway forward
         (timeline=True); clock64 at value seen, work begin, FINISHED issued."""
-        t = np.zeros((self.num_workers, 8), dtype=np.uint64)
+        t = np.zeros((self.num_workers, 12), dtype=np.uint64)
         _lib.check(self._lib.lk_last_timeline(self._h, t.ctypes.data, self.num_workers))
         return t
 

@@ -36,6 +36,9 @@ KNOBS = {
     "gateway-replicas4": dict(poll_mode="gateway", poll_replicas=4),
     "hybrid-replicas2": dict(poll_mode="hybrid", poll_replicas=2),
     "ack-window": dict(ack_window=True),
+    "no-ack-delay": dict(ack_delay_ns=0),
+    "ack-delay-1us": dict(ack_delay_ns=1000),
+    "ack-delay-replicas2": dict(ack_delay_ns=500, poll_replicas=2),   # the delay applies to 1 replica only
     "timeline": dict(timeline=True, poll_mode="gateway"),
     "pure-spin": dict(spin_strategy=native.PURE_SPIN),
     "stages2": dict(ring_stages=2),

@@ -357,3 +357,14 @@ def test_pyfast_error_codes_raise(tmp_path):
     with pytest.raises(HangDetected):
         s.wait(1)
     assert len(s.timings) == 0
+
+
+def test_ack_delay_config():
+    from paper_2310_01212_b200 import native
+    c = native.NativeConfig().to_c()
+    assert c.ack_delay_ns == 200 and not c.flags & _lib.CF_NO_ACK_DELAY
+    c = native.NativeConfig(ack_delay_ns=0).to_c()
+    assert c.flags & _lib.CF_NO_ACK_DELAY
+    for bad in (-1, 100_001):
+        with pytest.raises(errors.UsageError):
+            native.NativeConfig(ack_delay_ns=bad)
