@@ -122,6 +122,11 @@ typedef struct lk_config {
                                     once is ordered behind FINISHED on the link, reaches host memory
                                     before the host can have answered, and costs a wasted round
                                     trip; 0 = 200 (LK_CF_NO_ACK_DELAY: poll at once) */
+  uint32_t idle_delay_ns;        /* the same after publishing the NOP that ends a handshake, for a
+                                    host that re-triggers the same worker at once: set it to the
+                                    host's re-trigger time (~300 ns from a C loop, ~600 ns through
+                                    Python); a load that misses costs a round trip.  0 = none */
+  uint32_t reserved;
 } lk_config;
 
 /* How to_gpu words reach the workers.  DIRECT: every worker polls its own

@@ -97,6 +97,8 @@ class lk_config(C.Structure):
         ("ring_stages", C.c_uint32),
         ("sm_partition", C.c_uint32),
         ("ack_delay_ns", C.c_uint32),
+        ("idle_delay_ns", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 

@@ -520,7 +520,8 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.trace_capacity == 0) cfg.trace_capacity = 65536;
   if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
   if (cfg.ack_delay_ns == 0) cfg.ack_delay_ns = 200;
-  if (cfg.ack_delay_ns > 100000) return fail(LK_E_CONFIG, "ack_delay_ns must be at most 100000");
+  if (cfg.ack_delay_ns > 100000 || cfg.idle_delay_ns > 100000)
+    return fail(LK_E_CONFIG, "ack_delay_ns and idle_delay_ns must be at most 100000");
 
   int ndev = 0;
   LK_CUDA(cudaGetDeviceCount(&ndev));
@@ -728,8 +729,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   {
     int khz = 0;   // SM clock: the delay is spun on clock64
     if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, cfg.device) != cudaSuccess || khz <= 0) khz = 1965000;
-    a.ack_delay_cyc = (cfg.flags & LK_CF_NO_ACK_DELAY) ? 0u
-                                                      : uint32_t(uint64_t(cfg.ack_delay_ns) * uint64_t(khz) / 1000000ull);
+    const bool off = (cfg.flags & LK_CF_NO_ACK_DELAY) != 0;
+    a.ack_delay_cyc = off ? 0u : uint32_t(uint64_t(cfg.ack_delay_ns) * uint64_t(khz) / 1000000ull);
+    a.idle_delay_cyc = uint32_t(uint64_t(cfg.idle_delay_ns) * uint64_t(khz) / 1000000ull);
   }
   {
     CtxScope cs(s->part.ca);

@@ -590,6 +590,7 @@ struct Elected {           // thread 0's private protocol state
   uint32_t tcnt;
   uint32_t nload;          // LK_CF_TIMELINE, DIRECT: cell loads issued while awaiting the ack
   bool dirty;              // cur not yet stepped to a fixed point
+  bool idle_pub;           // just published NOP (ack consumed): the host may trigger this worker next
   uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
   uint64_t c_seen;         // clock64 at the same point
   uint64_t t_fwd;          // GATEWAY + LK_CF_TIMELINE: globaltimer when the gateway forwarded it
@@ -691,6 +692,7 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
   }
   if (e.st.phase == LK_PHASE_FINISHED && w == LK_NOP) {
     publish_fast(a, wid, LK_NOP, LK_PHASE_IDLE);
+    e.idle_pub = true;
     if (a.flags & LK_CF_TIMELINE) {
       unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
       tl[9] = e.t_seen; tl[10] = e.nload; tl[11] = e.c_seen;
@@ -753,11 +755,15 @@ __device__ __forceinline__ uint32_t settle(const lk_dev_args& a, uint32_t wid, E
 // and answered -- and the ack waits a whole extra round trip for the next
 // load.  Waiting ack_delay_cyc (~200 ns: the host's detect-and-write time)
 // first makes that one load the one that sees the ack: the empty-task cycle
-// drops from 4.5 to 3.5 us (tools/ab_ack.py, tools/ack_breakdown.py).
-__device__ __forceinline__ void ack_delay(const lk_dev_args& a) {
-  if (!a.ack_delay_cyc) return;
+// drops from 4.5 to 3.5 us (tools/ab_ack.py, tools/ack_breakdown.py).  The
+// NOP that closes a handshake can be answered the same way when the host
+// re-triggers the same worker at once: idle_delay_cyc (opt-in; the host's
+// re-trigger time, ~300 ns from C, ~600 ns from Python) before the next
+// load (tools/ab_idle.py).
+__device__ __forceinline__ void spin_cycles(uint32_t cyc) {
+  if (!cyc) return;
   const uint64_t c0 = clock64();
-  while (clock64() - c0 < a.ack_delay_cyc) {
+  while (clock64() - c0 < cyc) {
   }
 }
 
@@ -776,7 +782,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
   for (;;) {
     const uint32_t act = settle(a, wid, e);
     if (act != LK_ACT_NONE) return act;
-    if (K == 1 && e.st.phase == LK_PHASE_FINISHED) ack_delay(a);
+    if (K == 1 && e.st.phase == LK_PHASE_FINISHED) spin_cycles(a.ack_delay_cyc);
     unsigned long long v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -791,7 +797,11 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
           if (f == kFastBegin) return LK_ACT_BEGIN;
           fresh = f == kFastNone;          // settled in place: keep polling
           if (fresh) break;
-          if (K == 1 && e.st.phase == LK_PHASE_FINISHED) ack_delay(a);
+          if (K == 1) {
+            if (e.st.phase == LK_PHASE_FINISHED) spin_cycles(a.ack_delay_cyc);
+            else if (e.idle_pub) spin_cycles(a.idle_delay_cyc);
+          }
+          e.idle_pub = false;
           v[k] = ld_cell(base + k * step, acquire);
           if (timeline) ++e.nload;
           continue;
@@ -832,7 +842,9 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         const uint32_t f = fast_step(a, wid, e);
         if (f == kFastBegin) return LK_ACT_BEGIN;
         if (f == kFastNone) break;                  // general path
-        if (e.st.phase == LK_PHASE_FINISHED) ack_delay(a);
+        if (e.st.phase == LK_PHASE_FINISHED) spin_cycles(a.ack_delay_cyc);
+        else if (e.idle_pub) spin_cycles(a.idle_delay_cyc);
+        e.idle_pub = false;
         v = ld_cell(cell, acquire);
         if (timeline) ++e.nload;
         if (gap && e.st.phase == LK_PHASE_FINISHED) {
@@ -1077,6 +1089,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.rseq = 0;
   e.tcnt = 0;
   e.nload = 0;
+  e.idle_pub = false;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   e.t_seen = 0;
   e.c_seen = 0;

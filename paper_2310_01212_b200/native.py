@@ -75,6 +75,7 @@ class NativeConfig:
     ack_window: bool = False        # direct/1 replica: second load while awaiting the ack
     dynamic_tiles: bool = False     # payload maps: static 7/8 share + a pool claimed by early finishers
     ack_delay_ns: int = 200         # direct/1 replica: first poll for the ack this long after FINISHED (0: at once)
+    idle_delay_ns: int = 0          # opt-in: first poll for the next WORK this long after the closing NOP
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
 
@@ -89,8 +90,8 @@ class NativeConfig:
             raise UsageError("wait_timeout_s must be positive")
         if self.poll_mode not in POLL_MODES:
             raise UsageError(f"unknown poll mode {self.poll_mode!r}")
-        if not 0 <= self.ack_delay_ns <= 100_000:
-            raise UsageError("ack_delay_ns must be in [0, 100000]")
+        if not 0 <= self.ack_delay_ns <= 100_000 or not 0 <= self.idle_delay_ns <= 100_000:
+            raise UsageError("ack_delay_ns and idle_delay_ns must be in [0, 100000]")
 
     def to_c(self) -> "_lib.lk_config":
         c = _lib.lk_config()
@@ -112,6 +113,7 @@ class NativeConfig:
         c.poll_mode = POLL_MODES[self.poll_mode]
         c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
         c.ack_delay_ns = self.ack_delay_ns
+        c.idle_delay_ns = self.idle_delay_ns
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)

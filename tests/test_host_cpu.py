@@ -42,7 +42,7 @@ def test_abi_version_and_strerror_without_gpu():
 
 def test_struct_sizes_match_header():
     assert C.sizeof(_lib.lk_desc) == 64
-    assert C.sizeof(_lib.lk_config) == 80
+    assert C.sizeof(_lib.lk_config) == 88
     assert C.sizeof(_lib.lk_trace_rec) == 32
     fields = [f for f, _ in _lib.lk_config._fields_]
     body = re.sub(r"/\*.*?\*/", "", HEADER, flags=re.S)
@@ -363,8 +363,9 @@ def test_ack_delay_config():
     from paper_2310_01212_b200 import native
     c = native.NativeConfig().to_c()
     assert c.ack_delay_ns == 200 and not c.flags & _lib.CF_NO_ACK_DELAY
-    c = native.NativeConfig(ack_delay_ns=0).to_c()
-    assert c.flags & _lib.CF_NO_ACK_DELAY
+    assert c.idle_delay_ns == 0
+    c = native.NativeConfig(ack_delay_ns=0, idle_delay_ns=300).to_c()
+    assert c.flags & _lib.CF_NO_ACK_DELAY and c.idle_delay_ns == 300
     for bad in (-1, 100_001):
         with pytest.raises(errors.UsageError):
             native.NativeConfig(ack_delay_ns=bad)
