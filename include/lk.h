@@ -126,7 +126,10 @@ typedef struct lk_config {
                                     host that re-triggers the same worker at once: set it to the
                                     host's re-trigger time (~300 ns from a C loop, ~600 ns through
                                     Python); a load that misses costs a round trip.  0 = none */
-  uint32_t reserved;
+  uint32_t tma_min_workers;      /* payload dispatches to fewer workers use 128-bit LSU loads even
+                                    with the TMA ring on: a lone SM streams ~30% faster that way,
+                                    the whole GPU faster through the ring (tools/tma_vs_lsu_count.py);
+                                    0 = 49, 1 = always the ring */
 } lk_config;
 
 /* How to_gpu words reach the workers.  DIRECT: every worker polls its own

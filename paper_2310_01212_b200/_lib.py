@@ -98,7 +98,7 @@ class lk_config(C.Structure):
         ("sm_partition", C.c_uint32),
         ("ack_delay_ns", C.c_uint32),
         ("idle_delay_ns", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("tma_min_workers", C.c_uint32),
     ]
 
 

@@ -520,6 +520,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.trace_capacity == 0) cfg.trace_capacity = 65536;
   if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
   if (cfg.ack_delay_ns == 0) cfg.ack_delay_ns = 200;
+  if (cfg.tma_min_workers == 0) cfg.tma_min_workers = 49;
   if (cfg.ack_delay_ns > 100000 || cfg.idle_delay_ns > 100000)
     return fail(LK_E_CONFIG, "ack_delay_ns and idle_delay_ns must be at most 100000");
 
@@ -726,6 +727,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.poll_mode = cfg.poll_mode;
   a.use_tma = use_tma ? 1 : 0;
   a.ring_stages = cfg.ring_stages;
+  a.tma_min_workers = cfg.tma_min_workers;
   {
     int khz = 0;   // SM clock: the delay is spun on clock64
     if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, cfg.device) != cudaSuccess || khz <= 0) khz = 1965000;

@@ -41,6 +41,7 @@ struct lk_dev_args {
   uint32_t ring_stages;            // TMA ring depth (16-KiB stages)
   uint32_t ack_delay_cyc;          // DIRECT, 1 replica: SM cycles between FINISHED and the first ack poll
   uint32_t idle_delay_cyc;         // ... and between the handshake's closing NOP and the next poll
+  uint32_t tma_min_workers;        // payload dispatches to fewer workers take the LSU path
   lk_dev_trace* trace;             // device, num_workers * trace_cap
   uint32_t* trace_cnt;             // device, num_workers
   uint32_t cell_u64;               // to_gpu cell stride in u64 (DIRECT cells and replicas)

@@ -1163,8 +1163,11 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     wsync(T);
     if (sm.cmd == kCmdExit) break;
     const lk_desc d = sm.desc;
-    run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T, rp, g,
-              (a.flags & LK_CF_DYNAMIC_TILES) != 0);
+    // a narrow dispatch streams through 128-bit LSU loads: a lone SM moves
+    // ~110 GB/s that way against ~85 GB/s through the ring, which wins only
+    // once enough SMs share the dispatch to load HBM (tools/tma_vs_lsu_count.py)
+    run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T,
+              sm.count >= a.tma_min_workers ? rp : nullptr, g, (a.flags & LK_CF_DYNAMIC_TILES) != 0);
     wsync(T);
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();

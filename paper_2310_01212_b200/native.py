@@ -76,6 +76,7 @@ class NativeConfig:
     dynamic_tiles: bool = False     # payload maps: static 7/8 share + a pool claimed by early finishers
     ack_delay_ns: int = 200         # direct/1 replica: first poll for the ack this long after FINISHED (0: at once)
     idle_delay_ns: int = 0          # opt-in: first poll for the next WORK this long after the closing NOP
+    tma_min_workers: int = 49       # payload dispatches to fewer workers use LSU loads (1: always the ring)
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
 
@@ -92,6 +93,8 @@ class NativeConfig:
             raise UsageError(f"unknown poll mode {self.poll_mode!r}")
         if not 0 <= self.ack_delay_ns <= 100_000 or not 0 <= self.idle_delay_ns <= 100_000:
             raise UsageError("ack_delay_ns and idle_delay_ns must be in [0, 100000]")
+        if self.tma_min_workers < 1:
+            raise UsageError("tma_min_workers must be >= 1")
 
     def to_c(self) -> "_lib.lk_config":
         c = _lib.lk_config()
@@ -114,6 +117,7 @@ class NativeConfig:
         c.wait_timeout_ns = int(self.wait_timeout_s * 1e9)
         c.ack_delay_ns = self.ack_delay_ns
         c.idle_delay_ns = self.idle_delay_ns
+        c.tma_min_workers = self.tma_min_workers
         c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)

@@ -43,6 +43,7 @@ KNOBS = {
     "timeline": dict(timeline=True, poll_mode="gateway"),
     "pure-spin": dict(spin_strategy=native.PURE_SPIN),
     "stages2": dict(ring_stages=2),
+    "lsu-below-17": dict(tma_min_workers=17),      # NW=16: every dispatch on LSU loads
     "stages12-lsu": dict(ring_stages=12, tma_payload=False),
     "slots8": dict(num_slots=8),
 }
@@ -51,6 +52,7 @@ KNOBS = {
 @pytest.mark.parametrize("name", list(KNOBS))
 def test_knob_program(name):
     kw = dict(KNOBS[name])
+    kw.setdefault("tma_min_workers", 1)   # NW=16 workers: keep the ring path under test
     s, _ = native.NativeSession.start(native.NativeConfig(num_workers=NW, record_trace=True, trace_capacity=2048,
                                                           spin_yield_threshold=200, **kw))
     bufs = []
