@@ -121,7 +121,9 @@ typedef struct lk_config {
                                     long before it polls for the host's NOP ack.  A poll issued at
                                     once is ordered behind FINISHED on the link, reaches host memory
                                     before the host can have answered, and costs a wasted round
-                                    trip; 0 = 200 (LK_CF_NO_ACK_DELAY: poll at once) */
+                                    trip.  The starting value: each worker adapts it to the host's
+                                    answer time, within 1/4..4x (LK_CF_ACK_FIXED: no adaptation);
+                                    0 = 300 (LK_CF_NO_ACK_DELAY: poll at once) */
   uint32_t idle_delay_ns;        /* the same after publishing the NOP that ends a handshake, for a
                                     host that re-triggers the same worker at once: set it to the
                                     host's re-trigger time (~300 ns from a C loop, ~600 ns through
@@ -158,6 +160,7 @@ typedef struct lk_config {
                                     meant for SMs slowed unevenly by co-running work) */
 #define LK_CF_NO_ACK_DELAY 128u  /* DIRECT, 1 replica: poll for the ack right after FINISHED
                                     (lk_config.ack_delay_ns) */
+#define LK_CF_ACK_FIXED    256u  /* keep ack_delay_ns as configured (no per-worker adaptation) */
 #define LK_CF_LAZY_ACK      16u  /* lk_wait returns once the NOP ack is written; the next trigger or
                                     dispose touching that worker waits for its republished NOP */
 

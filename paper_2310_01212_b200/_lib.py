@@ -44,6 +44,7 @@ CF_LAZY_ACK = 16
 CF_ACK_WINDOW = 32
 CF_DYNAMIC_TILES = 64
 CF_NO_ACK_DELAY = 128
+CF_ACK_FIXED = 256
 POLL_DIRECT = 0
 POLL_GATEWAY = 1
 POLL_HYBRID = 2

@@ -519,7 +519,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.num_slots == 0) cfg.num_slots = 1024;
   if (cfg.trace_capacity == 0) cfg.trace_capacity = 65536;
   if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
-  if (cfg.ack_delay_ns == 0) cfg.ack_delay_ns = 200;
+  if (cfg.ack_delay_ns == 0) cfg.ack_delay_ns = 300;
   if (cfg.tma_min_workers == 0) cfg.tma_min_workers = 49;
   if (cfg.ack_delay_ns > 100000 || cfg.idle_delay_ns > 100000)
     return fail(LK_E_CONFIG, "ack_delay_ns and idle_delay_ns must be at most 100000");

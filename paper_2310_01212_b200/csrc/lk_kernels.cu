@@ -588,7 +588,8 @@ struct Elected {           // thread 0's private protocol state
   uint32_t hint;           // host hint bits of the current value (LK_HINT_*)
   uint32_t dseq, rseq;     // HYBRID: writes seen on the direct cell / via the event ring
   uint32_t tcnt;
-  uint32_t nload;          // LK_CF_TIMELINE, DIRECT: cell loads issued while awaiting the ack
+  uint32_t nload;          // DIRECT: cell loads issued since the ack wait began
+  uint32_t ack_cyc;        // DIRECT, 1 replica: this worker's current ack delay (adapted, see ack_adapt)
   bool dirty;              // cur not yet stepped to a fixed point
   bool idle_pub;           // just published NOP (ack consumed): the host may trigger this worker next
   uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
@@ -650,6 +651,27 @@ __device__ __forceinline__ void publish_fast(const lk_dev_args& a, uint32_t wid,
   st_relaxed_sys(a.status + uint64_t(wid) * a.status_u64, uint64_t(word) | (uint64_t(phase) << 32));
 }
 
+// The ack delay (see spin_cycles below) is per worker and adapts to the host:
+// a host that needs longer than the delay to see FINISHED and write the NOP
+// makes the delayed load miss, and the NOP arrives on the second load; the
+// delay then grows by a quarter of its configured value.  Every ack seen on
+// the first load shrinks it by 1/256, so it settles just above the host's
+// answer time (boxes differ: 150-250 ns measured, tools/ab_ack.py) with a
+// ~2% miss rate.  Acks that took more loads (wide masks: the host acks after
+// the last worker finished) say nothing about that time and are ignored.
+// Bounds: 1/4 to 4x the configured delay.
+__device__ __forceinline__ void ack_adapt(const lk_dev_args& a, Elected& e) {
+  if (!a.ack_delay_cyc || a.replicas != 1 || (a.flags & LK_CF_ACK_FIXED)) return;
+  if (e.nload == 1) {
+    const uint32_t lo = a.ack_delay_cyc >> 2;
+    e.ack_cyc -= e.ack_cyc >> 8;
+    if (e.ack_cyc < lo) e.ack_cyc = lo;
+  } else if (e.nload == 2) {
+    const uint32_t hi = a.ack_delay_cyc << 2;
+    e.ack_cyc = min(e.ack_cyc + (a.ack_delay_cyc >> 2), hi);
+  }
+}
+
 // The two transitions every empty-task round trip makes, settled in place
 // right where the new value was seen (no descriptor fetch, no trip through
 // the general dispatch code and its cold instruction-cache lines):
@@ -686,13 +708,13 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
     tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
     if (a.flags & LK_CF_TIMELINE) {
       tl[0] = e.t_seen; tl[4] = e.t_fwd; tl[8] = globaltimer();
-      e.nload = 0;
     }
     return kFastSettled;
   }
   if (e.st.phase == LK_PHASE_FINISHED && w == LK_NOP) {
     publish_fast(a, wid, LK_NOP, LK_PHASE_IDLE);
     e.idle_pub = true;
+    ack_adapt(a, e);
     if (a.flags & LK_CF_TIMELINE) {
       unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
       tl[9] = e.t_seen; tl[10] = e.nload; tl[11] = e.c_seen;
@@ -767,6 +789,11 @@ __device__ __forceinline__ void spin_cycles(uint32_t cyc) {
   }
 }
 
+__device__ __forceinline__ void ack_wait(Elected& e) {
+  spin_cycles(e.ack_cyc);
+  e.nload = 0;
+}
+
 // Spin until the state machine begins work or exits.  The to_gpu cell is K
 // replicas {word, seq} on separate 128-B lines; one ld.relaxed.sys per replica
 // is kept in flight, staggered by spacing_ns, so the host's write is sampled K
@@ -782,7 +809,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
   for (;;) {
     const uint32_t act = settle(a, wid, e);
     if (act != LK_ACT_NONE) return act;
-    if (K == 1 && e.st.phase == LK_PHASE_FINISHED) spin_cycles(a.ack_delay_cyc);
+    if (K == 1 && e.st.phase == LK_PHASE_FINISHED) ack_wait(e);
     unsigned long long v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -798,16 +825,16 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
           fresh = f == kFastNone;          // settled in place: keep polling
           if (fresh) break;
           if (K == 1) {
-            if (e.st.phase == LK_PHASE_FINISHED) spin_cycles(a.ack_delay_cyc);
+            if (e.st.phase == LK_PHASE_FINISHED) ack_wait(e);
             else if (e.idle_pub) spin_cycles(a.idle_delay_cyc);
           }
           e.idle_pub = false;
           v[k] = ld_cell(base + k * step, acquire);
-          if (timeline) ++e.nload;
+          ++e.nload;
           continue;
         }
         v[k] = ld_cell(base + k * step, acquire);
-        if (timeline) ++e.nload;
+        ++e.nload;
         if (K > 1) __nanosleep(a.spacing_ns);
         else if (a.backoff_ns) __nanosleep(a.backoff_ns);
       }
@@ -842,11 +869,11 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         const uint32_t f = fast_step(a, wid, e);
         if (f == kFastBegin) return LK_ACT_BEGIN;
         if (f == kFastNone) break;                  // general path
-        if (e.st.phase == LK_PHASE_FINISHED) spin_cycles(a.ack_delay_cyc);
+        if (e.st.phase == LK_PHASE_FINISHED) ack_wait(e);
         else if (e.idle_pub) spin_cycles(a.idle_delay_cyc);
         e.idle_pub = false;
         v = ld_cell(cell, acquire);
-        if (timeline) ++e.nload;
+        ++e.nload;
         if (gap && e.st.phase == LK_PHASE_FINISHED) {
           const uint64_t c0 = clock64();
           while (clock64() - c0 < gap) {
@@ -857,7 +884,7 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         continue;
       }
       v = ld_cell(cell, acquire);
-      if (timeline) ++e.nload;
+      ++e.nload;
       if (a.backoff_ns) __nanosleep(a.backoff_ns);
     }
   }
@@ -1089,6 +1116,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.rseq = 0;
   e.tcnt = 0;
   e.nload = 0;
+  e.ack_cyc = a.ack_delay_cyc;
   e.idle_pub = false;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   e.t_seen = 0;

@@ -74,7 +74,9 @@ class NativeConfig:
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
     ack_window: bool = False        # direct/1 replica: second load while awaiting the ack
     dynamic_tiles: bool = False     # payload maps: static 7/8 share + a pool claimed by early finishers
-    ack_delay_ns: int = 200         # direct/1 replica: first poll for the ack this long after FINISHED (0: at once)
+    ack_delay_ns: int = 300         # direct/1 replica: first poll for the ack this long after FINISHED (0: at
+                                    # once); adapted per worker to the host's answer time
+    ack_adaptive: bool = True       # False: keep ack_delay_ns fixed
     idle_delay_ns: int = 0          # opt-in: first poll for the next WORK this long after the closing NOP
     tma_min_workers: int = 49       # payload dispatches to fewer workers use LSU loads (1: always the ring)
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
@@ -125,7 +127,8 @@ class NativeConfig:
                    | (_lib.CF_LAZY_ACK if self.lazy_ack else 0)
                    | (_lib.CF_ACK_WINDOW if self.ack_window else 0)
                    | (_lib.CF_DYNAMIC_TILES if self.dynamic_tiles else 0)
-                   | (0 if self.ack_delay_ns else _lib.CF_NO_ACK_DELAY))
+                   | (0 if self.ack_delay_ns else _lib.CF_NO_ACK_DELAY)
+                   | (0 if self.ack_adaptive else _lib.CF_ACK_FIXED))
         return c
 
 

@@ -38,6 +38,7 @@ KNOBS = {
     "ack-window": dict(ack_window=True),
     "no-ack-delay": dict(ack_delay_ns=0),
     "idle-delay": dict(idle_delay_ns=300),
+    "ack-fixed": dict(ack_adaptive=False, ack_delay_ns=250),
     "ack-delay-1us": dict(ack_delay_ns=1000, idle_delay_ns=1500),
     "ack-delay-replicas2": dict(ack_delay_ns=500, poll_replicas=2),   # the delay applies to 1 replica only
     "timeline": dict(timeline=True, poll_mode="gateway"),

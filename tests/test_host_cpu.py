@@ -362,7 +362,8 @@ def test_pyfast_error_codes_raise(tmp_path):
 def test_ack_delay_config():
     from paper_2310_01212_b200 import native
     c = native.NativeConfig().to_c()
-    assert c.ack_delay_ns == 200 and not c.flags & _lib.CF_NO_ACK_DELAY
+    assert c.ack_delay_ns == 300 and not c.flags & (_lib.CF_NO_ACK_DELAY | _lib.CF_ACK_FIXED)
+    assert native.NativeConfig(ack_adaptive=False).to_c().flags & _lib.CF_ACK_FIXED
     assert c.idle_delay_ns == 0
     c = native.NativeConfig(ack_delay_ns=0, idle_delay_ns=300).to_c()
     assert c.flags & _lib.CF_NO_ACK_DELAY and c.idle_delay_ns == 300

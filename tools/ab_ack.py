@@ -1,7 +1,6 @@
 """Ack-phase polling variants, interleaved: after publishing FINISHED a worker
-(a) reloads its cell at once (ack_delay_ns=0), (b) also samples it again
-poll_spacing_ns later (ack_window), (c) waits ack_delay_ns before its first
-reload (the default, 200 ns).  148 workers, round robin, C loop."""
+(a) reloads its cell at once (ack_delay_ns=0), (b) waits a fixed ack_delay_ns before its
+first reload, (c) starts from ack_delay_ns and adapts it (the default).  148 workers, round robin, C loop."""
 import sys
 
 sys.path.insert(0, ".")
@@ -12,10 +11,10 @@ from paper_2310_01212_b200.device import WorkDescriptor  # noqa: E402
 
 native.pin_host_thread(0)
 variants = {"no-delay": dict(ack_delay_ns=0)}
-for sp in (150, 300):
-    variants[f"window{sp}"] = dict(ack_window=True, poll_spacing_ns=sp, ack_delay_ns=0)
-for d in (100, 150, 200, 250, 300, 400):
-    variants[f"delay{d}"] = dict(ack_delay_ns=d)
+for d in (150, 200, 250, 300, 400):
+    variants[f"fixed{d}"] = dict(ack_delay_ns=d, ack_adaptive=False)
+for d in (150, 300, 600):
+    variants[f"adapt{d}"] = dict(ack_delay_ns=d)
 res = {k: [] for k in variants}
 for trial in range(3):
     for name, kw in variants.items():
