@@ -890,7 +890,9 @@ def run_lk_arm(args, world, rank, local):
                    "total_rounds": int(units), "threads_per_worker": cfg.threads_per_worker,
                    "cell_stride": cfg.cell_stride, "poll_backoff_ns": cfg.poll_backoff_ns,
                    "poll_mode": cfg.poll_mode, "poll_replicas": cfg.poll_replicas,
-                   "poll_spacing_ns": cfg.poll_spacing_ns, "payload_path": "tma" if cfg.tma_payload else "lsu",
+                   "poll_spacing_ns": cfg.poll_spacing_ns, "ack_delay_ns": cfg.ack_delay_ns,
+                   "ack_adaptive": cfg.ack_adaptive, "payload_path": "tma" if cfg.tma_payload else "lsu",
+                   "tma_min_workers": cfg.tma_min_workers,
                    "host_cores_local": pinned, "host_core": pinned_core, "l2": "n/a for the empty task (no payload); payload "
                    "GB/s rotate buffers over >= 4x L2",
                    "timing": "host CLOCK_MONOTONIC per round; max over ranks"},
@@ -905,7 +907,7 @@ def run_lk_arm(args, world, rank, local):
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 1), "unit": "tasks/s",
                 "h2d_bytes_per_step": 2 * 8 * cfg.poll_replicas * R, "d2h_bytes_per_step": 3 * 8 * R,
-                "note": "Python API session.trigger+session.wait per task (ctypes -> liblk.so), "
+                "note": "Python API session.trigger+session.wait per task (the _lkfast CPython path -> liblk.so), "
                         f"{e2e_rounds} tasks; host<->device traffic per task is the mailbox cells "
                         "themselves: WORK + ack down (8 B x replicas each), WORKING/FINISHED/NOP up (8 B each)"},
         "gpu_launches": 1,
