@@ -639,6 +639,17 @@ class LaunchSyncBaseline:
 ThreadSpawnBaseline = LaunchSyncBaseline
 
 
+def profile_run(cfg: Optional[NativeConfig] = None, rounds: int = 20000) -> int:
+    """Boot, run `rounds` round-robin empty-task handshakes from a host thread
+    started before the kernel launch, and tear down (lk_profile_run): the
+    persistent kernel under ncu (--replay-mode application).  Returns the
+    rounds' host wall time in ns."""
+    cfg = cfg or NativeConfig()
+    ns = C.c_uint64()
+    _lib.check(_lib.load().lk_profile_run(C.byref(cfg.to_c()), rounds, C.byref(ns)))
+    return ns.value
+
+
 def sm_topology(device: int = 0) -> list[int]:
     """GPC group of every SM (index = %smid), from clustered probe launches
     (lk_sm_topology).  Call with no session live.  Combine with a session's
