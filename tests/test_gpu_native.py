@@ -598,3 +598,16 @@ def test_huge_slot_numbers_are_refused_cleanly():
     session.trigger(1, TINY_WORK)
     session.wait(1)
     session.dispose()
+
+
+def test_profile_run_completes_and_frees_the_device():
+    """lk_profile_run: a session driven by the internal host thread boots,
+    runs its handshakes, exits and releases the device claim (a normal
+    session starts right after)."""
+    ns = native.profile_run(native.NativeConfig(num_workers=16), 2000)
+    assert ns > 0
+    s = start(4)
+    s.trigger(1, TINY_WORK)
+    s.wait(1)
+    s.dispose()
+    assert_trace_ok(s)

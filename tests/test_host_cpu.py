@@ -370,3 +370,10 @@ def test_ack_delay_config():
     for bad in (-1, 100_001):
         with pytest.raises(errors.UsageError):
             native.NativeConfig(ack_delay_ns=bad)
+
+
+def test_profile_run_refuses_non_direct_configs():
+    from paper_2310_01212_b200 import native
+    for cfg in (native.NativeConfig(poll_mode="gateway"), native.NativeConfig(record_trace=True)):
+        with pytest.raises(errors.ConfigError):
+            native.profile_run(cfg, 10)
