@@ -273,12 +273,15 @@ int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks,
                        uint64_t* trig_ns, uint64_t* done_ns, uint64_t* cycle_ns);
 /* A profiling run of the persistent kernel itself: boots a DIRECT session
  * whose handshakes come from a host thread started before the kernel launch
- * -- `rounds` round-robin empty-task dispatches, then EXIT -- and tears it
- * down.  Under a profiler that returns from the launch only once the kernel
- * has exited (ncu; use --replay-mode application), this is a complete run
- * rather than a deadlock.  The thread makes no CUDA calls.  *elapsed_ns: the
- * rounds' host wall time. */
-int lk_profile_run(const lk_config* cfg, uint64_t rounds, uint64_t* elapsed_ns);
+ * and tears it down.  The thread runs `rounds` dispatches, then EXIT: with
+ * ndesc == 0 round-robin empty tasks on single workers; else full-mask
+ * dispatches of descs[r % ndesc] (staged in slots 1..ndesc before the
+ * launch), each acked before the next.  Under a profiler that returns from
+ * the launch only once the kernel has exited (ncu; use --replay-mode
+ * application), this is a complete run rather than a deadlock.  The thread
+ * makes no CUDA calls.  *elapsed_ns: the rounds' host wall time. */
+int lk_profile_run(const lk_config* cfg, const lk_desc* descs, uint32_t ndesc, uint64_t rounds,
+                   uint64_t* elapsed_ns);
 /* Device-side spans of the last dispatch per worker (globaltimer ns):
  * begin (WORK observed) and end (work done, before FINISHED). */
 int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n);

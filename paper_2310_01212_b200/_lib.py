@@ -148,7 +148,7 @@ SIGNATURES = {
     "lk_protocol_complete": (I32, [PU32, PU32, PU32, PU32]),
     "lk_validate_trace": (I32, [P, P, P, U64, PI64, C.c_char_p, U32, PU64, U32, PU32]),
     "lk_bench_roundtrip": (I32, [P, MASK, U32, U32, U32, U64, P, P, P]),
-    "lk_profile_run": (I32, [C.POINTER(lk_config), U64, C.POINTER(C.c_uint64)]),
+    "lk_profile_run": (I32, [C.POINTER(lk_config), P, U32, U64, C.POINTER(C.c_uint64)]),
     "lk_last_spans": (I32, [P, P, P, U32]),
     "lk_last_timeline": (I32, [P, P, U32]),
     "lk_last_host_times": (I32, [P, P, U32]),

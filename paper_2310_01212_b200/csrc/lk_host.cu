@@ -495,6 +495,8 @@ static void release_device(int dev) {
 static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* d, const uint64_t* mask, uint32_t nwords);
 
 struct ProfileRun {
+  const lk_desc* descs = nullptr;   // payload items, dispatched to every worker in turn (null: empty tasks)
+  uint32_t ndesc = 0;
   uint64_t rounds = 0;
   uint64_t elapsed_ns = 0;
   int rc = LK_OK;
@@ -519,6 +521,16 @@ static void profile_driver(lk_session* s, ProfileRun* pr) {
   }
   const uint64_t t0 = now_ns();
   for (uint64_t r = 0; r < pr->rounds && pr->rc == LK_OK; ++r) {
+    if (pr->ndesc) {   // full-mask payload dispatch of slot 1 + r % ndesc, then the ack
+      const uint32_t w = LK_WORK_BASE + 1 + uint32_t(r % pr->ndesc);
+      for (uint32_t i = 0; i < s->nw; ++i) s->host_write(i, w);
+      for (uint32_t i = 0; i < s->nw && pr->rc == LK_OK; ++i)
+        if (!spin(i, LK_FINISHED, 10ull * 1000000000ull)) pr->rc = LK_E_HANG;
+      for (uint32_t i = 0; i < s->nw; ++i) s->host_write(i, LK_NOP);
+      for (uint32_t i = 0; i < s->nw && pr->rc == LK_OK; ++i)
+        if (!spin(i, LK_NOP, 10ull * 1000000000ull)) pr->rc = LK_E_HANG;
+      continue;
+    }
     const uint32_t i = uint32_t(r % s->nw);
     s->host_write(i, LK_WORK_BASE, LK_HINT_EMPTY);
     if (!spin(i, LK_FINISHED, 10ull * 1000000000ull)) { pr->rc = LK_E_HANG; break; }
@@ -785,7 +797,13 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     lk_desc ed;
     memset(&ed, 0, sizeof ed);
     ed.kind = LK_KIND_EMPTY;
-    const int src = stage_locked(s, 0, &ed, nullptr, 0);
+    int src = stage_locked(s, 0, &ed, nullptr, 0);
+    std::vector<uint64_t> full(s->nwords, 0);
+    for (uint32_t i = 0; i < s->nw; ++i) full[i >> 6] |= 1ull << (i & 63);
+    for (uint32_t k = 0; k < pr->ndesc && !src; ++k) {
+      if (pr->descs[k].kind >= LK_KIND_COUNT || k + 1 >= cfg.num_slots) src = fail(LK_E_USAGE, "bad profile descriptor");
+      else src = stage_locked(s, k + 1, &pr->descs[k], full.data(), s->nwords);
+    }
     if (src) return cleanup(src);
     driver = std::thread(profile_driver, s, pr);
   }
@@ -850,11 +868,14 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   return LK_OK;
 }
 
-extern "C" int lk_profile_run(const lk_config* cfg, uint64_t rounds, uint64_t* elapsed_ns) {
-  if (!cfg) return fail(LK_E_USAGE, "null argument");
+extern "C" int lk_profile_run(const lk_config* cfg, const lk_desc* descs, uint32_t ndesc, uint64_t rounds,
+                              uint64_t* elapsed_ns) {
+  if (!cfg || (ndesc && !descs)) return fail(LK_E_USAGE, "null argument");
   if (cfg->poll_mode != LK_POLL_DIRECT || cfg->record_trace)
     return fail(LK_E_CONFIG, "profile runs use DIRECT polling without trace recording");
   ProfileRun pr;
+  pr.descs = descs;
+  pr.ndesc = ndesc;
   pr.rounds = rounds;
   t_profile = &pr;
   lk_session* s = nullptr;

@@ -639,14 +639,18 @@ class LaunchSyncBaseline:
 ThreadSpawnBaseline = LaunchSyncBaseline
 
 
-def profile_run(cfg: Optional[NativeConfig] = None, rounds: int = 20000) -> int:
-    """Boot, run `rounds` round-robin empty-task handshakes from a host thread
-    started before the kernel launch, and tear down (lk_profile_run): the
-    persistent kernel under ncu (--replay-mode application).  Returns the
-    rounds' host wall time in ns."""
+def profile_run(cfg: Optional[NativeConfig] = None, rounds: int = 20000, works=()) -> int:
+    """Boot, run `rounds` handshakes from a host thread started before the
+    kernel launch, and tear down (lk_profile_run): the persistent kernel
+    under ncu (--replay-mode application).  No `works`: round-robin empty
+    tasks; else full-mask dispatches of works[r % len(works)] (payload
+    WorkDescriptors).  Returns the rounds' host wall time in ns."""
     cfg = cfg or NativeConfig()
+    ds = [as_work(w).to_c() for w in works]
+    arr = (_lib.lk_desc * max(1, len(ds)))(*ds)
     ns = C.c_uint64()
-    _lib.check(_lib.load().lk_profile_run(C.byref(cfg.to_c()), rounds, C.byref(ns)))
+    _lib.check(_lib.load().lk_profile_run(C.byref(cfg.to_c()), C.cast(arr, C.c_void_p) if ds else None, len(ds),
+                                          rounds, C.byref(ns)))
     return ns.value
 
 

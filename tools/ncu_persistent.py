@@ -1,18 +1,37 @@
 """The persistent kernel itself under ncu: lk_profile_run boots a DIRECT
-session whose round-robin empty-task handshakes come from a host thread
-started before the launch, so ncu's serialized launch returns.  Run as
+session whose dispatches come from a host thread started before the launch,
+so ncu's serialized launch returns.  Run as
 
     ncu --replay-mode application --clock-control none --set full \\
-        -k lk_persistent_kernel -c 1 -o out python tools/ncu_persistent.py [rounds]
+        -k lk_persistent_kernel -c 1 -o out python tools/ncu_persistent.py [rounds] [saxpy]
 
-Without ncu it prints the rounds' tasks/s (a sanity check of the hook)."""
+No second argument: round-robin empty tasks (configs[1] shape).  `saxpy`:
+full-mask saxpy_f32 dispatches, 64 MiB per vector, rotating over 4 buffer
+sets (512 MiB, L2-cold), for the in-situ DRAM traffic per dispatch.
+Without ncu it prints the run's rate (a sanity check of the hook)."""
 import sys
 
 sys.path.insert(0, ".")
 from paper_2310_01212_b200 import native  # noqa: E402
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
 
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
+payload = len(sys.argv) > 2 and sys.argv[2] == "saxpy"
 native.pin_host_thread(0)
-ns = native.profile_run(native.NativeConfig(), rounds)
-print(f"profile run: {rounds} round-robin empty tasks in {ns / 1e6:.1f} ms = {rounds / (ns / 1e9) / 1e3:.1f}k tasks/s",
-      flush=True)
+if not payload:
+    ns = native.profile_run(native.NativeConfig(), rounds)
+    print(f"profile run: {rounds} round-robin empty tasks in {ns / 1e6:.1f} ms = "
+          f"{rounds / (ns / 1e9) / 1e3:.1f}k tasks/s", flush=True)
+else:
+    n = (64 << 20) // 4
+    bufs, works = [], []
+    for k in range(4):
+        x, y = DeviceBuffer(4 * n), DeviceBuffer(4 * n)
+        bufs += [x, y]
+        works.append(WorkDescriptor(slot=1 + k, kind="saxpy_f32", data_in_ref=(x, y), data_out_ref=y, alpha=1.5))
+    ns = native.profile_run(native.NativeConfig(), rounds, works)
+    alg = 12 * n
+    print(f"profile run: {rounds} full-mask saxpy_f32 dispatches (64 MiB/vector) in {ns / 1e6:.2f} ms = "
+          f"{rounds * alg / ns:.1f} GB/s including handshakes; algorithmic bytes/dispatch {alg}", flush=True)
+    for b in bufs:
+        b.free()
