@@ -611,3 +611,25 @@ def test_profile_run_completes_and_frees_the_device():
     s.wait(1)
     s.dispose()
     assert_trace_ok(s)
+
+
+def test_profile_run_payload_dispatches():
+    """lk_profile_run with payload descriptors: full-mask dispatches of each
+    in turn; three in-place saxpy passes equal the oracle applied three times."""
+    from oracle import work as W
+    from paper_2310_01212_b200.device import DeviceBuffer
+    n = 100_003
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    y = rng.uniform(-1, 1, n).astype(np.float32)
+    dx, dy = DeviceBuffer.from_array(x), DeviceBuffer.from_array(y)
+    try:
+        w = WorkDescriptor(slot=1, kind="saxpy_f32", data_in_ref=(dx, dy), data_out_ref=dy, alpha=0.5)
+        assert native.profile_run(native.NativeConfig(num_workers=32), 3, [w]) > 0
+        want = y
+        for _ in range(3):
+            want = W.saxpy_f32(0.5, x, want)
+        np.testing.assert_array_equal(dy.download(np.float32, n).view(np.uint32), want.view(np.uint32))
+    finally:
+        dx.free()
+        dy.free()
