@@ -125,9 +125,11 @@ typedef struct lk_config {
                                     answer time, within 1/4..4x (LK_CF_ACK_FIXED: no adaptation);
                                     0 = 300 (LK_CF_NO_ACK_DELAY: poll at once) */
   uint32_t idle_delay_ns;        /* the same after publishing the NOP that ends a handshake, for a
-                                    host that re-triggers the same worker at once: set it to the
-                                    host's re-trigger time (~300 ns from a C loop, ~600 ns through
-                                    Python); a load that misses costs a round trip.  0 = none */
+                                    host that re-triggers the same worker at once (~300 ns from a C
+                                    loop, ~600 ns through Python).  The starting value: each worker
+                                    grows it while its WORK keeps arriving one load late, and leaves
+                                    it at 0 when other workers are triggered in between (round
+                                    robin); LK_CF_ACK_FIXED keeps it fixed.  0 = start at none */
   uint32_t tma_min_workers;      /* payload dispatches to fewer workers use 128-bit LSU loads even
                                     with the TMA ring on: a lone SM streams ~30% faster that way,
                                     the whole GPU faster through the ring (tools/tma_vs_lsu_count.py);

@@ -592,6 +592,8 @@ struct Elected {           // thread 0's private protocol state
   uint32_t ack_cyc;        // DIRECT, 1 replica: this worker's current ack delay (adapted, see ack_adapt)
   bool dirty;              // cur not yet stepped to a fixed point
   bool idle_pub;           // just published NOP (ack consumed): the host may trigger this worker next
+  bool idle_armed;         // the idle wait ran: the next WORK's load count adapts idle_cyc
+  uint32_t idle_cyc;       // DIRECT, 1 replica: this worker's current idle delay (idle_adapt)
   uint64_t t_seen;         // globaltimer when the current to_gpu value arrived
   uint64_t c_seen;         // clock64 at the same point
   uint64_t t_fwd;          // GATEWAY + LK_CF_TIMELINE: globaltimer when the gateway forwarded it
@@ -672,6 +674,22 @@ __device__ __forceinline__ void ack_adapt(const lk_dev_args& a, Elected& e) {
   }
 }
 
+// The idle delay adapts the same way, from idle_delay_ns (default 0): a WORK
+// that arrives on the second load after the closing NOP means the host
+// re-triggers this worker right after each handshake, a little later than
+// the delay; the delay grows by ~65 ns (cap ~1.5 us).  A WORK on the first
+// load shrinks it by 1/256.  A WORK after more loads (the host triggered
+// other workers in between: round robin) leaves it alone, so only loops
+// that re-trigger one worker back to back get a delay (tools/ab_idle.py).
+constexpr uint32_t kIdleStepCyc = 128, kIdleMaxCyc = 3000;
+__device__ __forceinline__ void idle_adapt(const lk_dev_args& a, Elected& e) {
+  if (!e.idle_armed) return;
+  e.idle_armed = false;
+  if (a.replicas != 1 || (a.flags & LK_CF_ACK_FIXED)) return;
+  if (e.nload == 1) e.idle_cyc -= e.idle_cyc >> 8;
+  else if (e.nload == 2) e.idle_cyc = min(e.idle_cyc + kIdleStepCyc, kIdleMaxCyc);
+}
+
 // The two transitions every empty-task round trip makes, settled in place
 // right where the new value was seen (no descriptor fetch, no trip through
 // the general dispatch code and its cold instruction-cache lines):
@@ -690,6 +708,7 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
     // IDLE x WORK(s) of any other kind: publish WORKING and begin at once; the
     // word stays dirty so it is re-stepped after completion, as in settle().
     publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
+    idle_adapt(a, e);
     e.st = lk_wstate{LK_PHASE_WORKING, w - LK_WORK_BASE};
     e.pub = LK_WORKING;
     e.dirty = true;
@@ -701,6 +720,7 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
     publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
     publish_fast(a, wid, LK_FINISHED, LK_PHASE_FINISHED);
     const uint64_t c_fin = clock64();
+    idle_adapt(a, e);
     e.st = lk_wstate{LK_PHASE_FINISHED, w - LK_WORK_BASE};
     e.pub = LK_FINISHED;
     e.dirty = false;
@@ -794,6 +814,12 @@ __device__ __forceinline__ void ack_wait(Elected& e) {
   e.nload = 0;
 }
 
+__device__ __forceinline__ void idle_wait(Elected& e) {
+  spin_cycles(e.idle_cyc);
+  e.nload = 0;
+  e.idle_armed = true;
+}
+
 // Spin until the state machine begins work or exits.  The to_gpu cell is K
 // replicas {word, seq} on separate 128-B lines; one ld.relaxed.sys per replica
 // is kept in flight, staggered by spacing_ns, so the host's write is sampled K
@@ -826,7 +852,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
           if (fresh) break;
           if (K == 1) {
             if (e.st.phase == LK_PHASE_FINISHED) ack_wait(e);
-            else if (e.idle_pub) spin_cycles(a.idle_delay_cyc);
+            else if (e.idle_pub) idle_wait(e);
           }
           e.idle_pub = false;
           v[k] = ld_cell(base + k * step, acquire);
@@ -870,7 +896,7 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         if (f == kFastBegin) return LK_ACT_BEGIN;
         if (f == kFastNone) break;                  // general path
         if (e.st.phase == LK_PHASE_FINISHED) ack_wait(e);
-        else if (e.idle_pub) spin_cycles(a.idle_delay_cyc);
+        else if (e.idle_pub) idle_wait(e);
         e.idle_pub = false;
         v = ld_cell(cell, acquire);
         ++e.nload;
@@ -1118,6 +1144,8 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.nload = 0;
   e.ack_cyc = a.ack_delay_cyc;
   e.idle_pub = false;
+  e.idle_armed = false;
+  e.idle_cyc = a.idle_delay_cyc;
   e.dirty = true;  // boot: step NOP -> INIT, then NOP -> IDLE
   e.t_seen = 0;
   e.c_seen = 0;

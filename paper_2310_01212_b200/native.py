@@ -77,7 +77,8 @@ class NativeConfig:
     ack_delay_ns: int = 300         # direct/1 replica: first poll for the ack this long after FINISHED (0: at
                                     # once); adapted per worker to the host's answer time
     ack_adaptive: bool = True       # False: keep ack_delay_ns fixed
-    idle_delay_ns: int = 0          # opt-in: first poll for the next WORK this long after the closing NOP
+    idle_delay_ns: int = 0          # first poll for the next WORK this long after the closing NOP (start;
+                                    # adapted up for back-to-back re-triggers of one worker)
     tma_min_workers: int = 49       # payload dispatches to fewer workers use LSU loads (1: always the ring)
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker

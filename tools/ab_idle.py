@@ -1,5 +1,5 @@
-"""Idle delay (the first poll after the NOP that closes a handshake) vs how
-soon the host re-triggers the same worker: a single-worker C loop, a
+"""Idle delay (the first poll after the NOP that closes a handshake; adaptive,
+from the given start) vs how soon the host re-triggers the same worker: a single-worker C loop, a
 single-worker Python-API loop, 4-worker and 148-worker round robin.
 ack_delay_ns stays at its default; interleaved trials."""
 import sys
@@ -12,7 +12,7 @@ from paper_2310_01212_b200 import native  # noqa: E402
 from paper_2310_01212_b200.device import WorkDescriptor  # noqa: E402
 
 native.pin_host_thread(0)
-idles = [int(x) for x in sys.argv[1:]] or [1, 200, 300, 400, 600, 900]
+idles = [int(x) for x in sys.argv[1:]] or [0, 300, 600]
 res = {}
 for trial in range(3):
     for idle in idles:
