@@ -727,6 +727,24 @@ def run_lk_arm(args, world, rank, local):
     _, fdone, fcyc = session.bench_roundtrip([full], 0, args.full_rounds)
     extras["full_mask"] = {"trigger_to_done": lat_summary(fdone), "round_trip": lat_summary(fcyc),
                            "tasks_per_s": round(args.full_rounds / (fcyc.sum() / 1e9), 1)}
+    # one worker re-triggered back to back (the adaptive idle delay's case),
+    # from C and through the Python API
+    _, sdone, scyc = session.bench_roundtrip([1], 0, 3000)
+    _, sdone, scyc = session.bench_roundtrip([1], 0, args.full_rounds)
+    empty_w = WorkDescriptor(slot=0, kind="empty")
+    for _k in range(2000):
+        session.trigger(1, empty_w)
+        session.wait(1)
+    t_py = time.perf_counter_ns()
+    for _k in range(args.full_rounds):
+        session.trigger(1, empty_w)
+        session.wait(1)
+    t_py = time.perf_counter_ns() - t_py
+    session.timings.clear()
+    extras["single_worker"] = {"trigger_to_done": lat_summary(sdone), "round_trip": lat_summary(scyc),
+                               "tasks_per_s": round(args.full_rounds / (scyc.sum() / 1e9), 1),
+                               "python_api_tasks_per_s": round(args.full_rounds / (t_py / 1e9), 1),
+                               "note": "worker 0 re-triggered back to back (adaptive idle delay engaged)"}
 
     # the small-transfer case the paper's pathology is about (PAPER:160-162,
     # P/link.py:84-122): a 4-byte cudaMemcpy each way (stream-synchronous)
