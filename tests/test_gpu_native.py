@@ -633,3 +633,22 @@ def test_profile_run_payload_dispatches():
     finally:
         dx.free()
         dy.free()
+
+
+def test_adaptive_ack_delay_lands_the_ack_on_the_first_load():
+    """DIRECT, default ack delay: after a warm-up the worker's first load
+    after FINISHED sees the host's NOP (timeline word 10 = loads issued while
+    awaiting the ack); with the delay off the first load always misses."""
+    def ack_loads(**kw):
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=16, spin_strategy=native.PURE_SPIN,
+                                                              timeline=True, **kw))
+        try:
+            s.register(WorkDescriptor(slot=0, kind="empty"))
+            s.bench_roundtrip([1 << i for i in range(16)], 0, 16 * 400)
+            return s.last_timeline()[:, 10].astype(int)
+        finally:
+            s.close()
+    with_delay = ack_loads()
+    without = ack_loads(ack_delay_ns=0)
+    assert np.median(with_delay) == 1, with_delay
+    assert np.median(without) >= 2, without
