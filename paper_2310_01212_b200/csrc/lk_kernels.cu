@@ -859,10 +859,10 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
           ++e.nload;
           continue;
         }
+        if (K == 1 && a.backoff_ns) __nanosleep(a.backoff_ns);   // before the load: a real gap between polls
         v[k] = ld_cell(base + k * step, acquire);
         ++e.nload;
         if (K > 1) __nanosleep(a.spacing_ns);
-        else if (a.backoff_ns) __nanosleep(a.backoff_ns);
       }
       if (!fresh && K > 1 && a.backoff_ns) __nanosleep(a.backoff_ns);
     }
@@ -909,9 +909,9 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         }
         continue;
       }
+      if (a.backoff_ns) __nanosleep(a.backoff_ns);   // before the load: a real gap between polls
       v = ld_cell(cell, acquire);
       ++e.nload;
-      if (a.backoff_ns) __nanosleep(a.backoff_ns);
     }
   }
 }
