@@ -420,19 +420,19 @@ struct ReduceSmem {
 // fp64 into *(double*)aux.
 template <int U>
 __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t rank, uint32_t count,
-                                             uint32_t* ctr, ReduceSmem& sm, uint32_t T, Ring* ring,
-                                             uint32_t& g) {
+                                             uint32_t* ctr, ReduceSmem& sm, uint32_t T, Ring& ring,
+                                             bool ring_on, uint32_t& g) {
   const uint32_t t = threadIdx.x;
   const float* x = reinterpret_cast<const float*>(d.in0);
   float acc = 0.f;
-  if (ring && !(d.flags & LK_DF_SCALAR)) {
+  if (ring_on && !(d.flags & LK_DF_SCALAR)) {
     const uint4* x4 = reinterpret_cast<const uint4*>(x);
     const uint64_t vb = p.b >> 2, ve = p.e >> 2;
     constexpr uint32_t kTileV = kStageBytes / 16;
     const uint64_t nv = ve > vb ? ve - vb : 0;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     ring_stream(
-        *ring, g, uint32_t((nv + kTileV - 1) / kTileV), T,
+        ring, g, uint32_t((nv + kTileV - 1) / kTileV), T,
         [&](uint32_t i, uint8_t* stage, uint64_t* bar) {
           const uint64_t v0 = vb + uint64_t(i) * kTileV;
           const uint32_t bytes = uint32_t(min(uint64_t(kTileV), ve - v0)) * 16u;
@@ -539,42 +539,45 @@ __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
 }
 
 // Payload work shared by both kernels; every thread of the CTA calls it.
-// ring == nullptr (or misaligned buffers): 128-bit LSU loads; else the TMA ring.
+// !ring_on (or misaligned buffers): 128-bit LSU loads; else the TMA ring.
+// The ring travels by reference with a flag, never as a pointer to the
+// caller's local: a pointer would pin the Ring in local memory and turn
+// every field access on the per-tile path into an LDL.
 __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
-                                          uint32_t* ctr, ReduceSmem& rs, uint32_t T, Ring* ring,
+                                          uint32_t* ctr, ReduceSmem& rs, uint32_t T, Ring& ring, bool ring_on,
                                           uint32_t& g, bool dyn = false) {
   const Part p = partition(d.n, rank, count);
-  const bool tma = ring != nullptr && !(d.flags & LK_DF_SCALAR);
-  dyn = dyn && tma && T >= 64 && ring->tile != nullptr;
+  const bool tma = ring_on && !(d.flags & LK_DF_SCALAR);
+  dyn = dyn && tma && T >= 64 && ring.tile != nullptr;
   if (dyn) {   // the pool's atomics cost ~1 us: only worth it with >= 8 tiles per worker
     const uint64_t tile_v = (d.kind == LK_KIND_HBM_STREAM) ? kStageBytes / 16 : kStageBytes / 32;
     dyn = ((d.n >> 2) + tile_v - 1) / tile_v >= 8ull * count;
   }
   switch (d.kind) {
     case LK_KIND_VECTOR_ADD_I32:
-      if (dyn) map_tma_dyn<true>(d, rank, count, OpAddI32{}, T, *ring, g, ctr + 1);
-      else if (tma) map_tma<true>(d, p, OpAddI32{}, T, *ring, g);
+      if (dyn) map_tma_dyn<true>(d, rank, count, OpAddI32{}, T, ring, g, ctr + 1);
+      else if (tma) map_tma<true>(d, p, OpAddI32{}, T, ring, g);
       else map_chunk<4, true>(d, p, OpAddI32{}, T);
       break;
     case LK_KIND_SAXPY_F32:
-      if (dyn) map_tma_dyn<true>(d, rank, count, OpSaxpy{d.alpha}, T, *ring, g, ctr + 1);
-      else if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, *ring, g);
+      if (dyn) map_tma_dyn<true>(d, rank, count, OpSaxpy{d.alpha}, T, ring, g, ctr + 1);
+      else if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, ring, g);
       else map_chunk<4, true>(d, p, OpSaxpy{d.alpha}, T);
       break;
     case LK_KIND_HBM_STREAM: {
       const uint64_t passes = d.iterations ? d.iterations : 1;
       for (uint64_t k = 0; k < passes; ++k) {
         if (dyn && passes == 1) {   // multi-pass: a fast worker would claim the next pass early
-          map_tma_dyn<false>(d, rank, count, OpCopy{}, T, *ring, g, ctr + 1);
+          map_tma_dyn<false>(d, rank, count, OpCopy{}, T, ring, g, ctr + 1);
         } else if (tma) {
-          map_tma<false>(d, p, OpCopy{}, T, *ring, g);
+          map_tma<false>(d, p, OpCopy{}, T, ring, g);
         } else {
           map_chunk<8, false>(d, p, OpCopy{}, T);
         }
       }
       break;
     }
-    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs, T, ring, g); break;
+    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs, T, ring, ring_on, g); break;
     default: break;
   }
 }
@@ -1046,14 +1049,18 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
       if (__all_sync(0xffffffffu, mine)) {
         const uint32_t word = uint32_t(w0 >> 32);
         const uint32_t hint = uint32_t(__shfl_sync(0xffffffffu, w, 5)) & 0xFFu;
-        unsigned long long m[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) m[j] = __shfl_sync(0xffffffffu, w, j + 1) & ((1ull << kRingMaskBits) - 1);
+        // the four 48-bit mask words stay in registers: a runtime index into
+        // an array would put it in local memory
+        const unsigned long long mm = (1ull << kRingMaskBits) - 1;
+        const unsigned long long m0 = __shfl_sync(0xffffffffu, w, 1) & mm, m1 = __shfl_sync(0xffffffffu, w, 2) & mm,
+                                 m2 = __shfl_sync(0xffffffffu, w, 3) & mm, m3 = __shfl_sync(0xffffffffu, w, 4) & mm;
         const uint64_t t_fwd = timeline ? globaltimer() : 0;
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
           const uint32_t i = lane + 32u * q;
-          if (i < nw && (m[i / kRingMaskBits] >> (i % kRingMaskBits) & 1ull)) {
+          const uint32_t wi = i / kRingMaskBits;
+          const unsigned long long mw = wi == 0 ? m0 : wi == 1 ? m1 : wi == 2 ? m2 : m3;
+          if (i < nw && (mw >> (i % kRingMaskBits) & 1ull)) {
             ++wseq[q];
             unsigned long long* mb = a.dmb + uint64_t(i) * a.dmb_u64;
             if (timeline) st_relaxed_gpu64(mb + 1, t_fwd);
@@ -1129,9 +1136,9 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   }
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages, sm.tile, &sm.ring_g};
-  Ring* rp = a.use_tma ? &ring : nullptr;
+  const bool ring_ok = a.use_tma != 0;
   uint32_t g = 0;
-  if (rp) ring_init(ring, T);
+  if (ring_ok) ring_init(ring, T);
   Elected e;
   e.st = lk_wstate{LK_PHASE_BOOTING, 0};
   e.pub = LK_NOP;  // cells start at the NOP sentinel (protocol.py:217-218)
@@ -1222,8 +1229,8 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     // a narrow dispatch streams through 128-bit LSU loads: a lone SM moves
     // ~110 GB/s that way against ~85 GB/s through the ring, which wins only
     // once enough SMs share the dispatch to load HBM (tools/tma_vs_lsu_count.py)
-    run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T,
-              sm.count >= a.tma_min_workers ? rp : nullptr, g, (a.flags & LK_CF_DYNAMIC_TILES) != 0);
+    run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T, ring,
+              ring_ok && sm.count >= a.tma_min_workers, g, (a.flags & LK_CF_DYNAMIC_TILES) != 0);
     wsync(T);
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();
@@ -1258,7 +1265,7 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
   Ring ring{dyn_smem, full, empty, kDefaultStages, nullptr, nullptr};   // static tiles only
   uint32_t g = 0;
   if (use_tma) ring_init(ring, blockDim.x);
-  run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, use_tma ? &ring : nullptr, g);
+  run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, ring, use_tma != 0, g);
 }
 
 // ---------------------------------------------------------------- ping-pong
