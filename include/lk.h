@@ -111,7 +111,7 @@ typedef struct lk_config {
   uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 1 */
   uint32_t poll_spacing_ns;      /* stagger between replica loads / sweeps; 0 = 300 */
   uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default), LK_POLL_GATEWAY or LK_POLL_HYBRID */
-  uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 128 */
+  uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 64 */
   uint32_t ring_stages;          /* TMA payload ring depth in 16-KiB stages, 2..12; 0 = 6 */
   uint32_t sm_partition;         /* 0: the persistent kernel spans the GPU.  N: it runs in a green
                                     context of >= N SMs (driver granularity: multiples of 8), one

@@ -554,7 +554,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.cell_stride != 8 && cfg.cell_stride != 16 && cfg.cell_stride != 32 && cfg.cell_stride != 64 &&
       cfg.cell_stride != 128)
     return fail(LK_E_CONFIG, "cell_stride must be 8, 16, 32, 64 or 128");
-  if (cfg.status_stride == 0) cfg.status_stride = 128;
+  if (cfg.status_stride == 0) cfg.status_stride = 64;   // one host cache line per worker: tools/ab_status_stride.py
   if (cfg.status_stride != 16 && cfg.status_stride != 32 && cfg.status_stride != 64 && cfg.status_stride != 128)
     return fail(LK_E_CONFIG, "status_stride must be 16, 32, 64 or 128");
   if (cfg.poll_mode > LK_POLL_HYBRID) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);

@@ -24,6 +24,7 @@ KNOBS = {
     "cell8": dict(cell_stride=8),
     "cell64": dict(cell_stride=64),
     "status16": dict(status_stride=16),
+    "status128": dict(status_stride=128),
     "status32-cell16": dict(status_stride=32, cell_stride=16),
     "threads32": dict(threads_per_worker=32),           # producer and consumer in one warp
     "threads64": dict(threads_per_worker=64),
