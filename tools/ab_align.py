@@ -1,5 +1,7 @@
 """LK_CF_ALIGN A/B: idle polls timed to the latest publish + the host's
-reaction time, against free-running polls.  C loops (148 round robin, 4
+reaction time, against free-running polls.  The option was removed after
+this A/B measured it worse from C; the tool records the
+run and needs that experimental build (git history) to execute.  C loops (148 round robin, 4
 round robin, one worker) and the Python API round robin; interleaved."""
 import sys
 import time
