@@ -8,13 +8,18 @@
 //    The other worker threads park on a named barrier (no issue slots used)
 //    and only wake for payload work items.
 //    How to_gpu values reach thread 0 (lk_config.poll_mode):
-//     - GATEWAY (default): one extra warp in CTA 0 polls the dense host
-//       doorbell array (all workers' to_gpu cells, K staggered replica sweeps
-//       in flight, ~10 PCIe line reads per sweep) and forwards each new value
-//       to the worker's mailbox line in device memory; workers poll L2.  The
-//       PCIe link sees tens of outstanding reads instead of 148 x K, and no
-//       worker thread ever holds an in-flight PCIe load.
-//     - DIRECT: every worker polls its own host cell replicas over PCIe.
+//     - DIRECT (default): thread 0 polls its own host cell over PCIe, one
+//       load in flight; after FINISHED it waits a per-worker adaptive delay
+//       before polling for the ack (ack_wait), and after the closing NOP an
+//       adaptive idle delay when the host re-triggers it back to back.
+//     - GATEWAY: one extra warp in CTA 0 polls a ring of host events and
+//       forwards each to the masked workers' mailbox lines in device memory;
+//       workers poll L2.  One event reaches a full mask.
+//     - HYBRID: direct cells for narrow writes, ring events for wide ones,
+//       forwarded by two poller warps per CTA into shared memory.
+//  * Payload work (run_multi): elementwise maps and a reduction streamed
+//    through a TMA bulk-copy ring in shared memory, or 128-bit LSU loads for
+//    dispatches to few workers (a lone SM streams faster that way).
 //  * lk_work_kernel: the same work functions as an ordinary kernel, for the
 //    cudaLaunchKernel+cudaStreamSynchronize baseline (ThreadSpawnBaseline
 //    analogue, native.py:304-331).
