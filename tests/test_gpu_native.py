@@ -652,3 +652,23 @@ def test_adaptive_ack_delay_lands_the_ack_on_the_first_load():
     without = ack_loads(ack_delay_ns=0)
     assert np.median(with_delay) == 1, with_delay
     assert np.median(without) >= 2, without
+
+
+def test_abort_after_worker_death_reclaims_the_device():
+    """A dead worker leaves the session unusable; abort() retires the kernel
+    (EXIT to the survivors), close() frees it, and the device takes a new
+    session at once (the one-session claim is released)."""
+    session = start(4)
+    _lib.check(session._lib.lk_debug_poke(session._h, 2, 9))
+    session._spin_until(lambda: session.worker_phase[2] is protocol.Phase.EXITED, "device exit", [2])
+    with pytest.raises(UsageError, match="worker 2 died"):
+        session.trigger(0b0001, TINY_WORK)
+    session.abort(timeout_s=5.0)
+    assert not session._kernel_alive()
+    session.close()
+    _LIVE.remove(session)
+    fresh = start(4)
+    fresh.trigger(0b1111, TINY_WORK)
+    fresh.wait(0b1111)
+    fresh.dispose()
+    assert_trace_ok(fresh)
