@@ -672,3 +672,26 @@ def test_abort_after_worker_death_reclaims_the_device():
     fresh.wait(0b1111)
     fresh.dispose()
     assert_trace_ok(fresh)
+
+
+def test_wait_timeout_raises_hang_then_a_later_wait_completes():
+    """lk_wait's C-side spin honours wait_timeout (native.py:233-248): work
+    that outlasts it raises HangDetected naming the workers, the dispatch
+    stays pending, and a later wait collects it once the worker finishes."""
+    session = start(1, wait_timeout_s=0.02)
+    session.trigger(1, WorkDescriptor(slot=0, iterations=60_000_000))
+    with pytest.raises(HangDetected) as ei:
+        session.wait(1)
+    assert ei.value.sm_ids == (0,)
+    assert session.pending_mask == 1
+    for _ in range(500):
+        try:
+            session.wait(1)
+            break
+        except HangDetected:
+            continue
+    else:
+        pytest.fail("the long task never finished")
+    assert session.pending_mask == 0
+    session.dispose()
+    assert_trace_ok(session)
