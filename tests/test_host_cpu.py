@@ -377,3 +377,24 @@ def test_profile_run_refuses_non_direct_configs():
     for cfg in (native.NativeConfig(poll_mode="gateway"), native.NativeConfig(record_trace=True)):
         with pytest.raises(errors.ConfigError):
             native.profile_run(cfg, 10)
+
+
+def test_illegal_word_injection_into_a_b200_trace_is_detected():
+    """Criterion 7's injection check (T/test_acceptance.py:168-176,
+    T/test_protocol.py:277-291) on the device trace recorded on a B200: an
+    illegal word at a random position is caught by the oracle replay and by
+    the product validator, at or before that position."""
+    import random
+    from oracle import protocol as O
+    _, recs = _gpu_trace_records()
+    writes = [(r.side, r.sm_id, r.word) for r in recs]
+    rng = random.Random(20250808)
+    for _ in range(60):
+        idx = rng.randrange(len(writes))
+        side, sm, _ = writes[idx]
+        bad = list(writes)
+        bad[idx] = (side, sm, rng.choice([3, 5, 9, 13, 15]))
+        v = O.replay(bad).violation          # (index, reason)
+        assert v is not None and v[0] <= idx
+        pv = protocol.validate_trace(bad)
+        assert pv is not None and pv.index <= idx
