@@ -38,6 +38,7 @@ typedef struct {
   PyTypeObject* work_type;
   PyObject* ph_trigger;
   PyObject* ph_wait;
+  int keep_gil;          /* lk_trigger cannot spin (no lazy ack, no event ring): skip the GIL round trip */
 } Fast;
 
 static PyObject* g_zero;
@@ -59,12 +60,14 @@ static void fast_dealloc(Fast* f) {
 static int fast_init(Fast* f, PyObject* args, PyObject* kw) {
   unsigned long long h, trig, wt;
   unsigned int nwords;
+  int keep_gil = 0;
   PyObject *staged, *cache, *rows, *limit, *tt, *wtp, *pt, *pw;
   (void)kw;
-  if (!PyArg_ParseTuple(args, "KIKKO!O!O!O!O!O!UU", &h, &nwords, &trig, &wt, &PyDict_Type, &staged,
+  if (!PyArg_ParseTuple(args, "KIKKO!O!O!O!O!O!UU|p", &h, &nwords, &trig, &wt, &PyDict_Type, &staged,
                         &PyDict_Type, &cache, &PyList_Type, &rows, &PyLong_Type, &limit, &PyType_Type, &tt,
-                        &PyType_Type, &wtp, &pt, &pw))
+                        &PyType_Type, &wtp, &pt, &pw, &keep_gil))
     return -1;
+  f->keep_gil = keep_gil;
   if (!h || !trig || !wt || nwords == 0) {
     PyErr_SetString(PyExc_ValueError, "null handle or entry point");
     return -1;
@@ -182,9 +185,13 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
   const uint64_t* m = (const uint64_t*)PyBytes_AS_STRING(mb);
   uint64_t ns = 0;
   int rc;
-  Py_BEGIN_ALLOW_THREADS
-  rc = f->trig(f->h, m, f->nwords, (uint32_t)sl, NULL, &ns);
-  Py_END_ALLOW_THREADS
+  if (f->keep_gil) {   /* a few stores and checks under the session mutex: ~100 ns */
+    rc = f->trig(f->h, m, f->nwords, (uint32_t)sl, NULL, &ns);
+  } else {
+    Py_BEGIN_ALLOW_THREADS
+    rc = f->trig(f->h, m, f->nwords, (uint32_t)sl, NULL, &ns);
+    Py_END_ALLOW_THREADS
+  }
   Py_DECREF(mb);
   if (rc) return PyLong_FromLong(rc);
   return record(f, f->ph_trigger, ns, mask);

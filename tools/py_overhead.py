@@ -36,6 +36,15 @@ for trial in range(3):
         trig(h, m, nw, 0, None, ur)
         wait(h, m, nw, ur)
     raw_ns = (time.perf_counter_ns() - t0) / N
+    # the CPython fast object directly (no Python method frame around it)
+    f = s._fast
+    t0 = time.perf_counter_ns()
+    for k in range(N):
+        m = 1 << (k % n)
+        f.trigger(m, w)
+        f.wait(m)
+    fast_ns = (time.perf_counter_ns() - t0) / N
+    s.timings.clear()
     # API
     t0 = time.perf_counter_ns()
     for k in range(N):
@@ -44,6 +53,7 @@ for trial in range(3):
         s.wait(m)
     api_ns = (time.perf_counter_ns() - t0) / N
     s.timings.clear()
-    print(f"per task: C loop {c_ns:7.0f} ns | bare ctypes {raw_ns:7.0f} ns | API {api_ns:7.0f} ns", flush=True)
+    print(f"per task: C loop {c_ns:7.0f} ns | bare ctypes {raw_ns:7.0f} ns | _lkfast direct {fast_ns:7.0f} ns | "
+          f"API {api_ns:7.0f} ns", flush=True)
 s.dispose()
 s.close()
