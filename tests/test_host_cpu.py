@@ -398,3 +398,25 @@ def test_illegal_word_injection_into_a_b200_trace_is_detected():
         assert v is not None and v[0] <= idx
         pv = protocol.validate_trace(bad)
         assert pv is not None and pv.index <= idx
+
+
+def test_committed_bench_line_keeps_the_contract():
+    """The bench line committed under profiles/ carries every key the driver
+    and the judge read (bench contract), with the roofline and baseline
+    objects complete."""
+    import json
+    d = json.loads((ROOT / "profiles" / "r01_bench_line.json").read_text())
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "cpu_baseline", "clocks",
+              "gpu_launches"):
+        assert k in d, k
+    assert d["warmup"] >= 3 and d["n_gpus"] >= 1 and d["value"] > 0 and "workload" in d["config"]
+    assert set(d["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
+    assert set(d["roofline"]) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
+    assert abs(d["roofline"]["frac"] - d["roofline"]["achieved"] / d["roofline"]["peak"]) < 1e-3
+    assert set(d["cpu_baseline"]) >= {"value", "unit", "cores", "kind", "sample"}
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    assert d["gpu_launches"] >= 1
+    r = json.loads((ROOT / "profiles" / "r01_bench_reference_line.json").read_text())
+    assert r["impl"] == "reference" and r["metric"] == d["metric"] and r["unit"] == d["unit"]
+    assert set(r["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
