@@ -227,3 +227,36 @@ def test_cpu_port_matches_live_reference_projection(reference):
     port.dispose()
     ref_w = [(r.side, r.sm_id, r.word) for r in rs.recorded_trace()]
     assert projection.projections(ref_w, 2) == projection.projections(port.writes(), 2)
+
+
+# ---------------------------------------------------------------- properties
+
+def test_product_state_machine_walks_match_the_oracle():
+    """Property check beyond the goldens (hypothesis): random walks of words
+    -- legal ones, gap words, slots up to MAX_SLOT -- through the product's
+    __host__ __device__ state machine and through the reference-pinned
+    oracle give the same phase, slot, publish and action at every step, and
+    a violation at the same step.  A begun item is completed the way the
+    worker completes it (complete_work) before the walk goes on."""
+    hypothesis = pytest.importorskip("hypothesis")
+    st = hypothesis.strategies
+    words = st.one_of(st.sampled_from([O.NOP, O.EXIT, 0, 1, 2, 3, 5, 9, 15]),
+                      st.integers(O.WORK_BASE, O.WORK_BASE + 40),
+                      st.integers(O.WORK_BASE, 0xFFFFFFFF))
+
+    @hypothesis.settings(max_examples=400, deadline=None)
+    @hypothesis.given(st.lists(words, min_size=1, max_size=40))
+    def walk(seq):
+        case = {"phase": O.BOOT, "slot": None}
+        for w in seq:
+            case["word"] = w
+            want, got = _oracle_step(case), _product_step(case)
+            assert got == want, (case, got, want)
+            if "violation" in want or want["action"] == "exit":
+                return
+            if want["action"] is not None:   # began work: the worker completes it
+                ph, sl, _pub, _ = O.complete(want["phase"], want["slot"])
+                case = {"phase": ph, "slot": sl}
+            else:
+                case = {"phase": want["phase"], "slot": want["slot"]}
+    walk()
