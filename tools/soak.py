@@ -1,0 +1,55 @@
+"""Soak: one session (default config) runs mixed traffic for `minutes`
+(default 5) -- round-robin and single-worker empty tasks from C, full-mask
+dispatches, Python-API round robin, saxpy payloads checked against the
+oracle -- and reports any error, the rounds done and the worst latencies."""
+import sys
+import time
+
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+
+from oracle import work as W  # noqa: E402
+from paper_2310_01212_b200 import host, native  # noqa: E402
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
+
+minutes = float(sys.argv[1]) if len(sys.argv) > 1 else 5.0
+native.pin_host_thread(0)
+s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN))
+n = s.num_workers
+empty = WorkDescriptor(slot=0, kind="empty")
+s.register(empty)
+rr = [1 << i for i in range(n)]
+full = host.full_mask(n)
+k = 1 << 20
+rng = np.random.default_rng(0)
+x = rng.uniform(-1, 1, k).astype(np.float32)
+y0 = rng.uniform(-1, 1, k).astype(np.float32)
+dx, dy = DeviceBuffer.from_array(x), DeviceBuffer.from_array(y0)
+sax = WorkDescriptor(slot=1, kind="saxpy_f32", data_in_ref=(dx, dy), data_out_ref=dy, alpha=1.0)
+rounds, worst, payloads = 0, 0, 0
+deadline = time.monotonic() + 60 * minutes
+while time.monotonic() < deadline:
+    _, done, cyc = s.bench_roundtrip(rr, 0, 100_000)
+    rounds += len(done)
+    worst = max(worst, int(cyc.max()))
+    _, done, cyc = s.bench_roundtrip([1, 2], 0, 20_000)
+    rounds += len(done)
+    _, done, cyc = s.bench_roundtrip([full], 0, 2_000)
+    rounds += len(done)
+    for j in range(2_000):
+        m = rr[j % n]
+        s.trigger(m, empty)
+        s.wait(m)
+    rounds += 2_000
+    s.timings.clear()
+    dy.upload(y0)
+    s.trigger(full, sax)
+    s.wait(full)
+    np.testing.assert_array_equal(dy.download(np.float32, k).view(np.uint32), W.saxpy_f32(1.0, x, y0).view(np.uint32))
+    payloads += 1
+s.dispose()
+s.close()
+dx.free()
+dy.free()
+print(f"soak {minutes:.1f} min: {rounds} handshakes, {payloads} checked saxpy dispatches, no error; "
+      f"worst round-robin cycle {worst / 1e3:.1f} us", flush=True)
