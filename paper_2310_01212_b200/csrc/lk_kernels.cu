@@ -695,7 +695,7 @@ __device__ __forceinline__ void idle_adapt(const lk_dev_args& a, Elected& e) {
   e.idle_armed = false;
   if (a.replicas != 1 || (a.flags & LK_CF_ACK_FIXED)) return;
   if (e.nload == 1) e.idle_cyc -= e.idle_cyc >> 8;
-  else if (e.nload == 2) e.idle_cyc = min(e.idle_cyc + kIdleStepCyc, kIdleMaxCyc);
+  else if (e.nload == 2) e.idle_cyc = min(e.idle_cyc + kIdleStepCyc, max(kIdleMaxCyc, a.idle_delay_cyc));
 }
 
 // The two transitions every empty-task round trip makes, settled in place
