@@ -69,7 +69,9 @@ extern "C" {
 
 /* to_gpu hint bits (top byte of a cell; set by the host from the staged
  * descriptor of the slot a WORK word names) */
-#define LK_HINT_EMPTY  1u   /* the slot holds an EMPTY descriptor: no descriptor fetch */
+#define LK_HINT_EMPTY  1u   /* the slot holds no work (EMPTY, or busy_loop of 0 iterations): no descriptor fetch */
+#define LK_HINT_CACHED 2u   /* every masked worker last fetched this slot at its current stage version:
+                               reuse the cached descriptor (and trigger mask), no fetch */
 
 /* descriptor flags */
 #define LK_DF_SCALAR   1u   /* pointers not 16-B aligned: scalar path */

@@ -267,6 +267,10 @@ struct lk_session {
   std::vector<uint64_t> ack_pending;                      // nwords, under mu
   std::vector<uint8_t> registered;                        // per slot
   std::vector<lk_desc> reg_desc;                          // host copy per slot
+  // descriptor caching (LK_HINT_CACHED): a slot's stage version goes up with
+  // every upload; each worker's last fetched (slot, version)
+  std::vector<uint32_t> slot_ver;                         // per slot
+  std::vector<uint32_t> wslot, wver;                      // per worker
   std::vector<std::vector<uint64_t>> reg_mask;            // per slot (nwords)
   bool disposed = false;
   bool kernel_done = false;
@@ -645,6 +649,9 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->scratch.assign(s->nwords, 0);
   s->ack_pending.assign(s->nwords, 0);
   s->reg_desc.resize(cfg.num_slots);
+  s->slot_ver.assign(cfg.num_slots, 0);
+  s->wslot.assign(s->nw, 0xFFFFFFFFu);
+  s->wver.assign(s->nw, 0);
   s->reg_mask.resize(cfg.num_slots);
   s->host_seq.assign(s->nw, 0);
   s->host_times.assign(3 * size_t(s->nw), 0);
@@ -920,6 +927,7 @@ static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* d, const ui
                           cudaMemcpyHostToDevice, s->copy_stream));
   LK_CUDA(cudaStreamSynchronize(s->copy_stream));  // in place before any WORK word names it
   s->registered[slot] = 1;
+  ++s->slot_ver[slot];   // workers' cached copies of this slot are stale now
   s->reg_desc[slot] = *d;
   s->reg_mask[slot] = std::move(m);
   return LK_OK;
@@ -972,9 +980,24 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
     return fail(LK_E_USAGE, "descriptor slot %u not registered", slot);
   }
   const uint32_t word = LK_WORK_BASE + slot;
-  const uint32_t hint = s->reg_desc[slot].kind == LK_KIND_EMPTY ? LK_HINT_EMPTY : 0u;
+  // a busy_loop of 0 iterations (the reference's default WorkDescriptor,
+  // P/device.py:48-66) is an empty task: the worker may skip the fetch too
+  const lk_desc& rd = s->reg_desc[slot];
+  const bool no_work = rd.kind == LK_KIND_EMPTY || (rd.kind == LK_KIND_BUSY_LOOP && rd.iterations == 0);
+  uint32_t hint = no_work ? LK_HINT_EMPTY : 0u;
+  const uint32_t ver = s->slot_ver[slot];
+  if (!no_work) {   // every masked worker fetched this slot version last: it may reuse its copy
+    bool cached = true;
+    for (uint32_t i : ids) cached &= s->wslot[i] == slot && s->wver[i] == ver;
+    if (cached) hint |= LK_HINT_CACHED;
+  }
   if (!s->post(ids, word, hint)) return fail(LK_E_HANG, "event ring full: gateway not consuming");
   const uint64_t t1 = now_ns();
+  if (!no_work)
+    for (uint32_t i : ids) {   // what each worker now holds (fetched, or reused)
+      s->wslot[i] = slot;
+      s->wver[i] = ver;
+    }
   for (uint32_t i : ids) {
     s->host_times[3 * i] = t_call;
     s->host_times[3 * i + 1] = t1;
@@ -1180,6 +1203,7 @@ extern "C" int lk_read_cells(lk_session* s, uint32_t* to_gpu, uint32_t* from_gpu
 extern "C" int lk_debug_poke(lk_session* s, uint32_t worker, uint32_t word) {
   if (!s || worker >= s->nw) return fail(LK_E_USAGE, "bad worker");
   std::lock_guard<std::mutex> g(s->mu);
+  s->wslot[worker] = 0xFFFFFFFFu;   // a poked WORK may refill the worker's descriptor cache
   s->post(std::vector<uint32_t>{worker}, word);
   return LK_OK;
 }

@@ -529,6 +529,8 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
 // (a special-register read ptxas may neither fold nor hoist) and folds it into
 // a value the caller keeps live, so the trip count is really executed -- an
 // empty asm body in the loop lets ptxas compute the count and drop the loop.
+// Kept out of line: inlined into the poll loop's fast path, the loop was
+// dropped (the fast-path test caught it: 32 cycles for 10^5 iterations).
 __device__ __noinline__ uint32_t busy_loop(uint64_t iterations) {
   uint32_t acc = 0;
   for (uint64_t i = 0; i < iterations; ++i) {
@@ -597,6 +599,9 @@ struct Elected {           // thread 0's private protocol state
   uint32_t dseq, rseq;     // HYBRID: writes seen on the direct cell / via the event ring
   uint32_t tcnt;
   uint32_t nload;          // DIRECT: cell loads issued since the ack wait began
+  uint32_t cslot;          // slot of the cached descriptor (sm.cdesc), or ~0
+  uint32_t ckind;          // its kind and iterations, for the cached single-thread fast path
+  uint64_t citer;
   uint32_t ack_cyc;        // DIRECT, 1 replica: this worker's current ack delay (adapted, see ack_adapt)
   bool dirty;              // cur not yet stepped to a fixed point
   bool idle_pub;           // just published NOP (ack consumed): the host may trigger this worker next
@@ -711,6 +716,28 @@ enum FastResult : uint32_t { kFastNone = 0, kFastSettled = 1, kFastBegin = 2 };
 __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid, Elected& e) {
   if (a.record_trace | (a.flags & LK_CF_FENCE_ALWAYS)) return kFastNone;
   const uint32_t w = e.cur;
+  if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && (e.hint & LK_HINT_CACHED) &&
+      w - LK_WORK_BASE == e.cslot && single_thread_kind(e.ckind)) {
+    // a cached busy_loop/empty item: run it right here, like an empty task
+    const uint64_t c_begin = clock64();
+    publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
+    if (e.ckind == LK_KIND_BUSY_LOOP) {
+      const uint32_t r = busy_loop(e.citer);
+      asm volatile("" ::"r"(r));   // the count is consumed: the loop must run
+    }
+    publish_fast(a, wid, LK_FINISHED, LK_PHASE_FINISHED);
+    const uint64_t c_fin = clock64();
+    e.st = lk_wstate{LK_PHASE_FINISHED, w - LK_WORK_BASE};
+    e.pub = LK_FINISHED;
+    e.dirty = false;
+    idle_adapt(a, e);
+    unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
+    tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
+    if (a.flags & LK_CF_TIMELINE) {
+      tl[0] = e.t_seen; tl[4] = e.t_fwd; tl[8] = globaltimer();
+    }
+    return kFastSettled;
+  }
   if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && !(e.hint & LK_HINT_EMPTY) &&
       w - LK_WORK_BASE < a.num_slots) {
     // IDLE x WORK(s) of any other kind: publish WORKING and begin at once; the
@@ -1112,6 +1139,8 @@ struct PersistSmem {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint32_t tile[kMaxStages], ring_g;
   unsigned long long chan[2];      // HYBRID: latest direct-cell value, latest mailbox value
+  lk_desc cdesc;                   // this worker's last fetched descriptor (LK_HINT_CACHED)
+  unsigned long long cmask[4];     // ... and its slot's trigger mask
   uint32_t stop;                   // HYBRID: the protocol thread left its loop
   uint32_t sink;                   // keeps busy_loop's result live
 };
@@ -1154,6 +1183,9 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.rseq = 0;
   e.tcnt = 0;
   e.nload = 0;
+  e.cslot = 0xFFFFFFFFu;
+  e.ckind = 0;
+  e.citer = 0;
   e.ack_cyc = a.ack_delay_cyc;
   e.idle_pub = false;
   e.idle_armed = false;
@@ -1183,10 +1215,16 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
           write_timeline(a, wid, e, t_b, t_b, c_begin_e, clock64(), tl);
           continue;
         }
-        // descriptor and the slot's trigger mask in one L2 round trip
+        // descriptor and the slot's trigger mask: reused from this worker's
+        // cache when the host says it is current (LK_HINT_CACHED; the slot is
+        // checked too), else one L2 round trip, which refills the cache
         lk_desc d;
         unsigned long long mk[4] = {0ull, 0ull, 0ull, 0ull};
-        {
+        if ((e.hint & LK_HINT_CACHED) && e.cslot == slot) {
+          d = sm.cdesc;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mk[k] = sm.cmask[k];
+        } else {
           const uint4* src = reinterpret_cast<const uint4*>(a.desc + slot);
           uint4* dst = reinterpret_cast<uint4*>(&d);
           const unsigned long long* m = a.slot_mask + uint64_t(slot) * a.nwords;
@@ -1195,6 +1233,12 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (uint32_t(k) < a.nwords) mk[k] = ld_cg64(m + k);
+          sm.cdesc = d;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) sm.cmask[k] = mk[k];
+          e.cslot = slot;
+          e.ckind = d.kind;
+          e.citer = d.iterations;
         }
         if (d.kind >= LK_KIND_COUNT) { report_error(a, wid, e, LK_WERR_BAD_KIND, slot + LK_WORK_BASE); sm.cmd = kCmdExit; break; }
         if (single_thread_kind(d.kind)) {

@@ -695,3 +695,40 @@ def test_wait_timeout_raises_hang_then_a_later_wait_completes():
     assert session.pending_mask == 0
     session.dispose()
     assert_trace_ok(session)
+
+
+def test_cached_descriptor_fast_path_runs_the_work():
+    """LK_HINT_CACHED: re-dispatching the same staged busy_loop descriptor to
+    the same worker skips the descriptor fetch and runs the loop on the fast
+    path -- the iterations still all execute, a restaged slot is fetched
+    again, and the handshakes stay legal."""
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=2, spin_strategy=native.PURE_SPIN))
+    _LIVE.append(s)
+    cyc = {}
+    for n in (100_000, 1_000_000):
+        w = WorkDescriptor(slot=3, iterations=n)
+        for rep in range(3):                      # rep 0 fetches, reps 1-2 reuse the cache
+            s.trigger(1, w)
+            s.wait(1)
+            t = s.last_timeline().astype(np.int64)
+            cyc[(n, rep)] = int(t[0, 7] - t[0, 6])
+    for n in (100_000, 1_000_000):
+        for rep in range(3):
+            assert cyc[(n, rep)] >= n, cyc
+    assert cyc[(1_000_000, 2)] > 5 * cyc[(100_000, 2)], cyc
+    # payload kinds through the cache: same descriptor and mask twice, both exact
+    from oracle import work as W
+    from paper_2310_01212_b200.device import DeviceBuffer
+    a = np.arange(4096, dtype=np.int32)
+    da, db, do = DeviceBuffer.from_array(a), DeviceBuffer.from_array(a), DeviceBuffer(4 * 4096)
+    try:
+        w = WorkDescriptor(slot=5, kind="vector_add_i32", data_in_ref=(da, db), data_out_ref=do)
+        for rep in range(2):
+            do.upload(np.zeros(4096, dtype=np.int32))
+            s.trigger(0b11, w)
+            s.wait(0b11)
+            np.testing.assert_array_equal(do.download(np.int32, 4096), W.vector_add_i32(a, a))
+    finally:
+        for b in (da, db, do):
+            b.free()
+    s.dispose()
