@@ -716,6 +716,7 @@ def test_cached_descriptor_fast_path_runs_the_work():
         for rep in range(3):
             assert cyc[(n, rep)] >= n, cyc
     assert cyc[(1_000_000, 2)] > 5 * cyc[(100_000, 2)], cyc
+    assert cyc[(1_000_000, 0)] > 5 * cyc[(100_000, 2)], cyc   # restaged slot 3: no stale copy
     # payload kinds through the cache: same descriptor and mask twice, both exact
     from oracle import work as W
     from paper_2310_01212_b200.device import DeviceBuffer
