@@ -164,10 +164,10 @@ def _make_fast(session: "NativeSession", raw):
         log.debug("_lkfast not built: trigger/wait use ctypes only")
         return None
     addr = lambda fn: C.cast(fn, C.c_void_p).value  # noqa: E731
-    # lk_trigger spins only to settle a lazy ack or on a full event ring;
-    # otherwise it is ~100 ns of stores and checks, and keeping the GIL beats
-    # releasing and re-taking it
-    keep_gil = session.cfg.poll_mode == "direct" and not session.cfg.lazy_ack
+    # keep_gil=False: lk_trigger drops the GIL like every other call.  Holding
+    # it across the ~100-ns call measured within noise (tools/ab_gil.py)
+    # and would stall other Python threads if the call ever spun.
+    keep_gil = False
     return _lkfast.Fast(session._h.value, session.nwords, addr(raw.lk_trigger), addr(raw.lk_wait),
                         session._staged, session._mask_cache, session._timings._rows,
                         1 << session.num_workers, PhaseTiming, WorkDescriptor, PHASE_TRIGGER, PHASE_WAIT, keep_gil)
