@@ -783,6 +783,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.gw_tail = const_cast<unsigned long long*>(s->gw_tail);
   a.dmb = s->d_dmb;
   a.exited = s->d_exited;
+  a.sink = s->d_exited + 64;   // same zeroed page, its own 128-B line
   a.ring_entries = s->ring_entries;
   a.dmb_u64 = 16;
   a.nw = s->nw;

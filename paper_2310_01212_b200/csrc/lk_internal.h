@@ -32,6 +32,7 @@ struct lk_dev_args {
   unsigned long long* gw_tail;     // host-mapped: events the gateway has consumed
   unsigned long long* dmb;         // device mailboxes (GATEWAY), worker i at dmb[i*dmb_u64]
   uint32_t* exited;                // device: workers that left their loop
+  uint32_t* sink;                  // device (own line): busy_loop results of the fast path land here
   uint32_t ring_entries;           // entries per event-ring replica
   uint32_t dmb_u64;
   uint32_t nw;                     // workers

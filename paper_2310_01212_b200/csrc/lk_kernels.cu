@@ -529,9 +529,12 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
 // (a special-register read ptxas may neither fold nor hoist) and folds it into
 // a value the caller keeps live, so the trip count is really executed -- an
 // empty asm body in the loop lets ptxas compute the count and drop the loop.
-// Kept out of line: inlined into the poll loop's fast path, the loop was
-// dropped (the fast-path test caught it: 32 cycles for 10^5 iterations).
-__device__ __noinline__ uint32_t busy_loop(uint64_t iterations) {
+// Inline, so the cached fast path pays no call into cold code; every caller
+// stores the result to global memory (a.sink, the baseline's counter line):
+// an unused result -- or one stored only to shared memory -- lets ptxas
+// drop the whole loop (the fast-path test caught that: 32 cycles for 10^5
+// iterations).
+__device__ __forceinline__ uint32_t busy_loop(uint64_t iterations) {
   uint32_t acc = 0;
   for (uint64_t i = 0; i < iterations; ++i) {
     uint32_t c;
@@ -721,10 +724,7 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
     // a cached busy_loop/empty item: run it right here, like an empty task
     const uint64_t c_begin = clock64();
     publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
-    if (e.ckind == LK_KIND_BUSY_LOOP) {
-      const uint32_t r = busy_loop(e.citer);
-      asm volatile("" ::"r"(r));   // the count is consumed: the loop must run
-    }
+    if (e.ckind == LK_KIND_BUSY_LOOP) *a.sink = busy_loop(e.citer);   // stored: the loop must run
     publish_fast(a, wid, LK_FINISHED, LK_PHASE_FINISHED);
     const uint64_t c_fin = clock64();
     e.st = lk_wstate{LK_PHASE_FINISHED, w - LK_WORK_BASE};
@@ -1142,7 +1142,6 @@ struct PersistSmem {
   lk_desc cdesc;                   // this worker's last fetched descriptor (LK_HINT_CACHED)
   unsigned long long cmask[4];     // ... and its slot's trigger mask
   uint32_t stop;                   // HYBRID: the protocol thread left its loop
-  uint32_t sink;                   // keeps busy_loop's result live
 };
 
 __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(const __grid_constant__ lk_dev_args a) {
@@ -1245,7 +1244,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
           const bool tl = (a.flags & LK_CF_TIMELINE) != 0;
           c_begin = clock64();
           t_begin = tl ? globaltimer() : 0;
-          if (d.kind == LK_KIND_BUSY_LOOP) sm.sink = busy_loop(d.iterations);
+          if (d.kind == LK_KIND_BUSY_LOOP) *a.sink = busy_loop(d.iterations);   // global store: the loop must run
           const uint64_t t_end = tl ? globaltimer() : 0;
           const lk_step_out o = lk_complete_work(e.st);
           publish(a, wid, e, o.publish, (a.flags & LK_CF_FENCE_ALWAYS) != 0);
@@ -1308,7 +1307,9 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   if (single_thread_kind(d.kind)) {
-    if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) rs.last = busy_loop(d.iterations);
+    // the result goes to global memory (the counter line's spare word), which
+    // ptxas cannot treat as dead; a dead shared store would let it drop the loop
+    if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) ctr[3] = busy_loop(d.iterations);
     return;
   }
   Ring ring{dyn_smem, full, empty, kDefaultStages, nullptr, nullptr};   // static tiles only
