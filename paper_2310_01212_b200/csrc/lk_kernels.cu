@@ -527,14 +527,15 @@ __device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t 
 
 // native.py:63-67 counts to `iterations`.  Each iteration here reads %clock
 // (a special-register read ptxas may neither fold nor hoist) and folds it into
-// a value the caller keeps live, so the trip count is really executed -- an
-// empty asm body in the loop lets ptxas compute the count and drop the loop.
-// Inline, so the cached fast path pays no call into cold code; every caller
-// stores the result to global memory (a.sink, the baseline's counter line):
-// an unused result -- or one stored only to shared memory -- lets ptxas
-// drop the whole loop (the fast-path test caught that: 32 cycles for 10^5
-// iterations).
-__device__ __forceinline__ uint32_t busy_loop(uint64_t iterations) {
+// a value the caller stores to global memory (a.sink, the baseline's counter
+// line), so the trip count is really executed: an unused result, or one only
+// stored to shared memory, lets ptxas drop the loop.  One out-of-line copy
+// serves every call site -- the persistent kernel's fast and general paths
+// and the baseline kernel -- so an iteration costs the same everywhere and
+// LK and launch+sync run the same work in the same time (table2).  Inlined
+// copies were unrolled differently per site (2x apart in time per
+// iteration).
+__device__ __noinline__ uint32_t busy_loop(uint64_t iterations) {
   uint32_t acc = 0;
   for (uint64_t i = 0; i < iterations; ++i) {
     uint32_t c;
