@@ -9,9 +9,13 @@
  *   - a WorkDescriptor object already staged in its slot for this worker set,
  *   - the timing row appended to session.timings (host.TimingLog rows), and
  *     an equal PhaseTiming returned.
- * Anything else returns None and native.py takes its Python path, which
- * holds the full rules (validation messages, staging, foreign descriptors).
- * A failing C call returns its LK_E_* code (an int) for native.py to raise.
+ * Anything else goes to the session's Python path (slow_trigger/slow_wait,
+ * called with the session from a weak reference), which holds the full rules
+ * (validation messages, staging, foreign descriptors).  A failing C call is
+ * raised through `raiser(rc, mask, is_wait)`.  native.py binds the two
+ * methods as the session's own `trigger`/`wait`, so a task costs no Python
+ * frame at all on the common path.  (Without the slow-path arguments a
+ * decline returns None and an error its LK_E_* code, for the caller.)
  *
  * The two entry points are passed in as addresses taken from the ctypes
  * handle of liblk.so, so this module and ctypes share one loaded library
@@ -39,6 +43,10 @@ typedef struct {
   PyObject* ph_trigger;
   PyObject* ph_wait;
   int keep_gil;          /* lk_trigger cannot spin (no lazy ack, no event ring): skip the GIL round trip */
+  PyObject* slow_trigger;   /* NativeSession._trigger_slow (unbound) or NULL */
+  PyObject* slow_wait;      /* NativeSession._wait_slow (unbound) or NULL */
+  PyObject* wref;           /* weak reference to the session (no reference cycle) */
+  PyObject* raiser;         /* raiser(rc, mask, is_wait) raises the LK_E_* code's exception */
 } Fast;
 
 static PyObject* g_zero;
@@ -54,6 +62,10 @@ static void fast_dealloc(Fast* f) {
   Py_XDECREF(f->work_type);
   Py_XDECREF(f->ph_trigger);
   Py_XDECREF(f->ph_wait);
+  Py_XDECREF(f->slow_trigger);
+  Py_XDECREF(f->slow_wait);
+  Py_XDECREF(f->wref);
+  Py_XDECREF(f->raiser);
   Py_TYPE(f)->tp_free((PyObject*)f);
 }
 
@@ -62,12 +74,23 @@ static int fast_init(Fast* f, PyObject* args, PyObject* kw) {
   unsigned int nwords;
   int keep_gil = 0;
   PyObject *staged, *cache, *rows, *limit, *tt, *wtp, *pt, *pw;
+  PyObject *st = NULL, *sw = NULL, *wr = NULL, *rs = NULL;
   (void)kw;
-  if (!PyArg_ParseTuple(args, "KIKKO!O!O!O!O!O!UU|p", &h, &nwords, &trig, &wt, &PyDict_Type, &staged,
+  if (!PyArg_ParseTuple(args, "KIKKO!O!O!O!O!O!UU|pOOOO", &h, &nwords, &trig, &wt, &PyDict_Type, &staged,
                         &PyDict_Type, &cache, &PyList_Type, &rows, &PyLong_Type, &limit, &PyType_Type, &tt,
-                        &PyType_Type, &wtp, &pt, &pw, &keep_gil))
+                        &PyType_Type, &wtp, &pt, &pw, &keep_gil, &st, &sw, &wr, &rs))
     return -1;
   f->keep_gil = keep_gil;
+  if (st && sw && wr && rs) {
+    if (!PyWeakref_CheckRef(wr)) {
+      PyErr_SetString(PyExc_TypeError, "session must come as a weak reference");
+      return -1;
+    }
+    Py_INCREF(st); Py_XSETREF(f->slow_trigger, st);
+    Py_INCREF(sw); Py_XSETREF(f->slow_wait, sw);
+    Py_INCREF(wr); Py_XSETREF(f->wref, wr);
+    Py_INCREF(rs); Py_XSETREF(f->raiser, rs);
+  }
   if (!h || !trig || !wt || nwords == 0) {
     PyErr_SetString(PyExc_ValueError, "null handle or entry point");
     return -1;
@@ -144,15 +167,43 @@ static PyObject* record(Fast* f, PyObject* phase, uint64_t ns, PyObject* mask) {
   return t;
 }
 
+/* The Python path for what the C path declines (None without one). */
+static PyObject* decline(Fast* f, PyObject* slow, PyObject* const* args, Py_ssize_t nargs) {
+  if (!slow) Py_RETURN_NONE;
+  PyObject* sess = PyWeakref_GetObject(f->wref);   /* borrowed */
+  if (!sess) return NULL;
+  if (sess == Py_None) {
+    PyErr_SetString(PyExc_ReferenceError, "session is gone");
+    return NULL;
+  }
+  PyObject* callargs[3] = {sess, args[0], nargs > 1 ? args[1] : NULL};
+  Py_INCREF(sess);
+  PyObject* r = PyObject_Vectorcall(slow, callargs, (size_t)(nargs + 1), NULL);
+  Py_DECREF(sess);
+  return r;
+}
+
+/* A failing C call: raised through the session's raiser (its LK_E_* code as an
+ * int without one). */
+static PyObject* failed(Fast* f, int rc, PyObject* mask, int is_wait) {
+  if (!f->raiser) return PyLong_FromLong(rc);
+  PyObject* r = PyObject_CallFunction(f->raiser, "iOi", rc, mask, is_wait);
+  if (r) {   /* the raiser must raise */
+    Py_DECREF(r);
+    PyErr_Format(PyExc_RuntimeError, "LK error %d", rc);
+  }
+  return NULL;
+}
+
 static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
   if (nargs != 2) {
     PyErr_SetString(PyExc_TypeError, "trigger(mask, work)");
     return NULL;
   }
   PyObject *mask = args[0], *work = args[1];
-  if (Py_TYPE(work) != f->work_type) Py_RETURN_NONE;
+  if (Py_TYPE(work) != f->work_type) return decline(f, f->slow_trigger, args, nargs);
   PyObject* mb = mask_words(f, mask);
-  if (!mb) Py_RETURN_NONE;
+  if (!mb) return decline(f, f->slow_trigger, args, nargs);
   PyObject* slot = PyObject_GetAttr(work, s_slot);
   if (!slot) {
     Py_DECREF(mb);
@@ -164,12 +215,12 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
   if (PyErr_Occurred()) {
     PyErr_Clear();
     Py_DECREF(mb);
-    Py_RETURN_NONE;
+    return decline(f, f->slow_trigger, args, nargs);
   }
   if (!st || !PyTuple_CheckExact(st) || PyTuple_GET_SIZE(st) != 3 || PyTuple_GET_ITEM(st, 0) != work ||
       sl > 0xFFFFFFFFul) {
     Py_DECREF(mb);
-    Py_RETURN_NONE;
+    return decline(f, f->slow_trigger, args, nargs);
   }
   /* staged for this worker set: key is the mask for payload kinds, else 0
    * (the entry is held across the comparisons, which could run Python code) */
@@ -180,7 +231,7 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
   if (same != 1) {
     PyErr_Clear();
     Py_DECREF(mb);
-    Py_RETURN_NONE;
+    return decline(f, f->slow_trigger, args, nargs);
   }
   const uint64_t* m = (const uint64_t*)PyBytes_AS_STRING(mb);
   uint64_t ns = 0;
@@ -193,7 +244,7 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
     Py_END_ALLOW_THREADS
   }
   Py_DECREF(mb);
-  if (rc) return PyLong_FromLong(rc);
+  if (rc) return failed(f, rc, mask, 0);
   return record(f, f->ph_trigger, ns, mask);
 }
 
@@ -204,7 +255,7 @@ static PyObject* fast_wait(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
   }
   PyObject* mask = args[0];
   PyObject* mb = mask_words(f, mask);
-  if (!mb) Py_RETURN_NONE;
+  if (!mb) return decline(f, f->slow_wait, args, nargs);
   const uint64_t* m = (const uint64_t*)PyBytes_AS_STRING(mb);
   uint64_t ns = 0;
   int rc;
@@ -212,7 +263,7 @@ static PyObject* fast_wait(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
   rc = f->wait(f->h, m, f->nwords, &ns);
   Py_END_ALLOW_THREADS
   Py_DECREF(mb);
-  if (rc) return PyLong_FromLong(rc);
+  if (rc) return failed(f, rc, mask, 1);
   return record(f, f->ph_wait, ns, mask);
 }
 

@@ -18,6 +18,7 @@ import ctypes as C
 import dataclasses
 import logging
 import time
+import weakref
 from dataclasses import dataclass
 from typing import Optional
 
@@ -168,9 +169,20 @@ def _make_fast(session: "NativeSession", raw):
     # it across the ~100-ns call measured within noise (tools/ab_gil.py)
     # and would stall other Python threads if the call ever spun.
     keep_gil = False
+    # declines go to the session's Python path (held weakly: the session owns
+    # the Fast object through its bound methods), errors to _raise_lk
     return _lkfast.Fast(session._h.value, session.nwords, addr(raw.lk_trigger), addr(raw.lk_wait),
                         session._staged, session._mask_cache, session._timings._rows,
-                        1 << session.num_workers, PhaseTiming, WorkDescriptor, PHASE_TRIGGER, PHASE_WAIT, keep_gil)
+                        1 << session.num_workers, PhaseTiming, WorkDescriptor, PHASE_TRIGGER, PHASE_WAIT, keep_gil,
+                        NativeSession._trigger_slow, NativeSession._wait_slow, weakref.ref(session), _raise_lk)
+
+
+def _raise_lk(rc: int, mask: int, is_wait: int) -> None:
+    """Raise the exception of an LK_E_* code from the fast path (as the Python
+    path would: a wait names its workers)."""
+    if is_wait:
+        _lib.raise_for(rc, sm_ids=tuple(sms_in_mask(mask)))
+    _lib.raise_for(rc)
 
 
 def _warn_lazy_loading() -> None:
@@ -223,7 +235,8 @@ class NativeSession:
         self._cells2 = (C.c_uint32 * num_workers)()
         self._cells3 = (C.c_uint32 * num_workers)()
         self._raw = raw
-        self._fast = _make_fast(self, raw)
+        self._fast = None
+        self._bind_fast()
 
     # -- bring-up ----------------------------------------------------------
 
@@ -319,7 +332,20 @@ class NativeSession:
         # type and point the C fast path at the new rows
         self._timings = v if isinstance(v, TimingLog) else TimingLog(v)
         if getattr(self, "_fast", None) is not None:
-            self._fast = _make_fast(self, self._raw)
+            self._bind_fast()
+
+    def _bind_fast(self) -> None:
+        """Serve `trigger`/`wait` from the CPython fast path: its methods become
+        this session's own attributes, so the common call runs no Python frame."""
+        self._fast = f = _make_fast(self, self._raw)
+        if f is not None:
+            self.__dict__["trigger"] = f.trigger
+            self.__dict__["wait"] = f.wait
+
+    def _unbind_fast(self) -> None:
+        self._fast = None
+        self.__dict__.pop("trigger", None)
+        self.__dict__.pop("wait", None)
 
     def _require_live(self) -> None:
         if self.disposed:
@@ -361,14 +387,17 @@ class NativeSession:
     # _is_staged, _timing) are inlined, which halves the wrapper's cost over
     # the bare ctypes calls (tools/py_overhead.py).  Semantics are the helpers'.
     def trigger(self, mask: int, work: WorkDescriptor) -> PhaseTiming:
-        """Dispatch: one word write per masked worker, no kernel launch."""
+        """Dispatch: one word write per masked worker, no kernel launch.
+
+        A live session normally answers this name from its instance: the
+        CPython fast path (csrc/lk_pyfast.c), which hands anything it does not
+        serve to _trigger_slow.  This method serves explicit class calls."""
         f = self._fast
-        if f is not None:   # staged descriptor, cached mask: all in C (csrc/lk_pyfast.c)
-            r = f.trigger(mask, work)
-            if r is not None:
-                if r.__class__ is PhaseTiming:
-                    return r
-                _lib.raise_for(r)
+        if f is not None:
+            return f.trigger(mask, work)
+        return self._trigger_slow(mask, work)
+
+    def _trigger_slow(self, mask: int, work: WorkDescriptor) -> PhaseTiming:
         if self.disposed:
             raise UsageError("session already disposed")
         if mask <= 0 or mask >> self.num_workers:
@@ -406,14 +435,14 @@ class NativeSession:
         return st is not None and st[0] is work and st[1] == key
 
     def wait(self, mask: int) -> PhaseTiming:
-        """Spin (in C) until every masked worker published FINISHED, then ack."""
+        """Spin (in C) until every masked worker published FINISHED, then ack.
+        (Served like trigger: the fast path, falling back to _wait_slow.)"""
         f = self._fast
         if f is not None:
-            r = f.wait(mask)
-            if r is not None:
-                if r.__class__ is PhaseTiming:
-                    return r
-                _lib.raise_for(r, sm_ids=tuple(sms_in_mask(mask)))
+            return f.wait(mask)
+        return self._wait_slow(mask)
+
+    def _wait_slow(self, mask: int) -> PhaseTiming:
         if self.disposed:
             raise UsageError("session already disposed")
         if mask <= 0 or mask >> self.num_workers:
@@ -465,7 +494,7 @@ class NativeSession:
         rc = self._lib.lk_dispose(self._h, C.byref(self._u64))
         _lib.check(rc, sm_ids=tuple(range(self.num_workers)))
         self.disposed = True
-        self._fast = None
+        self._unbind_fast()
         timing = PhaseTiming(PHASE_DISPOSE, self._u64.value, full_mask(self.num_workers))
         self.timings.append(timing)
         return timing
@@ -473,13 +502,13 @@ class NativeSession:
     def abort(self, timeout_s: float = 10.0) -> None:
         """Retire the kernel whatever the host state (dead worker, pending work)."""
         if self._h:
-            self._fast = None
+            self._unbind_fast()
             _lib.check(self._lib.lk_abort(self._h, int(timeout_s * 1e9)))
             self.disposed = True
 
     def close(self) -> None:
         """Dispose (or abort) if needed and free the runtime's memory."""
-        self._fast = None
+        self._unbind_fast()
         if self._h:
             if not self.disposed:
                 try:

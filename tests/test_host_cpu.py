@@ -309,37 +309,47 @@ def _fake_session(tmp_path, handle=1):
 
 
 def test_pyfast_path_matches_python_path(tmp_path):
+    """The C path serves staged descriptors with cached masks; everything it
+    declines goes to the Python path (same results, same errors), and the
+    session's trigger/wait are the C methods themselves."""
     s, lib = _fake_session(tmp_path)
     calls = C.c_uint32.in_dll(lib, "calls")
     w = WorkDescriptor(slot=3, kind="empty")
     s._staged[3] = (w, 0, False)
     m = (1 << 130) | 1
-    # first use: mask not cached -> Python path (which caches it)
-    t1 = s.trigger(m, w)
-    assert t1 == host.PhaseTiming(host.PHASE_TRIGGER, 1003, m) and calls.value == 1
-    assert s._fast.trigger(m, w) == host.PhaseTiming(host.PHASE_TRIGGER, 1003, m)   # now the C path serves it
+    # first use: mask not cached -> declined to the Python path (which caches it)
+    t1 = s._fast.trigger(m, w)
+    assert t1 == host.PhaseTiming(host.PHASE_TRIGGER, 1003, m) and calls.value == 1 and m in s._mask_cache
+    assert s._fast.trigger(m, w) == host.PhaseTiming(host.PHASE_TRIGGER, 1003, m)   # now served in C
     assert list((C.c_uint64 * 4).in_dll(lib, "last"))[:3] == [1, 0, 1 << 2]
     assert s._fast.wait(m) == host.PhaseTiming(host.PHASE_WAIT, 77, m)
     assert s.timings == [t1, t1, host.PhaseTiming(host.PHASE_WAIT, 77, m)]
     assert isinstance(s.timings[-1], host.PhaseTiming)
-    # the C path declines what the Python path must handle
-    w2 = WorkDescriptor(slot=3, kind="empty")          # equal fields, different object: restage
-    assert s._fast.trigger(m, w2) is None
-    assert s._fast.trigger(m, object()) is None        # not a WorkDescriptor
+    # declined cases take the Python path: restaging, foreign objects, bad masks
+    w2 = WorkDescriptor(slot=3, kind="empty")          # equal fields, different object
+    assert s._fast.trigger(m, w2).cycles == 1003 and s._staged[3][0] is w2
+    with pytest.raises(errors.UsageError):
+        s._fast.trigger(m, object())                   # not a work descriptor
     s._mask_cache[0] = bytes(24)
     s._mask_cache[1 << 148] = bytes(24)
-    assert s._fast.wait(0) is None                     # empty mask: the reference's error message
-    assert s._fast.wait(1 << 148) is None              # wider than the workers
-    assert s._fast.wait(True) is None                  # not an exact int
-    pay = WorkDescriptor(slot=4, kind="empty")
-    s._staged[4] = (pay, m, True)                      # payload staged for mask m only
-    assert s._fast.trigger(m, pay) is not None
-    s._mask(1)
-    assert s._fast.trigger(1, pay) is None             # another worker set: restage
-    # invalid masks still raise the reference's errors through the wrapper
     with pytest.raises(errors.UsageError):
-        s.wait(0)
+        s._fast.wait(0)                                # the reference's empty-mask error
+    with pytest.raises(errors.UsageError):
+        s._fast.wait(1 << 148)                         # wider than the workers
+    pay = WorkDescriptor(slot=4, kind="empty")
+    s._staged[4] = (pay, m, True)                      # staged for mask m only
+    n = calls.value
+    s._mask(1)
+    s._fast.trigger(1, pay)                            # another worker set: restaged by the Python path
+    assert calls.value == n + 1 and s._staged[4] == (pay, 0, False)
+    # the bound methods: a session's trigger/wait are the C ones
+    s._bind_fast()
+    assert s.trigger.__self__ is s._fast and s.wait.__self__ is s._fast
+    assert s.trigger(m, w2).phase == host.PHASE_TRIGGER
+    s._unbind_fast()
+    assert "trigger" not in s.__dict__ and s.trigger.__func__ is type(s).trigger
     # rebinding timings keeps both paths appending to the new log
+    s._bind_fast()
     s.timings = []
     s.wait(m)
     assert len(s.timings) == 1 and s.timings[0].phase == host.PHASE_WAIT
@@ -351,11 +361,14 @@ def test_pyfast_error_codes_raise(tmp_path):
     w = WorkDescriptor(slot=0, kind="empty")
     s._staged[0] = (w, 0, False)
     s._mask(1)
-    assert s._fast.trigger(1, w) == _lib.LK_E_HANG
+    with pytest.raises(HangDetected):
+        s._fast.trigger(1, w)                         # C path, raised through _raise_lk
+    s._bind_fast()
     with pytest.raises(HangDetected):
         s.trigger(1, w)
-    with pytest.raises(HangDetected):
+    with pytest.raises(HangDetected) as ei:
         s.wait(1)
+    assert ei.value.sm_ids == (0,)
     assert len(s.timings) == 0
 
 
