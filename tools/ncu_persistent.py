@@ -8,6 +8,7 @@ so ncu's serialized launch returns.  Run as
 No second argument: round-robin empty tasks (configs[1] shape).  `saxpy`:
 full-mask saxpy_f32 dispatches, 64 MiB per vector, rotating over 4 buffer
 sets (512 MiB, L2-cold), for the in-situ DRAM traffic per dispatch.
+`reduce`: full-mask block_reduce_f32 over 64 MiB, rotating 8 buffers.
 Without ncu it prints the run's rate (a sanity check of the hook)."""
 import sys
 
@@ -16,7 +17,8 @@ from paper_2310_01212_b200 import native  # noqa: E402
 from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
 
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
-payload = len(sys.argv) > 2 and sys.argv[2] == "saxpy"
+kind = sys.argv[2] if len(sys.argv) > 2 else ""
+payload = kind in ("saxpy", "reduce")
 native.pin_host_thread(0)
 if not payload:
     ns = native.profile_run(native.NativeConfig(), rounds)
@@ -25,13 +27,19 @@ if not payload:
 else:
     n = (64 << 20) // 4
     bufs, works = [], []
-    for k in range(4):
-        x, y = DeviceBuffer(4 * n), DeviceBuffer(4 * n)
-        bufs += [x, y]
-        works.append(WorkDescriptor(slot=1 + k, kind="saxpy_f32", data_in_ref=(x, y), data_out_ref=y, alpha=1.5))
+    for k in range(4 if kind == "saxpy" else 8):
+        if kind == "saxpy":
+            x, y = DeviceBuffer(4 * n), DeviceBuffer(4 * n)
+            bufs += [x, y]
+            works.append(WorkDescriptor(slot=1 + k, kind="saxpy_f32", data_in_ref=(x, y), data_out_ref=y, alpha=1.5))
+        else:
+            x, part, tot = DeviceBuffer(4 * n), DeviceBuffer(4 * 160), DeviceBuffer(8)
+            bufs += [x, part, tot]
+            works.append(WorkDescriptor(slot=1 + k, kind="block_reduce_f32", data_in_ref=x, data_out_ref=part,
+                                        total_ref=tot))
     ns = native.profile_run(native.NativeConfig(), rounds, works)
-    alg = 12 * n
-    print(f"profile run: {rounds} full-mask saxpy_f32 dispatches (64 MiB/vector) in {ns / 1e6:.2f} ms = "
+    alg = (12 if kind == "saxpy" else 4) * n
+    print(f"profile run: {rounds} full-mask {works[0].kind} dispatches (64 MiB/vector) in {ns / 1e6:.2f} ms = "
           f"{rounds * alg / ns:.1f} GB/s including handshakes; algorithmic bytes/dispatch {alg}", flush=True)
     for b in bufs:
         b.free()
