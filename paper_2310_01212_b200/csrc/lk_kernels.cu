@@ -707,11 +707,15 @@ __device__ __forceinline__ void idle_adapt(const lk_dev_args& a, Elected& e) {
   else if (e.nload == 2) e.idle_cyc = min(e.idle_cyc + kIdleStepCyc, max(kIdleMaxCyc, a.idle_delay_cyc));
 }
 
-// The two transitions every empty-task round trip makes, settled in place
-// right where the new value was seen (no descriptor fetch, no trip through
-// the general dispatch code and its cold instruction-cache lines):
-//   IDLE x WORK(s), slot s staged EMPTY (hint) -> publish WORKING, FINISHED;
-//      re-stepping the same word in FINISHED publishes FINISHED again (a no-op)
+// The transitions of a short round trip, settled in place right where the
+// new value was seen (no descriptor fetch, no trip through the general
+// dispatch code and its cold instruction-cache lines):
+//   IDLE x WORK(s), slot s cached (LK_HINT_CACHED) as busy_loop/empty -> publish
+//      WORKING, run the loop, publish FINISHED;
+//   IDLE x WORK(s), slot s holds no work (LK_HINT_EMPTY) -> publish WORKING,
+//      FINISHED; re-stepping the same word in FINISHED publishes FINISHED
+//      again (a no-op);
+//   IDLE x WORK(s) of a payload kind -> publish WORKING and begin at once;
 //   FINISHED x NOP -> publish NOP, IDLE; re-stepping NOP in IDLE is a no-op.
 // Exactly lk_worker_step + lk_complete_work for these cases (protocol.py:151-206);
 // anything else -- and every case while a trace is recorded -- takes settle().
