@@ -36,6 +36,10 @@ for mode in ("direct", "hybrid", "gateway"):
         line(f"{mode:8s} {nw:3d} workers round robin", done, cyc)
         _, done, cyc = s.bench_roundtrip([host.full_mask(nw)], 0, 20000)
         line(f"{mode:8s} {nw:3d} workers full mask", done, cyc)
+        if nw == 148:
+            s.bench_roundtrip([1], 0, 5000)
+            _, done, cyc = s.bench_roundtrip([1], 0, 100000)
+            line(f"{mode:8s} {nw:3d} workers, one re-triggered", done, cyc)
         s.dispose()
         s.close()
 b = native.LaunchSyncBaseline()
