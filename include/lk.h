@@ -165,6 +165,11 @@ typedef struct lk_config {
 #define LK_CF_NO_ACK_DELAY 128u  /* DIRECT, 1 replica: poll for the ack right after FINISHED
                                     (lk_config.ack_delay_ns) */
 #define LK_CF_ACK_FIXED    256u  /* keep ack_delay_ns as configured (no per-worker adaptation) */
+#define LK_CF_HOST_DESC    512u  /* DIRECT only: the descriptor table and slot masks live in the pinned
+                                    mapped host block (workers fetch them with sys-scope loads after an
+                                    acquire poll), so register/trigger/wait make no CUDA call at all: a
+                                    session stays usable while a profiler that serialises launches (ncu)
+                                    holds the runtime inside the persistent kernel's launch */
 #define LK_CF_LAZY_ACK      16u  /* lk_wait returns once the NOP ack is written; the next trigger or
                                     dispose touching that worker waits for its republished NOP */
 
@@ -275,6 +280,14 @@ int lk_validate_trace(const uint32_t* side, const int64_t* sm_id, const uint32_t
 int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks,
                        uint32_t nwords, uint32_t slot, uint64_t rounds,
                        uint64_t* trig_ns, uint64_t* done_ns, uint64_t* cycle_ns);
+/* The same loop, plus gap_ns[k] = the largest gap between consecutive TSC
+ * reads of the calling thread within round k's spins: microseconds there
+ * mean the host thread was not running (interrupt, tick, vCPU preemption),
+ * which attributes a slow round to the host rather than the link or GPU. */
+int lk_bench_roundtrip_gaps(lk_session* s, const uint64_t* masks, uint32_t nmasks,
+                            uint32_t nwords, uint32_t slot, uint64_t rounds,
+                            uint64_t* trig_ns, uint64_t* done_ns, uint64_t* cycle_ns,
+                            uint64_t* gap_ns);
 /* A profiling run of the persistent kernel itself: boots a DIRECT session
  * whose handshakes come from a host thread started before the kernel launch
  * and tears it down.  The thread runs `rounds` dispatches, then EXIT: with
@@ -297,6 +310,23 @@ int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t 
  * FINISHED issued, 9 globaltimer when the NOP ack was seen, 10 cell loads
  * issued in between, 11 clock64 when the NOP ack was seen. */
 int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n);
+/* Launch+sync floor: the cheapest conventional per-task flow, an empty
+ * <<<1,32,0>>> kernel joined by stream sync (LK_FLOOR_SYNC), by a host spin
+ * on cudaStreamQuery (LK_FLOOR_QUERY), or launched as a one-node CUDA graph
+ * (LK_FLOOR_GRAPH); spin_sched != 0 sets cudaDeviceScheduleSpin first.
+ * total_ns[k]: launch call start -> completion observed; launch_ns[k]: the
+ * launch call.  Replaces ThreadSpawnBaseline.launch/wait (native.py:304-331). */
+#define LK_FLOOR_SYNC  0u
+#define LK_FLOOR_QUERY 1u
+#define LK_FLOOR_GRAPH 2u
+int lk_launch_floor_bench(int device, uint32_t mode, uint32_t spin_sched, uint64_t rounds, uint64_t* total_ns,
+                          uint64_t* launch_ns);
+/* Per-worker count of to_gpu values the kernel's fast path settled in place
+ * (IDLE x WORK of an empty / cached single-thread item, IDLE x WORK begin of
+ * a payload item, FINISHED x NOP) since boot -- the path configs[1] times.
+ * With record_trace on, those steps append the same trace records as the
+ * general path.  Replaces no reference call: test/bench evidence only. */
+int lk_fast_count(lk_session* s, uint32_t* counts, uint32_t n);
 /* Host side of the same dispatches (CLOCK_MONOTONIC ns, t[3*i+k]): k=0
  * trigger call start, 1 WORK word written, 2 FINISHED observed by wait. */
 int lk_last_host_times(lk_session* s, uint64_t* t, uint32_t n);

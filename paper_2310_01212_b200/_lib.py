@@ -45,6 +45,10 @@ CF_ACK_WINDOW = 32
 CF_DYNAMIC_TILES = 64
 CF_NO_ACK_DELAY = 128
 CF_ACK_FIXED = 256
+CF_HOST_DESC = 512
+FLOOR_SYNC = 0
+FLOOR_QUERY = 1
+FLOOR_GRAPH = 2
 POLL_DIRECT = 0
 POLL_GATEWAY = 1
 POLL_HYBRID = 2
@@ -148,10 +152,13 @@ SIGNATURES = {
     "lk_protocol_complete": (I32, [PU32, PU32, PU32, PU32]),
     "lk_validate_trace": (I32, [P, P, P, U64, PI64, C.c_char_p, U32, PU64, U32, PU32]),
     "lk_bench_roundtrip": (I32, [P, MASK, U32, U32, U32, U64, P, P, P]),
+    "lk_bench_roundtrip_gaps": (I32, [P, MASK, U32, U32, U32, U64, P, P, P, P]),
     "lk_profile_run": (I32, [C.POINTER(lk_config), P, U32, U64, C.POINTER(C.c_uint64)]),
     "lk_last_spans": (I32, [P, P, P, U32]),
     "lk_last_timeline": (I32, [P, P, U32]),
     "lk_last_host_times": (I32, [P, P, U32]),
+    "lk_fast_count": (I32, [P, P, U32]),
+    "lk_launch_floor_bench": (I32, [I32, U32, U32, U64, P, P]),
     "lk_clock_offset": (I32, [I32, U32, PI64, PU64]),
     "lk_sm_topology": (I32, [I32, C.POINTER(C.c_int32), U32, PU32]),
     "lk_pingpong": (I32, [I32, U64, P]),

@@ -252,6 +252,8 @@ struct lk_session {
   uint32_t* d_exited = nullptr;
   lk_dev_trace* d_trace = nullptr;
   uint32_t* d_tcnt = nullptr;
+  uint32_t* d_fast = nullptr;      // per-worker fast-path counts (lk_fast_count)
+  bool host_desc = false;          // LK_CF_HOST_DESC: d_desc / d_mask point into host_block
 
   // host bookkeeping (guarded by mu)
   std::mutex mu;
@@ -274,6 +276,16 @@ struct lk_session {
   std::vector<std::vector<uint64_t>> reg_mask;            // per slot (nwords)
   bool disposed = false;
   bool kernel_done = false;
+  // The cooperative launch is issued from this thread.  Normally it returns
+  // at once; under a profiler that serialises launches (ncu) it returns only
+  // when the kernel exits, so the session's API keeps running meanwhile.
+  // launch_state: 0 launch call not returned yet, 1 launched, -1 failed.
+  std::thread launcher;
+  std::atomic<int> launch_state{0};
+  cudaError_t launch_err = cudaSuccess;
+  void join_launcher() {
+    if (launcher.joinable()) launcher.join();
+  }
   bool claimed = true;             // holds the device's one-session claim until the kernel retired
   void release_claim();
   uint64_t t_create = 0;
@@ -396,6 +408,14 @@ static int require_live(lk_session* s) {
 
 static int kernel_status(lk_session* s) {
   if (s->kernel_done) return 1;
+  const int ls = s->launch_state.load(std::memory_order_acquire);
+  if (ls == 0) return 0;     // launch call still inside the driver (or a profiler): resident
+  if (ls < 0) {
+    s->kernel_done = true;
+    fail(LK_E_CUDA, "cooperative launch: %s", cudaGetErrorString(s->launch_err));
+    return -1;
+  }
+  cudaSetDevice(s->device);
   CtxScope cs(s->part.ca);
   cudaError_t q = cudaStreamQuery(s->stream);
   if (q == cudaErrorNotReady) return 0;
@@ -442,12 +462,51 @@ struct Spinner {
   }
 };
 
+// Host-preemption probe (lk_bench_roundtrip_gaps): the largest gap between
+// consecutive TSC reads of the calling thread's spin loops in a round.  A
+// spinning iteration takes tens of ns, so a gap of microseconds means the
+// thread was not running: an interrupt, a timer tick or a vCPU preemption.
+struct GapProbe {
+  uint64_t last = 0, max = 0;
+};
+static thread_local GapProbe* t_gap = nullptr;
+
+static inline uint64_t tsc() {
+#if defined(__x86_64__)
+  return __rdtsc();
+#else
+  return now_ns();
+#endif
+}
+
+static inline void gap_tick() {
+  GapProbe* g = t_gap;
+  if (!g) return;
+  const uint64_t t = tsc();
+  if (g->last && t - g->last > g->max) g->max = t - g->last;
+  g->last = t;
+}
+
+// TSC ticks per ns, calibrated once against CLOCK_MONOTONIC over 20 ms.
+static double tsc_per_ns() {
+  static double r = 0.0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const uint64_t c0 = tsc(), n0 = now_ns();
+    usleep(20000);
+    const uint64_t c1 = tsc(), n1 = now_ns();
+    r = n1 > n0 ? double(c1 - c0) / double(n1 - n0) : 1.0;
+  });
+  return r;
+}
+
 // Spin until word(i) == want for every id.  Returns LK_OK, LK_E_HANG or
 // LK_E_WORKER_DIED.
 static int spin_words(lk_session* s, const std::vector<uint32_t>& ids, uint32_t want, const char* what) {
   Spinner sp(s);
   size_t j = 0;
   while (j < ids.size()) {
+    gap_tick();
     if (s->word(ids[j]) == want) {
       ++j;
       continue;
@@ -581,6 +640,10 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.wait_timeout_ns == 0) cfg.wait_timeout_ns = 10ull * 1000000000ull;
   if (cfg.ack_delay_ns == 0) cfg.ack_delay_ns = 300;
   if (cfg.tma_min_workers == 0) cfg.tma_min_workers = 49;
+  if ((cfg.flags & LK_CF_HOST_DESC) && cfg.poll_mode != LK_POLL_DIRECT)
+    return fail(LK_E_CONFIG, "host-resident descriptors (LK_CF_HOST_DESC) need DIRECT polling");
+  // the WORK word's poll must be an acquire for the host-written descriptor to be visible after it
+  if (cfg.flags & LK_CF_HOST_DESC) cfg.flags |= LK_CF_ACQUIRE_POLL;
   if (cfg.ack_delay_ns > 100000 || cfg.idle_delay_ns > 100000)
     return fail(LK_E_CONFIG, "ack_delay_ns and idle_delay_ns must be at most 100000");
 
@@ -683,7 +746,10 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   const size_t cells = al(size_t(s->nw) * cfg.status_stride);
   const size_t err_words = (size_t(s->nw) + 15) / 16 * 16;   // err[] then err_any on its own line
   const size_t errb = al(err_words * 8 + 128), smidb = al(size_t(s->nw) * 4);
-  const size_t host_bytes = tob + cells + errb + smidb;
+  const bool host_desc = (cfg.flags & LK_CF_HOST_DESC) != 0;
+  const size_t hdescb = host_desc ? al(size_t(cfg.num_slots) * sizeof(lk_desc)) : 0;
+  const size_t hmaskb = host_desc ? al(size_t(cfg.num_slots) * ((s->nw + 63) / 64) * 8) : 0;
+  const size_t host_bytes = tob + cells + errb + smidb + hdescb + hmaskb;
   cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&s->host_block), host_bytes,
                                  cudaHostAllocMapped | cudaHostAllocPortable);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(ce)));
@@ -695,6 +761,11 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->err = reinterpret_cast<volatile unsigned long long*>(s->host_block + tob + cells);
   s->smid = reinterpret_cast<volatile uint32_t*>(s->host_block + tob + cells + errb);
   s->err_any = reinterpret_cast<volatile uint32_t*>(s->err + err_words);
+  if (host_desc) {   // mapped + UVA: the host pointer is the device pointer
+    s->d_desc = reinterpret_cast<lk_desc*>(s->host_block + tob + cells + errb + smidb);
+    s->d_mask = reinterpret_cast<unsigned long long*>(s->host_block + tob + cells + errb + smidb + hdescb);
+    s->host_desc = true;
+  }
   for (uint32_t i = 0; i < s->nw; ++i) {
     for (uint32_t k = 0; k < s->replicas; ++k) {
       if (k < s->dreps && (!s->gateway || s->hybrid))
@@ -713,21 +784,26 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   const size_t exb = al(4);
   const size_t traceb = cfg.record_trace ? al(size_t(s->nw) * cfg.trace_capacity * sizeof(lk_dev_trace)) : 0;
   const size_t tcntb = al(size_t(s->nw) * 4);
-  const size_t dev_bytes = descb + maskb + ctrb + spanb + dmbb + exb + traceb + tcntb;
+  const size_t fastb = al(size_t(s->nw) * 4);
+  const size_t dev_bytes = descb + maskb + ctrb + spanb + dmbb + exb + traceb + tcntb + fastb;
   ce = dev_alloc(reinterpret_cast<void**>(&s->dev_block), dev_bytes);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "device alloc: %s", cudaGetErrorString(ce)));
   ce = cudaMemsetAsync(s->dev_block, 0, dev_bytes, svc_stream());
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(svc_stream());  // zeroed before the kernel reads it
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "memset: %s", cudaGetErrorString(ce)));
   uint8_t* p = s->dev_block;
-  s->d_desc = reinterpret_cast<lk_desc*>(p); p += descb;
-  s->d_mask = reinterpret_cast<unsigned long long*>(p); p += maskb;
+  if (!s->host_desc) {
+    s->d_desc = reinterpret_cast<lk_desc*>(p);
+    s->d_mask = reinterpret_cast<unsigned long long*>(p + descb);
+  }
+  p += descb + maskb;
   s->d_ctr = reinterpret_cast<uint32_t*>(p); p += ctrb;
   s->d_spans = reinterpret_cast<unsigned long long*>(p); p += spanb;
   s->d_dmb = reinterpret_cast<unsigned long long*>(p); p += dmbb;
   s->d_exited = reinterpret_cast<uint32_t*>(p); p += exb;
   s->d_trace = traceb ? reinterpret_cast<lk_dev_trace*>(p) : nullptr; p += traceb;
-  s->d_tcnt = reinterpret_cast<uint32_t*>(p);
+  s->d_tcnt = reinterpret_cast<uint32_t*>(p); p += tcntb;
+  s->d_fast = reinterpret_cast<uint32_t*>(p);
 
   ce = cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking);
   if (ce != cudaSuccess) return cleanup(fail(LK_E_CUDA, "stream: %s", cudaGetErrorString(ce)));
@@ -769,6 +845,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.spans = s->d_spans;
   a.trace = s->d_trace;
   a.trace_cnt = s->d_tcnt;
+  a.fast_cnt = s->d_fast;
   a.cell_u64 = s->cell_u64;
   a.status_u64 = s->status_u64;
   a.replicas = s->replicas;
@@ -815,7 +892,20 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     if (src) return cleanup(src);
     driver = std::thread(profile_driver, s, pr);
   }
-  {
+  if (!pr) {
+    // the launch runs on its own thread (see lk_session::launcher); the boot
+    // wait below watches both the workers and the launch's outcome
+    s->launcher = std::thread([s, a, launch_threads] {
+      cudaSetDevice(s->device);
+      cudaError_t e;
+      {
+        CtxScope cs(s->part.ca);
+        e = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);
+      }
+      s->launch_err = e;
+      s->launch_state.store(e == cudaSuccess ? 1 : -1, std::memory_order_release);
+    });
+  } else {
     CtxScope cs(s->part.ca);
     ce = lk_launch_persistent(a, s->nw, launch_threads, s->smem, s->stream);
   }
@@ -836,7 +926,6 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
     g_last_error = msg;
     return rc;
   }
-  if (ce != cudaSuccess) return cleanup(fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(ce)));
 
   // --- boot: every worker publishes INIT then NOP (native.py:113-118)
   // A failed boot frees the session only once the kernel has retired (the
@@ -848,13 +937,25 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
       s->post(s->all_ids, LK_EXIT);
       const uint64_t until = now_ns() + std::min<uint64_t>(cfg.wait_timeout_ns, 2000000000ull);
       while (kernel_status(s) == 0 && now_ns() < until) usleep(50);
-      if (kernel_status(s) == 0) return rc;
+      if (kernel_status(s) == 0) {
+        s->launcher.detach();   // still inside the launch call: leaked with the session
+        return rc;
+      }
     }
+    s->join_launcher();
     return cleanup(rc);
   };
   const uint64_t deadline = now_ns() + cfg.wait_timeout_ns;
   for (uint32_t i = 0; i < s->nw;) {
     if (s->word(i) == LK_NOP && s->phase(i) == LK_PHASE_IDLE) { ++i; continue; }
+    if (s->launch_state.load(std::memory_order_acquire) < 0) {
+      const int rc = fail(LK_E_INIT, "cooperative launch: %s", cudaGetErrorString(s->launch_err));
+      const std::string msg = g_last_error;
+      s->join_launcher();
+      cleanup(rc);
+      g_last_error = msg;
+      return rc;
+    }
     if (s->err[i]) {
       const int rc = fail(LK_E_INIT, "worker %u failed during boot", i);
       const std::string msg = g_last_error;
@@ -917,16 +1018,47 @@ static inline bool multi_worker_kind(uint32_t kind) {
 
 // Stage desc (+ the worker set that shards it) in the slot; a no-op when the
 // device copy is already identical.  Caller holds s->mu.
-static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* d, const uint64_t* mask, uint32_t nwords) {
+// A C caller's descriptor is checked and normalised before it reaches the
+// device: payload pointers must be 4-B aligned (element size) and non-null,
+// pointers that are not 16-B aligned take the scalar path (cp.async.bulk and
+// ld.global.v4 would fault on them), and the reduce's total is a double.
+static int normalise_desc(const lk_desc* in, lk_desc* out) {
+  *out = *in;
+  if (!multi_worker_kind(in->kind)) return LK_OK;
+  const bool two = in->kind == LK_KIND_VECTOR_ADD_I32 || in->kind == LK_KIND_SAXPY_F32;
+  if (in->n && (!in->in0 || !in->out || (two && !in->in1)))
+    return fail(LK_E_USAGE, "work kind %u needs non-null input and output pointers", in->kind);
+  const uint64_t any = in->in0 | in->in1 | in->out;
+  if (any & 3) return fail(LK_E_USAGE, "payload pointers must be 4-byte aligned");
+  if (in->aux & 7) return fail(LK_E_USAGE, "the reduce total pointer must be 8-byte aligned");
+  if (any & 15) out->flags |= LK_DF_SCALAR;
+  return LK_OK;
+}
+
+static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* din, const uint64_t* mask, uint32_t nwords) {
+  lk_desc dn;
+  int nrc = normalise_desc(din, &dn);
+  if (nrc) return nrc;
+  const lk_desc* d = &dn;
   std::vector<uint64_t> m(s->nwords, 0);
   if (mask && multi_worker_kind(d->kind))
     for (uint32_t k = 0; k < nwords && k < s->nwords; ++k) m[k] = mask[k];
   if (s->registered[slot] && memcmp(&s->reg_desc[slot], d, sizeof(lk_desc)) == 0 && s->reg_mask[slot] == m)
     return LK_OK;
-  LK_CUDA(cudaMemcpyAsync(s->d_desc + slot, d, sizeof(lk_desc), cudaMemcpyHostToDevice, s->copy_stream));
-  LK_CUDA(cudaMemcpyAsync(s->d_mask + uint64_t(slot) * s->nwords, m.data(), 8 * s->nwords,
-                          cudaMemcpyHostToDevice, s->copy_stream));
-  LK_CUDA(cudaStreamSynchronize(s->copy_stream));  // in place before any WORK word names it
+  if (s->host_desc) {
+    // plain stores into the mapped table; the WORK word that names the slot
+    // is written later with release semantics, and the worker polls it with
+    // an acquire load before fetching (LK_CF_HOST_DESC)
+    memcpy(s->d_desc + slot, d, sizeof(lk_desc));
+    memcpy(s->d_mask + uint64_t(slot) * s->nwords, m.data(), 8 * s->nwords);
+    std::atomic_thread_fence(std::memory_order_release);
+  } else {
+    LK_CUDA(cudaSetDevice(s->device));
+    LK_CUDA(cudaMemcpyAsync(s->d_desc + slot, d, sizeof(lk_desc), cudaMemcpyHostToDevice, s->copy_stream));
+    LK_CUDA(cudaMemcpyAsync(s->d_mask + uint64_t(slot) * s->nwords, m.data(), 8 * s->nwords,
+                            cudaMemcpyHostToDevice, s->copy_stream));
+    LK_CUDA(cudaStreamSynchronize(s->copy_stream));  // in place before any WORK word names it
+  }
   s->registered[slot] = 1;
   ++s->slot_ver[slot];   // workers' cached copies of this slot are stale now
   s->reg_desc[slot] = *d;
@@ -979,6 +1111,19 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
     if (rc) return rc;
   } else if (!s->registered[slot]) {
     return fail(LK_E_USAGE, "descriptor slot %u not registered", slot);
+  } else if (multi_worker_kind(s->reg_desc[slot].kind)) {
+    // a payload shards by the trigger mask: workers derive rank and count
+    // from the mask staged with the slot, so a different mask re-stages it
+    // (else chunks would be skipped or done twice, and the reduce's arrival
+    // count would never close)
+    const std::vector<uint64_t>& rm = s->reg_mask[slot];
+    bool same = true;
+    for (uint32_t k = 0; k < s->nwords; ++k) same &= rm[k] == (k < nwords ? mask[k] : 0ull);
+    if (!same) {
+      const lk_desc cur = s->reg_desc[slot];
+      rc = stage_locked(s, slot, &cur, mask, nwords);
+      if (rc) return rc;
+    }
   }
   const uint32_t word = LK_WORK_BASE + slot;
   // a busy_loop of 0 iterations (the reference's default WorkDescriptor,
@@ -1080,14 +1225,25 @@ extern "C" int lk_wait(lk_session* s, const uint64_t* mask, uint32_t nwords, uin
   return wait_impl(s, mask, nwords, ids, finished_ns, 0, nullptr);
 }
 
-extern "C" int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks, uint32_t nwords,
-                                  uint32_t slot, uint64_t rounds, uint64_t* trig_ns, uint64_t* done_ns,
-                                  uint64_t* cycle_ns) {
+static int bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks, uint32_t nwords, uint32_t slot,
+                           uint64_t rounds, uint64_t* trig_ns, uint64_t* done_ns, uint64_t* cycle_ns,
+                           uint64_t* gap_ns) {
   if (!s || !masks || nmasks == 0) return fail(LK_E_USAGE, "null argument");
   std::vector<uint32_t> ids;
   ids.reserve(s->nw);
+  GapProbe gp;
+  const double tpn = gap_ns ? tsc_per_ns() : 1.0;
+  struct Unset {
+    ~Unset() { t_gap = nullptr; }
+  } unset;
+  if (gap_ns) t_gap = &gp;
   for (uint64_t k = 0; k < rounds; ++k) {
     const uint64_t* m = masks + (k % nmasks) * uint64_t(nwords);
+    if (gap_ns) {
+      gp.max = 0;
+      gp.last = 0;
+      gap_tick();
+    }
     const uint64_t t0 = now_ns();
     uint64_t el = 0;
     int rc;
@@ -1103,8 +1259,25 @@ extern "C" int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t
     if (trig_ns) trig_ns[k] = el;
     if (done_ns) done_ns[k] = done_abs - t0;
     if (cycle_ns) cycle_ns[k] = t2 - t0;
+    if (gap_ns) {
+      gap_tick();
+      gap_ns[k] = uint64_t(double(gp.max) / tpn);
+    }
   }
   return LK_OK;
+}
+
+extern "C" int lk_bench_roundtrip(lk_session* s, const uint64_t* masks, uint32_t nmasks, uint32_t nwords,
+                                  uint32_t slot, uint64_t rounds, uint64_t* trig_ns, uint64_t* done_ns,
+                                  uint64_t* cycle_ns) {
+  return bench_roundtrip(s, masks, nmasks, nwords, slot, rounds, trig_ns, done_ns, cycle_ns, nullptr);
+}
+
+extern "C" int lk_bench_roundtrip_gaps(lk_session* s, const uint64_t* masks, uint32_t nmasks, uint32_t nwords,
+                                       uint32_t slot, uint64_t rounds, uint64_t* trig_ns, uint64_t* done_ns,
+                                       uint64_t* cycle_ns, uint64_t* gap_ns) {
+  if (!gap_ns) return fail(LK_E_USAGE, "null gap array");
+  return bench_roundtrip(s, masks, nmasks, nwords, slot, rounds, trig_ns, done_ns, cycle_ns, gap_ns);
 }
 
 // ------------------------------------------------------------------ dispose
@@ -1129,6 +1302,7 @@ extern "C" int lk_dispose(lk_session* s, uint64_t* elapsed_ns) {
     if (now_ns() > deadline) return fail(LK_E_HANG, "persistent kernel did not exit");
     usleep(20);
   }
+  s->join_launcher();
   s->disposed = true;
   s->release_claim();
   if (elapsed_ns) *elapsed_ns = now_ns() - t0;
@@ -1142,6 +1316,7 @@ extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
   if (!s) return fail(LK_E_USAGE, "null session");
   std::lock_guard<std::mutex> g(s->mu);
   if (s->kernel_done || kernel_status(s) != 0) {   // already retired (or failed): nothing to tell
+    s->join_launcher();
     s->disposed = true;
     s->release_claim();
     return LK_OK;
@@ -1154,6 +1329,7 @@ extern "C" int lk_abort(lk_session* s, uint64_t timeout_ns) {
     if (now_ns() > deadline) return fail(LK_E_HANG, "persistent kernel did not exit after abort");
     usleep(50);
   }
+  s->join_launcher();
   s->disposed = true;
   s->release_claim();
   return LK_OK;
@@ -1168,6 +1344,8 @@ extern "C" int lk_destroy(lk_session* s) {
       return fail(LK_E_HANG, "persistent kernel still resident; resources leaked");
     }
   }
+  s->join_launcher();
+  cudaSetDevice(s->device);
   cudaFreeHost(s->host_block);
   dev_free(s->dev_block);
   {
@@ -1248,6 +1426,15 @@ extern "C" int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n) {
   const uint32_t m = std::min(n, s->nw);
   LK_CUDA(cudaMemcpyAsync(t, s->d_spans, size_t(m) * 8 * LK_TIMELINE_WORDS, cudaMemcpyDeviceToHost,
                           s->copy_stream));
+  LK_CUDA(cudaStreamSynchronize(s->copy_stream));
+  return LK_OK;
+}
+
+extern "C" int lk_fast_count(lk_session* s, uint32_t* counts, uint32_t n) {
+  if (!s || !counts) return fail(LK_E_USAGE, "null argument");
+  const uint32_t m = std::min(n, s->nw);
+  LK_CUDA(cudaSetDevice(s->device));
+  LK_CUDA(cudaMemcpyAsync(counts, s->d_fast, size_t(m) * 4, cudaMemcpyDeviceToHost, s->copy_stream));
   LK_CUDA(cudaStreamSynchronize(s->copy_stream));
   return LK_OK;
 }
@@ -1620,6 +1807,63 @@ extern "C" int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_
   LK_CUDA(cudaEventElapsedTime(&ms, b->e0, b->e1));
   *avg_ms = ms / float(reps);
   return LK_OK;
+}
+
+// The fastest conventional launch+sync this host can do, per task: an empty
+// <<<1, 32, 0>>> kernel (no shared memory, no arguments) on a non-blocking
+// stream, joined by
+//   LK_FLOOR_SYNC:  cudaStreamSynchronize
+//   LK_FLOOR_QUERY: a host spin on cudaStreamQuery (no driver wait primitive)
+//   LK_FLOOR_GRAPH: the kernel as a one-node CUDA graph, cudaGraphLaunch +
+//                   cudaStreamSynchronize
+// with the device's host-wait policy set to cudaDeviceScheduleSpin first when
+// `spin_sched` (process-wide; the primary context takes the flag while live).
+// total_ns[k] = launch call start -> task observed complete; launch_ns[k] =
+// the launch call alone.  Replaces ThreadSpawnBaseline.launch/wait
+// (P/native.py:304-331) at its cheapest.
+extern "C" int lk_launch_floor_bench(int device, uint32_t mode, uint32_t spin_sched, uint64_t rounds,
+                                     uint64_t* total_ns, uint64_t* launch_ns) {
+  if (mode > LK_FLOOR_GRAPH) return fail(LK_E_USAGE, "unknown floor mode %u", mode);
+  LK_CUDA(cudaSetDevice(device));
+  if (spin_sched) LK_CUDA(cudaSetDeviceFlags(cudaDeviceScheduleSpin));
+  LK_CUDA(lk_preload_kernels());
+  cudaStream_t st;
+  LK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  int rc = LK_OK;
+  if (mode == LK_FLOOR_GRAPH) {
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) e = lk_launch_empty(st);
+    cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) rc = fail(LK_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  }
+  for (uint64_t k = 0; k < rounds && rc == LK_OK; ++k) {
+    const uint64_t t0 = now_ns();
+    cudaError_t e = mode == LK_FLOOR_GRAPH ? cudaGraphLaunch(exec, st) : lk_launch_empty(st);
+    const uint64_t t1 = now_ns();
+    if (e == cudaSuccess) {
+      if (mode == LK_FLOOR_QUERY) {
+        while ((e = cudaStreamQuery(st)) == cudaErrorNotReady) LK_PAUSE();
+      } else {
+        e = cudaStreamSynchronize(st);
+      }
+    }
+    const uint64_t t2 = now_ns();
+    if (e != cudaSuccess) {
+      rc = fail(LK_E_CUDA, "floor task: %s", cudaGetErrorString(e));
+      break;
+    }
+    if (launch_ns) launch_ns[k] = t1 - t0;
+    if (total_ns) total_ns[k] = t2 - t0;
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
 }
 
 extern "C" int lk_baseline_set_tma(lk_baseline* b, int on) {

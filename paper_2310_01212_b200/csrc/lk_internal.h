@@ -45,6 +45,7 @@ struct lk_dev_args {
   uint32_t tma_min_workers;        // payload dispatches to fewer workers take the LSU path
   lk_dev_trace* trace;             // device, num_workers * trace_cap
   uint32_t* trace_cnt;             // device, num_workers
+  uint32_t* fast_cnt;              // device, num_workers: values settled by the kernel's fast path
   uint32_t cell_u64;               // to_gpu cell stride in u64 (DIRECT cells and replicas)
   uint32_t status_u64;             // from_gpu status cell stride in u64
   uint32_t replicas;               // to_gpu replicas per worker: 1, 2, 4 or 8
@@ -70,6 +71,7 @@ cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_p
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads,
                            uint32_t* reduce_ctr, cudaStream_t st, int use_tma);
 size_t lk_ring_bytes(uint32_t stages);
+cudaError_t lk_launch_empty(cudaStream_t st);
 uint32_t lk_ring_max_stages();
 cudaError_t lk_launch_pingpong(volatile uint32_t* flag, volatile uint32_t* echo,
                                uint64_t rounds, cudaStream_t st);

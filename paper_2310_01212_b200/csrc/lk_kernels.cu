@@ -90,6 +90,12 @@ __device__ __forceinline__ uint4 ld_cg4(const uint4* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint4 ld_sys4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t ld_cg1(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -602,6 +608,7 @@ struct Elected {           // thread 0's private protocol state
   uint32_t hint;           // host hint bits of the current value (LK_HINT_*)
   uint32_t dseq, rseq;     // HYBRID: writes seen on the direct cell / via the event ring
   uint32_t tcnt;
+  uint32_t fhits;          // values settled by fast_step (mirrored to a.fast_cnt[wid])
   uint32_t nload;          // DIRECT: cell loads issued since the ack wait began
   uint32_t cslot;          // slot of the cached descriptor (sm.cdesc), or ~0
   uint32_t ckind;          // its kind and iterations, for the cached single-thread fast path
@@ -616,17 +623,22 @@ struct Elected {           // thread 0's private protocol state
   uint64_t t_fwd;          // GATEWAY + LK_CF_TIMELINE: globaltimer when the gateway forwarded it
 };
 
+// One device trace record: a value-changing from_gpu write, tagged with the
+// host write index it answers (P/native.py:135-140).  Both the general path
+// (publish) and the fast path (fast_step) record through here.
+__device__ __forceinline__ void trace_rec(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t word) {
+  lk_dev_trace* r = a.trace + uint64_t(wid) * a.trace_cap + (e.tcnt % a.trace_cap);
+  r->word = word;
+  r->hseq = e.seq;
+  r->t_ns = globaltimer();
+  ++e.tcnt;
+  a.trace_cnt[wid] = e.tcnt;
+  __threadfence();
+}
+
 __device__ __forceinline__ void publish(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t word,
                                         bool release) {
-  if (a.record_trace && word != e.pub) {
-    lk_dev_trace* r = a.trace + uint64_t(wid) * a.trace_cap + (e.tcnt % a.trace_cap);
-    r->word = word;
-    r->hseq = e.seq;
-    r->t_ns = globaltimer();
-    ++e.tcnt;
-    a.trace_cnt[wid] = e.tcnt;
-    __threadfence();
-  }
+  if (a.record_trace && word != e.pub) trace_rec(a, wid, e, word);
   const unsigned long long v = uint64_t(word) | (uint64_t(e.st.phase) << 32);
   unsigned long long* cell = a.status + uint64_t(wid) * a.status_u64;
   if (release) st_release_sys(cell, v); else st_relaxed_sys(cell, v);
@@ -665,9 +677,19 @@ __device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool ti
   return true;
 }
 
-__device__ __forceinline__ void publish_fast(const lk_dev_args& a, uint32_t wid, uint32_t word,
+// Fast-path publish: every call changes the cell's word (WORKING after NOP,
+// FINISHED after WORKING, NOP after FINISHED), so with record_trace on each
+// one is a trace record, exactly as publish() would write it.
+__device__ __forceinline__ void publish_fast(const lk_dev_args& a, uint32_t wid, Elected& e, uint32_t word,
                                              uint32_t phase) {
+  if (a.record_trace) trace_rec(a, wid, e, word);
   st_relaxed_sys(a.status + uint64_t(wid) * a.status_u64, uint64_t(word) | (uint64_t(phase) << 32));
+}
+
+// Per-worker count of values the fast path settled (lk_fast_count): the
+// evidence that the benchmarked branches ran, and were trace-checked.
+__device__ __forceinline__ void fast_hit(const lk_dev_args& a, uint32_t wid, Elected& e) {
+  a.fast_cnt[wid] = ++e.fhits;
 }
 
 // The ack delay (see spin_cycles below) is per worker and adapts to the host:
@@ -718,61 +740,77 @@ __device__ __forceinline__ void idle_adapt(const lk_dev_args& a, Elected& e) {
 //   IDLE x WORK(s) of a payload kind -> publish WORKING and begin at once;
 //   FINISHED x NOP -> publish NOP, IDLE; re-stepping NOP in IDLE is a no-op.
 // Exactly lk_worker_step + lk_complete_work for these cases (protocol.py:151-206);
-// anything else -- and every case while a trace is recorded -- takes settle().
+// anything else takes settle().  With record_trace on, every publish here
+// appends the same trace record publish() would, so the recorded sessions
+// replay the fast path itself (tests/test_gpu_fastpath.py).
+// The fast path's part of the dispatch timeline (lk_last_timeline): clock64
+// stamps always, globaltimer stamps under LK_CF_TIMELINE (same words as
+// write_timeline, plus word 8 = FINISHED issued for the ack-phase breakdown).
+__device__ __forceinline__ void fast_timeline(const lk_dev_args& a, uint32_t wid, const Elected& e,
+                                              uint64_t c_begin, uint64_t c_fin, uint64_t t_b, uint64_t t_e,
+                                              bool tlf) {
+  unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
+  tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
+  if (tlf) {
+    const uint64_t t_f = globaltimer();
+    tl[0] = e.t_seen; tl[1] = t_b; tl[2] = t_e; tl[3] = t_f; tl[4] = e.t_fwd; tl[8] = t_f;
+  }
+}
+
 enum FastResult : uint32_t { kFastNone = 0, kFastSettled = 1, kFastBegin = 2 };
 
 __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid, Elected& e) {
-  if (a.record_trace | (a.flags & LK_CF_FENCE_ALWAYS)) return kFastNone;
+  if (a.flags & LK_CF_FENCE_ALWAYS) return kFastNone;   // every FINISHED is a sys-scope release: settle()
   const uint32_t w = e.cur;
   if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && (e.hint & LK_HINT_CACHED) &&
       w - LK_WORK_BASE == e.cslot && single_thread_kind(e.ckind)) {
     // a cached busy_loop/empty item: run it right here, like an empty task
+    const bool tlf = (a.flags & LK_CF_TIMELINE) != 0;
     const uint64_t c_begin = clock64();
-    publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
+    const uint64_t t_b = tlf ? globaltimer() : 0;
+    publish_fast(a, wid, e, LK_WORKING, LK_PHASE_WORKING);
     if (e.ckind == LK_KIND_BUSY_LOOP) *a.sink = busy_loop(e.citer);   // stored: the loop must run
-    publish_fast(a, wid, LK_FINISHED, LK_PHASE_FINISHED);
+    const uint64_t t_e = tlf ? globaltimer() : 0;
+    publish_fast(a, wid, e, LK_FINISHED, LK_PHASE_FINISHED);
     const uint64_t c_fin = clock64();
     e.st = lk_wstate{LK_PHASE_FINISHED, w - LK_WORK_BASE};
     e.pub = LK_FINISHED;
     e.dirty = false;
     idle_adapt(a, e);
-    unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
-    tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
-    if (a.flags & LK_CF_TIMELINE) {
-      tl[0] = e.t_seen; tl[4] = e.t_fwd; tl[8] = globaltimer();
-    }
+    fast_timeline(a, wid, e, c_begin, c_fin, t_b, t_e, tlf);
+    fast_hit(a, wid, e);
     return kFastSettled;
   }
   if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && !(e.hint & LK_HINT_EMPTY) &&
       w - LK_WORK_BASE < a.num_slots) {
     // IDLE x WORK(s) of any other kind: publish WORKING and begin at once; the
     // word stays dirty so it is re-stepped after completion, as in settle().
-    publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
+    publish_fast(a, wid, e, LK_WORKING, LK_PHASE_WORKING);
     idle_adapt(a, e);
     e.st = lk_wstate{LK_PHASE_WORKING, w - LK_WORK_BASE};
     e.pub = LK_WORKING;
     e.dirty = true;
+    fast_hit(a, wid, e);
     return kFastBegin;
   }
   if (e.st.phase == LK_PHASE_IDLE && w >= LK_WORK_BASE && (e.hint & LK_HINT_EMPTY) &&
       w - LK_WORK_BASE < a.num_slots) {
+    const bool tlf = (a.flags & LK_CF_TIMELINE) != 0;
     const uint64_t c_begin = clock64();
-    publish_fast(a, wid, LK_WORKING, LK_PHASE_WORKING);
-    publish_fast(a, wid, LK_FINISHED, LK_PHASE_FINISHED);
+    const uint64_t t_b = tlf ? globaltimer() : 0;
+    publish_fast(a, wid, e, LK_WORKING, LK_PHASE_WORKING);
+    publish_fast(a, wid, e, LK_FINISHED, LK_PHASE_FINISHED);
     const uint64_t c_fin = clock64();
     idle_adapt(a, e);
     e.st = lk_wstate{LK_PHASE_FINISHED, w - LK_WORK_BASE};
     e.pub = LK_FINISHED;
     e.dirty = false;
-    unsigned long long* tl = a.spans + uint64_t(LK_TIMELINE_WORDS) * wid;
-    tl[5] = e.c_seen; tl[6] = c_begin; tl[7] = c_fin;
-    if (a.flags & LK_CF_TIMELINE) {
-      tl[0] = e.t_seen; tl[4] = e.t_fwd; tl[8] = globaltimer();
-    }
+    fast_timeline(a, wid, e, c_begin, c_fin, t_b, t_b, tlf);
+    fast_hit(a, wid, e);
     return kFastSettled;
   }
   if (e.st.phase == LK_PHASE_FINISHED && w == LK_NOP) {
-    publish_fast(a, wid, LK_NOP, LK_PHASE_IDLE);
+    publish_fast(a, wid, e, LK_NOP, LK_PHASE_IDLE);
     e.idle_pub = true;
     ack_adapt(a, e);
     if (a.flags & LK_CF_TIMELINE) {
@@ -782,6 +820,7 @@ __device__ __forceinline__ uint32_t fast_step(const lk_dev_args& a, uint32_t wid
     e.st.phase = LK_PHASE_IDLE;
     e.pub = LK_NOP;
     e.dirty = false;
+    fast_hit(a, wid, e);
     return kFastSettled;
   }
   return kFastNone;
@@ -1186,6 +1225,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
   e.dseq = 0;
   e.rseq = 0;
   e.tcnt = 0;
+  e.fhits = 0;
   e.nload = 0;
   e.cslot = 0xFFFFFFFFu;
   e.ckind = 0;
@@ -1232,11 +1272,19 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
           const uint4* src = reinterpret_cast<const uint4*>(a.desc + slot);
           uint4* dst = reinterpret_cast<uint4*>(&d);
           const unsigned long long* m = a.slot_mask + uint64_t(slot) * a.nwords;
+          if (a.flags & LK_CF_HOST_DESC) {   // host-mapped table: sys scope, never a stale L2 line
 #pragma unroll
-          for (int k = 0; k < 4; ++k) dst[k] = ld_cg4(src + k);
+            for (int k = 0; k < 4; ++k) dst[k] = ld_sys4(src + k);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (uint32_t(k) < a.nwords) mk[k] = ld_cg64(m + k);
+            for (int k = 0; k < 4; ++k)
+              if (uint32_t(k) < a.nwords) mk[k] = ld_cell(m + k, false);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = ld_cg4(src + k);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (uint32_t(k) < a.nwords) mk[k] = ld_cg64(m + k);
+          }
           sm.cdesc = d;
 #pragma unroll
           for (int k = 0; k < 4; ++k) sm.cmask[k] = mk[k];
@@ -1323,6 +1371,10 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
   run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, ring, use_tma != 0, g);
 }
 
+// The fastest conventional task: an empty kernel, one warp, no shared memory
+// (the launch+sync floor lk_launch_floor_bench measures LK against).
+__global__ void lk_empty_kernel() {}
+
 // ---------------------------------------------------------------- ping-pong
 __global__ void lk_pingpong_kernel(volatile uint32_t* flag, volatile uint32_t* echo, uint64_t rounds) {
   for (uint64_t r = 1; r <= rounds; ++r) {
@@ -1390,6 +1442,7 @@ cudaError_t lk_preload_kernels() {
     e = cudaFuncSetAttribute(lk_work_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(kDefaultStages * kStageBytes));
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_pingpong_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_empty_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_clocksync_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, lk_persistent_kernel);
   return e;
@@ -1413,6 +1466,11 @@ cudaError_t lk_launch_persistent(const lk_dev_args& a, uint32_t grid, uint32_t t
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads, uint32_t* reduce_ctr,
                            cudaStream_t st, int use_tma) {
   lk_work_kernel<<<grid, threads, use_tma ? kDefaultStages * kStageBytes : 0, st>>>(d, reduce_ctr, use_tma);
+  return cudaGetLastError();
+}
+
+cudaError_t lk_launch_empty(cudaStream_t st) {
+  lk_empty_kernel<<<1, 32, 0, st>>>();
   return cudaGetLastError();
 }
 

@@ -183,6 +183,25 @@ static PyObject* decline(Fast* f, PyObject* slow, PyObject* const* args, Py_ssiz
   return r;
 }
 
+/* A method object captured before the session closed: the handle is gone,
+ * so never call into liblk.so.  The session's Python path raises its
+ * "already disposed" UsageError; without one this is a RuntimeError. */
+static PyObject* closed(Fast* f, PyObject* slow, PyObject* const* args, Py_ssize_t nargs) {
+  if (slow && f->wref) {
+    PyObject* sess = PyWeakref_GetObject(f->wref);   /* borrowed */
+    if (sess && sess != Py_None) return decline(f, slow, args, nargs);
+    PyErr_Clear();
+  }
+  PyErr_SetString(PyExc_RuntimeError, "LK session closed");
+  return NULL;
+}
+
+static PyObject* fast_close(Fast* f, PyObject* unused) {
+  (void)unused;
+  f->h = NULL;
+  Py_RETURN_NONE;
+}
+
 /* A failing C call: raised through the session's raiser (its LK_E_* code as an
  * int without one). */
 static PyObject* failed(Fast* f, int rc, PyObject* mask, int is_wait) {
@@ -201,6 +220,7 @@ static PyObject* fast_trigger(Fast* f, PyObject* const* args, Py_ssize_t nargs) 
     return NULL;
   }
   PyObject *mask = args[0], *work = args[1];
+  if (!f->h) return closed(f, f->slow_trigger, args, nargs);
   if (Py_TYPE(work) != f->work_type) return decline(f, f->slow_trigger, args, nargs);
   PyObject* mb = mask_words(f, mask);
   if (!mb) return decline(f, f->slow_trigger, args, nargs);
@@ -254,6 +274,7 @@ static PyObject* fast_wait(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
     return NULL;
   }
   PyObject* mask = args[0];
+  if (!f->h) return closed(f, f->slow_wait, args, nargs);
   PyObject* mb = mask_words(f, mask);
   if (!mb) return decline(f, f->slow_wait, args, nargs);
   const uint64_t* m = (const uint64_t*)PyBytes_AS_STRING(mb);
@@ -270,6 +291,7 @@ static PyObject* fast_wait(Fast* f, PyObject* const* args, Py_ssize_t nargs) {
 static PyMethodDef fast_methods[] = {
     {"trigger", (PyCFunction)(void (*)(void))fast_trigger, METH_FASTCALL, "trigger(mask, work)"},
     {"wait", (PyCFunction)(void (*)(void))fast_wait, METH_FASTCALL, "wait(mask)"},
+    {"close", (PyCFunction)fast_close, METH_NOARGS, "forget the session handle (later calls never reach liblk.so)"},
     {NULL, NULL, 0, NULL}};
 
 static PyTypeObject FastType = {

@@ -113,6 +113,24 @@ def _numel(ref) -> Optional[int]:
     return None
 
 
+def _nbytes(ref) -> Optional[int]:
+    """Size of a payload buffer in bytes, or None for a raw address."""
+    if isinstance(ref, DeviceBuffer):
+        return ref.nbytes
+    if hasattr(ref, "numel") and hasattr(ref, "element_size"):
+        return int(ref.numel()) * int(ref.element_size())
+    nb = getattr(ref, "nbytes", None)
+    if isinstance(nb, int):
+        return nb
+    cai = getattr(ref, "__cuda_array_interface__", None)
+    if cai is not None:
+        n = 1
+        for d in cai["shape"]:
+            n *= int(d)
+        return n * np.dtype(cai["typestr"]).itemsize
+    return None
+
+
 def _dtype_name(ref) -> Optional[str]:
     dt = getattr(ref, "dtype", None)
     return None if dt is None else str(dt).replace("torch.", "")
@@ -185,6 +203,16 @@ class WorkDescriptor:
             if want[0] and dn is not None and dn != want[0]:
                 raise ConfigError(f"{self.kind} expects {want[0]} buffers, got {dn}")
         d.n = self.elements()
+        # the kernel writes out[0, n) (maps) and reads in*[0, n): a short
+        # buffer would be overrun on the device, so refuse it here
+        for r in ins + ((self.data_out_ref,) if self.kind != BLOCK_REDUCE_F32 else ()):
+            nb = _nbytes(r)
+            if nb is not None and nb < 4 * d.n:
+                raise ConfigError(f"{self.kind}: a {nb}-byte buffer cannot hold n={d.n} elements")
+        if self.kind == BLOCK_REDUCE_F32:
+            nb = _nbytes(self.total_ref)
+            if self.total_ref is not None and nb is not None and nb < 8:
+                raise ConfigError("block_reduce_f32: total_ref must hold one float64")
         d.in0 = _addr(ins[0])
         d.in1 = _addr(ins[1]) if len(ins) > 1 else 0
         d.out = _addr(self.data_out_ref)

@@ -83,6 +83,9 @@ class NativeConfig:
     tma_min_workers: int = 49       # payload dispatches to fewer workers use LSU loads (1: always the ring)
     lazy_ack: bool = False          # wait() returns once the ack is written; its consumption is
                                     # awaited by the next trigger/dispose of that worker
+    host_descriptors: bool = False  # descriptor table in pinned mapped host memory (direct mode):
+                                    # trigger/wait/register make no CUDA call, so the session works
+                                    # while a serialising profiler (ncu) holds the kernel's launch
 
     def __post_init__(self) -> None:
         if self.num_workers is not None and self.num_workers < 1:
@@ -130,8 +133,32 @@ class NativeConfig:
                    | (_lib.CF_ACK_WINDOW if self.ack_window else 0)
                    | (_lib.CF_DYNAMIC_TILES if self.dynamic_tiles else 0)
                    | (0 if self.ack_delay_ns else _lib.CF_NO_ACK_DELAY)
-                   | (0 if self.ack_adaptive else _lib.CF_ACK_FIXED))
+                   | (0 if self.ack_adaptive else _lib.CF_ACK_FIXED)
+                   | (_lib.CF_HOST_DESC if self.host_descriptors else 0))
         return c
+
+
+def init_device(device: int = 0) -> None:
+    """Create the device's primary CUDA context now (a one-byte allocation
+    through liblk.so), so the driver's helper threads are spawned with the
+    caller's current CPU affinity rather than a later, narrower one."""
+    lib = _lib.load()
+    p = C.c_uint64()
+    _lib.check(lib.lk_dev_alloc(device, 1, C.byref(p)))
+    _lib.check(lib.lk_dev_free(p.value))
+
+
+def under_profiler() -> bool:
+    """True inside a CUDA tool that injects itself into the process: Nsight
+    Compute's launcher exports NV_TPS_LAUNCH_TOKEN and the
+    NV_NSIGHT_INJECTION_* / NV_COMPUTE_PROFILER_PERFWORKS_DIR variables
+    (seen on the B200 box), other injection tools CUDA_INJECTION64_PATH.
+    Such tools may serialise launches, so a live session must then make no
+    CUDA calls."""
+    import os
+    keys = ("NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE", "NV_COMPUTE_PROFILER_PERFWORKS_DIR",
+            "CUDA_INJECTION64_PATH")
+    return any(os.environ.get(k) for k in keys)
 
 
 def pin_host_thread(device: int) -> int:
@@ -343,6 +370,8 @@ class NativeSession:
             self.__dict__["wait"] = f.wait
 
     def _unbind_fast(self) -> None:
+        if self._fast is not None:
+            self._fast.close()   # method objects captured earlier stop calling into liblk.so
         self._fast = None
         self.__dict__.pop("trigger", None)
         self.__dict__.pop("wait", None)
@@ -567,6 +596,21 @@ class NativeSession:
         _lib.check(rc)
         return trig, done, cyc
 
+    def bench_roundtrip_gaps(self, masks: list[int], slot: int, rounds: int):
+        """bench_roundtrip plus, per round, the largest gap (ns) in the host
+        thread's own spin loop (lk_bench_roundtrip_gaps): rounds whose gap is
+        microseconds long were slowed by the host thread being descheduled."""
+        packed = b"".join(self._mask(m) for m in masks)
+        trig = np.zeros(rounds, dtype=np.uint64)
+        done = np.zeros(rounds, dtype=np.uint64)
+        cyc = np.zeros(rounds, dtype=np.uint64)
+        gap = np.zeros(rounds, dtype=np.uint64)
+        rc = self._lib.lk_bench_roundtrip_gaps(self._h, packed, len(masks), self.nwords, slot, rounds,
+                                               trig.ctypes.data, done.ctypes.data, cyc.ctypes.data,
+                                               gap.ctypes.data)
+        _lib.check(rc)
+        return trig, done, cyc, gap
+
     def last_timeline(self) -> np.ndarray:
         """(num_workers, 8) record of each worker's last dispatch: globaltimer ns
         at value seen, work begin, work end, FINISHED issued, gateway forward
@@ -574,6 +618,14 @@ class NativeSession:
         t = np.zeros((self.num_workers, 12), dtype=np.uint64)
         _lib.check(self._lib.lk_last_timeline(self._h, t.ctypes.data, self.num_workers))
         return t
+
+    def fast_counts(self) -> np.ndarray:
+        """Per-worker count of to_gpu values the kernel's fast path settled
+        since boot (lk_fast_count): IDLE x WORK of an empty or cached
+        single-thread item, IDLE x WORK begin of a payload item, FINISHED x NOP."""
+        c = np.zeros(self.num_workers, dtype=np.uint32)
+        _lib.check(self._lib.lk_fast_count(self._h, c.ctypes.data, self.num_workers))
+        return c
 
     def last_host_times(self) -> np.ndarray:
         """(num_workers, 3) CLOCK_MONOTONIC ns of each worker's last dispatch:
@@ -713,6 +765,22 @@ def clock_offset(device: int = 0, rounds: int = 2000) -> tuple[int, int]:
     off, rtt = C.c_int64(), C.c_uint64()
     _lib.check(_lib.load().lk_clock_offset(device, rounds, C.byref(off), C.byref(rtt)))
     return off.value, rtt.value
+
+
+FLOOR_MODES = {"kernel_sync": _lib.FLOOR_SYNC, "kernel_query": _lib.FLOOR_QUERY, "graph_sync": _lib.FLOOR_GRAPH}
+
+
+def launch_floor(device: int, mode: str, rounds: int, spin_sched: bool = False):
+    """The cheapest conventional launch+sync per task (lk_launch_floor_bench):
+    an empty <<<1,32,0>>> kernel joined by stream sync ("kernel_sync"), by a
+    host spin on cudaStreamQuery ("kernel_query"), or as a one-node CUDA graph
+    ("graph_sync"); spin_sched sets cudaDeviceScheduleSpin (process-wide).
+    Returns (total_ns, launch_ns) arrays.  Run with no session live."""
+    total = np.zeros(rounds, dtype=np.uint64)
+    launch = np.zeros(rounds, dtype=np.uint64)
+    _lib.check(_lib.load().lk_launch_floor_bench(device, FLOOR_MODES[mode], 1 if spin_sched else 0, rounds,
+                                                 total.ctypes.data, launch.ctypes.data))
+    return total, launch
 
 
 def pingpong(device: int, rounds: int) -> np.ndarray:

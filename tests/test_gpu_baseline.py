@@ -90,3 +90,19 @@ def test_baseline_runs_beside_a_partitioned_session():
         assert O.replay([(r.side, r.sm_id, r.word) for r in session.recorded_trace()]).violation is None
     finally:
         session.close()
+
+
+@pytest.mark.parametrize("mode", ["kernel_sync", "kernel_query", "graph_sync"])
+def test_launch_floor_modes_run(mode):
+    """The cheapest conventional launch+sync flows (the ≥5x denominator's
+    candidates) each complete every task: completion is observed after the
+    launch call returns, and no task takes a whole second."""
+    total, launch = native.launch_floor(0, mode, 500)
+    assert (total >= launch).all()
+    assert int(total.max()) < 1_000_000_000
+    assert np.median(total) > 0
+
+
+def test_launch_floor_spin_schedule():
+    total, _ = native.launch_floor(0, "kernel_sync", 200, spin_sched=True)
+    assert np.median(total) > 0
