@@ -442,7 +442,7 @@ HEADLINE_EXTRAS = ("single_worker", "full_mask", "interference", "interference_g
 def measure_payload(session, kind, sizes_mib, reps, rotate_bytes):
     """GB/s of a payload kind dispatched to all workers, L2-cold by rotation."""
     from paper_2310_01212_b200 import host
-    from paper_2310_01212_b200.device import BYTES_PER_ELEMENT, DeviceBuffer, WorkDescriptor
+    from paper_2310_01212_b200.device import BYTES_PER_ELEMENT, DeviceBuffer, WorkDescriptor, reduce_blocks
     full = host.full_mask(session.num_workers)
     out = {}
     for mib in sizes_mib:
@@ -456,7 +456,7 @@ def measure_payload(session, kind, sizes_mib, reps, rotate_bytes):
                 bufs += [x, y]
                 works.append(WorkDescriptor(slot=100 + k, kind=kind, data_in_ref=(x, y), data_out_ref=y, alpha=1.5))
             else:
-                x, p, t = DeviceBuffer(4 * n), DeviceBuffer(4 * 160), DeviceBuffer(8)
+                x, p, t = DeviceBuffer(4 * n), DeviceBuffer(8 * reduce_blocks(n)), DeviceBuffer(8)
                 bufs += [x, p, t]
                 works.append(WorkDescriptor(slot=100 + k, kind=kind, data_in_ref=x, data_out_ref=p, total_ref=t))
         for w in works:

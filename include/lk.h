@@ -63,7 +63,9 @@ extern "C" {
 #define LK_KIND_BUSY_LOOP         1u  /* native.py:63-67 */
 #define LK_KIND_VECTOR_ADD_I32    2u  /* out[i] = in0[i] + in1[i] mod 2^32 */
 #define LK_KIND_SAXPY_F32         3u  /* out[i] = fl(fl(alpha*in0[i]) + in1[i]) */
-#define LK_KIND_BLOCK_REDUCE_F32  4u  /* out[rank] = sum(chunk); *(double*)aux = total */
+#define LK_KIND_BLOCK_REDUCE_F32  4u  /* ((double*)out)[b] = fp64 sum of 4096-element block b (ceil(n/4096)
+                                          entries); *(double*)aux = their fp64 combine.  Fixed order of
+                                          operations (oracle/work.py): the same bits for any mask/schedule */
 #define LK_KIND_HBM_STREAM        5u  /* out[i] = in0[i], `iterations` passes (>=1) */
 #define LK_KIND_COUNT             6u
 
@@ -91,7 +93,7 @@ typedef struct lk_desc {
   uint64_t in0;        /* device pointers */
   uint64_t in1;
   uint64_t out;
-  uint64_t aux;        /* BLOCK_REDUCE: double* total (0 = no combine) */
+  uint64_t aux;        /* BLOCK_REDUCE: double* total (0 = block partials only) */
   float    alpha;
   uint32_t reserved;
 } lk_desc;

@@ -44,14 +44,72 @@ def saxpy_f32(alpha: float, x: np.ndarray, y: np.ndarray) -> np.ndarray:
     return (prod + y.astype(np.float32)).astype(np.float32)
 
 
-def block_reduce_partials(x: np.ndarray, count: int) -> np.ndarray:
-    """Per-worker chunk sums, float64 (compare: exact on small-integer data,
-    rtol 1e-6 on U[0,1) data)."""
-    return np.array([x[b:e].astype(np.float64).sum() for b, e in partition(len(x), count)])
+# block_reduce_f32 (lk_kernels.cu: reduce_dyn / reduce_static) is defined
+# independently of the worker set, the schedule and the payload path, so
+# every dispatch of the same data gives bit-identical results:
+REDUCE_BLOCK = 4096    # elements per block (one 16-KiB TMA stage)
+REDUCE_VLANES = 512    # virtual lanes of the final combine
+
+
+def _butterfly(v: np.ndarray, axis_len: int) -> np.ndarray:
+    """xor butterfly over the last axis: for o = len/2 .. 1, v[l] = v[l] + v[l ^ o]
+    (fp64; every lane ends with the same value, IEEE addition commutes)."""
+    idx = np.arange(axis_len)
+    o = axis_len // 2
+    while o >= 1:
+        v = v + v[..., idx ^ o]
+        o //= 2
+    return v
+
+
+def block_reduce_partials(x: np.ndarray) -> np.ndarray:
+    """Per-block fp64 sums, one per 4096-element block (ceil(n/4096) values).
+    A block is 16 sub-blocks of 64 float4 vectors.  In sub-block s, lane l
+    (0..31) adds vector 64s + l, then vector 64s + 32 + l, into one fp32
+    accumulator per component (starting at +0, round to nearest); lane value
+    (a0 + a1) + (a2 + a3) in fp64; a 32-lane fp64 xor butterfly gives the
+    sub-block sum; the block sum is the pairwise fp64 tree over the 16
+    sub-block sums in index order.  Missing elements of a short last block
+    add nothing (+0.0 is exact here: the accumulators start at +0.0 and can
+    never hold -0.0)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    n = x.size
+    nb = -(-n // REDUCE_BLOCK)
+    if nb == 0:
+        return np.zeros(0, np.float64)
+    pad = np.zeros(nb * REDUCE_BLOCK, np.float32)
+    pad[:n] = x
+    blk = pad.reshape(nb, 16, 2, 32, 4)       # (block, sub, half, lane, component): element 4*(64s + 32h + l) + c
+    acc = (np.float32(0.0) + blk[:, :, 0]).astype(np.float32)
+    acc = (acc + blk[:, :, 1]).astype(np.float32)
+    a = acc.astype(np.float64)
+    lane = (a[..., 0] + a[..., 1]) + (a[..., 2] + a[..., 3])     # (block, sub, lane)
+    sub = _butterfly(lane, 32)[..., 0]                           # (block, sub)
+    while sub.shape[1] > 1:                                      # pairwise tree in index order
+        sub = sub[:, 0::2] + sub[:, 1::2]
+    return sub[:, 0]
+
+
+def block_reduce_combine(partials: np.ndarray) -> float:
+    """The total from the block partials: virtual lane j (0..511) adds
+    partials j, j+512, ... in order (fp64, from +0.0), then a 512-lane xor
+    butterfly."""
+    p = np.asarray(partials, np.float64)
+    m = -(-p.size // REDUCE_VLANES)
+    pad = np.zeros(max(1, m) * REDUCE_VLANES, np.float64)
+    pad[:p.size] = p
+    rows = pad.reshape(-1, REDUCE_VLANES)
+    s = np.zeros(REDUCE_VLANES, np.float64)
+    for r in rows:
+        s = s + r
+    return float(_butterfly(s, REDUCE_VLANES)[0])
 
 
 def block_reduce_total(x: np.ndarray) -> float:
-    return float(x.astype(np.float64).sum())
+    """*total of a block_reduce_f32 dispatch (bit-exact target); within
+    rounding of float(x.astype(float64).sum()), and equal to it on
+    small-integer data."""
+    return block_reduce_combine(block_reduce_partials(x))
 
 
 def hbm_stream(src: np.ndarray) -> np.ndarray:

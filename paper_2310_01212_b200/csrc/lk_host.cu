@@ -16,6 +16,7 @@
 #include <sched.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <time.h>
 #include <unistd.h>
@@ -869,6 +870,14 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   a.use_tma = use_tma ? 1 : 0;
   a.ring_stages = cfg.ring_stages;
   a.tma_min_workers = cfg.tma_min_workers;
+  {   // block_reduce schedule (tuning overrides for tools/reduce_sizes.py)
+    const char* e1 = getenv("LK_RED_SHARE8");
+    const char* e2 = getenv("LK_RED_CLAIM");
+    a.red_share8 = e1 ? uint32_t(atoi(e1)) : 6u;
+    a.red_claim = e2 ? uint32_t(atoi(e2)) : 2u;
+    if (a.red_share8 > 8) a.red_share8 = 8;
+    if (a.red_claim < 1) a.red_claim = 1;
+  }
   {
     int khz = 0;   // SM clock: the delay is spun on clock64
     if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, cfg.device) != cudaSuccess || khz <= 0) khz = 1965000;

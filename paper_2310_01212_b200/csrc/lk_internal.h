@@ -56,6 +56,8 @@ struct lk_dev_args {
   uint32_t record_trace;
   uint32_t backoff_ns;
   uint32_t flags;                  // LK_CF_*
+  uint32_t red_share8;             // block_reduce: static share of a fair share, in eighths (8: static only)
+  uint32_t red_claim;              // block_reduce: blocks per pool claim
 };
 
 // Launch wrappers (lk_kernels.cu).

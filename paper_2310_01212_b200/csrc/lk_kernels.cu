@@ -410,125 +410,331 @@ __device__ __forceinline__ void map_tma_dyn(const lk_desc& d, uint32_t rank, uin
   }
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+// ---------------------------------------------------------------- block reduce
+// block_reduce_f32 is defined on fixed 4096-element blocks (oracle/work.py:
+// block_reduce_partials / block_reduce_combine), independent of the mask,
+// the worker count, the thread count, the schedule and the payload path:
+//   sub-block s (0..15) of a block = its float4 vectors [64s, 64s + 64);
+//     lane l (0..31) adds vectors 64s + l, then 64s + 32 + l, into one fp32
+//     accumulator per component (from +0); lane value (a0 + a1) + (a2 + a3)
+//     in fp64; a 32-lane fp64 xor butterfly gives the sub-block's sum;
+//   out[b]  = pairwise fp64 tree over the 16 sub-block sums, in index order;
+//   *aux    = fp64 combine of out[0, nb): virtual lane j of 512 adds
+//             out[j], out[j + 512], ... in order, then a 512-lane butterfly.
+// So any worker may sum any block and any warp any sub-block: blocks are
+// handed out dynamically (a static share per worker, the rest claimed from a
+// pool), which absorbs dispatch skew and slow SMs without changing a bit of
+// the result, while every consumer warp still reads only two vectors per lane
+// of each ring stage, as the map kinds do.
+constexpr uint32_t kRedBlock = 4096;              // elements per block = one 16-KiB ring stage
+constexpr uint32_t kRedVecs = kRedBlock / 4;      // float4 vectors per block
+constexpr uint32_t kRedSubs = 16;                 // sub-blocks per block (64 vectors each)
+constexpr uint32_t kRedVLanes = 512;              // virtual lanes of the combine
+constexpr uint32_t kRedClaim = 2;                 // blocks per pool claim
+static_assert(kRedBlock * 4 == kStageBytes, "a reduce block is one ring stage");
 
 struct ReduceSmem {
-  float part[kMaxThreads / 32];
+  double comb[2 * kRedVLanes];             // the combine's two butterfly buffers
+  double sub[2][kMaxStages][kRedSubs];     // sub-block sums of a stage, by position parity
+  uint32_t cnt[2][kMaxStages];             // sub-blocks of a stage summed so far, by position parity
   uint32_t last;
 };
 
-// out[rank] = fp32 sum of the chunk (per-thread sequential, then a fixed
-// shuffle tree); the last worker to finish sums the partials in rank order in
-// fp64 into *(double*)aux.
-template <int U>
-__device__ __forceinline__ void reduce_chunk(const lk_desc& d, Part p, uint32_t rank, uint32_t count,
-                                             uint32_t* ctr, ReduceSmem& sm, uint32_t T, Ring& ring,
-                                             bool ring_on, uint32_t& g) {
+// Called once per kernel by thread 0, before the CTA's first barrier.
+__device__ __forceinline__ void reduce_smem_init(ReduceSmem& sm) {
+  for (uint32_t k = 0; k < kMaxStages; ++k) sm.cnt[0][k] = sm.cnt[1][k] = 0;
+}
+
+__device__ __forceinline__ double butterfly32(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);   // lanes l, l^o: same sum
+  return v;
+}
+
+__device__ __forceinline__ float4 as_f4(uint4 r) {
+  return make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z), __uint_as_float(r.w));
+}
+
+// A lane's part of a sub-block: its two vectors (either may be absent in a
+// short last block), `m1`/`m2` = elements present in each (0..4).
+__device__ __forceinline__ double sub_lane(float4 u, uint32_t m1, float4 w, uint32_t m2) {
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  const float uu[4] = {u.x, u.y, u.z, u.w}, ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (uint32_t(c) < m1) a[c] = __fadd_rn(a[c], uu[c]);
+    if (uint32_t(c) < m2) a[c] = __fadd_rn(a[c], ww[c]);
+  }
+  return (double(a[0]) + double(a[1])) + (double(a[2]) + double(a[3]));
+}
+
+// Elements of vector v (0..1023) of a block holding nvt full vectors plus
+// `tail` trailing elements.
+__device__ __forceinline__ uint32_t vec_elems(uint32_t v, uint32_t nvt, uint32_t tail) {
+  return v < nvt ? 4u : (v == nvt ? tail : 0u);
+}
+
+__device__ __forceinline__ double tree16(const double* s) {
+  return (((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]))) +
+         (((s[8] + s[9]) + (s[10] + s[11])) + ((s[12] + s[13]) + (s[14] + s[15])));
+}
+
+__device__ __forceinline__ void st_f64(double* p, double v) {
+  asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_cg_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// One block straight from global memory by one warp (LSU path; `vec`: x is
+// 16-B aligned).  Same sub-block sums and tree as the ring path.
+__device__ __forceinline__ double block_sum_global(const float* x, uint64_t b, uint64_t n, bool vec) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t e0 = b * kRedBlock;
+  const uint64_t ne = min(uint64_t(kRedBlock), n - e0);
+  const uint32_t nvt = uint32_t(ne >> 2), tail = uint32_t(ne & 3);
+  const uint32_t* xu = reinterpret_cast<const uint32_t*>(x) + e0;
+  auto load = [&](uint32_t v, uint32_t m) -> float4 {
+    if (m == 4 && vec) return as_f4(ld_cg4(reinterpret_cast<const uint4*>(xu) + v));
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+    for (uint32_t c = 0; c < m; ++c) e[c] = __uint_as_float(ld_cg1(xu + 4 * v + c));
+    return make_float4(e[0], e[1], e[2], e[3]);
+  };
+  // four sub-blocks at a time (8 loads in flight per lane), folded as they
+  // come: quad k = ((s0 + s1) + (s2 + s3)) of sub-blocks 4k..4k+3, and the
+  // block = (quad0 + quad1) + (quad2 + quad3) -- the same tree as tree16
+  double quad[4];
+#pragma unroll
+  for (uint32_t k = 0; k < 4; ++k) {
+    double l[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint32_t v1 = 64 * (4 * k + q) + lane, v2 = v1 + 32;
+      const uint32_t m1 = vec_elems(v1, nvt, tail), m2 = vec_elems(v2, nvt, tail);
+      const float4 u = m1 ? load(v1, m1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 w = m2 ? load(v2, m2) : make_float4(0.f, 0.f, 0.f, 0.f);
+      l[q] = sub_lane(u, m1, w, m2);
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) l[q] = butterfly32(l[q]);
+    quad[k] = (l[0] + l[1]) + (l[2] + l[3]);
+  }
+  return (quad[0] + quad[1]) + (quad[2] + quad[3]);
+}
+
+// Arrival count and, in the last worker to arrive, the combine of every
+// block partial into *aux (all T threads of that CTA).  ctr[0] = arrivals,
+// ctr[1] = pool claims; the last worker resets both for the slot's next
+// dispatch (no worker claims or arrives any more by then).
+__device__ __forceinline__ void reduce_finish(const lk_desc& d, uint32_t count, uint32_t* ctr, ReduceSmem& sm,
+                                              uint32_t T) {
   const uint32_t t = threadIdx.x;
-  const float* x = reinterpret_cast<const float*>(d.in0);
-  float acc = 0.f;
-  if (ring_on && !(d.flags & LK_DF_SCALAR)) {
-    const uint4* x4 = reinterpret_cast<const uint4*>(x);
-    const uint64_t vb = p.b >> 2, ve = p.e >> 2;
-    constexpr uint32_t kTileV = kStageBytes / 16;
-    const uint64_t nv = ve > vb ? ve - vb : 0;
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    ring_stream(
-        ring, g, uint32_t((nv + kTileV - 1) / kTileV), T,
-        [&](uint32_t i, uint8_t* stage, uint64_t* bar) {
-          const uint64_t v0 = vb + uint64_t(i) * kTileV;
-          const uint32_t bytes = uint32_t(min(uint64_t(kTileV), ve - v0)) * 16u;
-          mbar_expect_tx(bar, bytes);
-          bulk_g2s(stage, x4 + v0, bytes, bar);
-        },
-        [&](uint32_t i, const uint8_t* stage, uint32_t ci, uint32_t nc) {
-          const uint32_t nvt = uint32_t(min(uint64_t(kTileV), ve - (vb + uint64_t(i) * kTileV)));
-          for (uint32_t v = ci; v < nvt; v += nc) {
-            const uint4 r = lds4(stage + 16 * v);
-            s.x += __uint_as_float(r.x); s.y += __uint_as_float(r.y);
-            s.z += __uint_as_float(r.z); s.w += __uint_as_float(r.w);
-          }
-        });
-    acc = (s.x + s.y) + (s.z + s.w);
-    for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
-  } else if (d.flags & LK_DF_SCALAR) {
-    for (uint64_t i = p.b + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
+  wsync(T);                 // every block partial of this worker stored
+  if (t == 0) {
+    // acq_rel RMW after the barrier: releases this CTA's partial stores,
+    // and the last arrival acquires every other worker's
+    uint32_t prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
+    sm.last = prev == count - 1;
+  }
+  wsync(T);
+  if (!sm.last) return;
+  if (!d.aux) {             // partials only: just reset the slot's counters
+    if (t == 0) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+    return;
+  }
+  const double* part = reinterpret_cast<const double*>(d.out);
+  const uint64_t nb = (d.n + kRedBlock - 1) / kRedBlock;
+  double* s0 = sm.comb;
+  double* s1 = sm.comb + kRedVLanes;
+  for (uint32_t j = t; j < kRedVLanes; j += T) {
+    double acc = 0.0;
+    uint64_t i = j;
+    for (; i + 7ull * kRedVLanes < nb; i += 8ull * kRedVLanes) {   // eight loads in flight, added in order
+      double v[8];
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) v[u] = ld_cg_f64(part + i + u * kRedVLanes);
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; i < nb; i += kRedVLanes) acc += ld_cg_f64(part + i);
+    s0[j] = acc;
+  }
+  wsync(T);
+  uint32_t o = kRedVLanes / 2;
+  if (T == kRedVLanes) {    // one virtual lane per thread: levels >= 32 in shared memory, the rest in registers
+    for (; o >= 32; o >>= 1) {
+      s1[t] = s0[t] + s0[t ^ o];
+      wsync(T);
+      double* x = s0; s0 = s1; s1 = x;
+    }
+    const double v = butterfly32(s0[t]);
+    if (t == 0) st_f64(reinterpret_cast<double*>(d.aux), v);
   } else {
-    const uint4* x4 = reinterpret_cast<const uint4*>(x);
-    const uint64_t vb = p.b >> 2, ve = p.e >> 2;
-    uint64_t v = vb + t;
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (; v + uint64_t(U - 1) * T < ve; v += uint64_t(U) * T) {
-      uint4 r[U];
+    for (; o >= 1; o >>= 1) {
+      for (uint32_t j = t; j < kRedVLanes; j += T) s1[j] = s0[j] + s0[j ^ o];
+      wsync(T);
+      double* x = s0; s0 = s1; s1 = x;
+    }
+    if (t == 0) st_f64(reinterpret_cast<double*>(d.aux), s0[0]);
+  }
+  if (t == 0) {
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
+// Dynamic blocks through the TMA ring (T >= 64).  Lane 0 of warp 0 produces:
+// a static share of blocks by rank first, then pool claims of `claim_n`
+// blocks, the next claim in flight while the current one's copies are issued.
+// Consumer warp cw takes sub-blocks cw, cw + ncw, ... of every stage: reads
+// its two vectors per lane, releases the stage, then sums; the warp whose
+// sub-block completes the stage's count folds the 16 sums into out[block].
+// Sub-block sums live in shared memory by stage and position parity: a stage
+// is refilled only after every warp has passed it, so the next use of the
+// same parity cannot start before this one's fold is done.
+__device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint32_t count, uint32_t* ctr,
+                                           ReduceSmem& sm, uint32_t T, Ring& r, uint32_t& g, uint32_t share8,
+                                           uint32_t claim_n) {
+  const uint4* x4 = reinterpret_cast<const uint4*>(d.in0);
+  const uint32_t* xu = reinterpret_cast<const uint32_t*>(d.in0);
+  double* part = reinterpret_cast<double*>(d.out);
+  const uint64_t nv = d.n >> 2;                                   // full vectors, all blocks
+  const uint32_t tail = uint32_t(d.n & 3);
+  const uint32_t nb = uint32_t((d.n + kRedBlock - 1) / kRedBlock);
+  // static share: share8/8 of a fair share when every worker has >= 4
+  // blocks, else whatever divides evenly; the pool is the rest
+  const uint32_t fair = nb / count;
+  const uint32_t share = nb >= 4 * count ? (share8 * fair) / 8 : fair;
+  const uint32_t pool0 = share * count;
+  const uint32_t c0 = g, S = r.stages;
+  if (threadIdx.x == 0) {
+    uint32_t f = c0;
+    auto fill = [&](uint32_t b) {                                  // b = block or kTileEnd
+      const uint32_t st = f % S;
+      mbar_wait(r.empty + st, ((f / S) & 1u) ^ 1u);
+      r.tile[st] = b;
+      if (b == kTileEnd) {
+        mbar_arrive(r.full + st);                                  // wake consumers, no bytes
+      } else {
+        const uint64_t v0 = uint64_t(b) * kRedVecs;
+        const uint32_t bytes = v0 < nv ? uint32_t(min(uint64_t(kRedVecs), nv - v0)) * 16u : 0u;
+        mbar_expect_tx(r.full + st, bytes);                        // 0 bytes: a tail-only block
+        if (bytes) bulk_g2s(r.buf + st * kStageBytes, x4 + v0, bytes, r.full + st);
+      }
+      ++f;
+    };
+    // the first claim is issued before the static copies: its L2 round trip overlaps them
+    uint32_t claim = pool0 < nb ? atomicAdd(ctr + 1, claim_n) : nb;
+    for (uint32_t i = 0; i < share; ++i) fill(rank * share + i);
+    while (pool0 + claim < nb) {
+      const uint32_t b = pool0 + claim;
+      const uint32_t next = b + claim_n < nb ? atomicAdd(ctr + 1, claim_n) : nb;
+      for (uint32_t k = 0; k < claim_n && b + k < nb; ++k) fill(b + k);
+      claim = next;
+    }
+    fill(kTileEnd);
+    *r.gshared = f;
+  } else if (threadIdx.x >= 32) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t cw = (threadIdx.x >> 5) - 1, ncw = (T >> 5) - 1;
+    for (uint32_t c = c0;; ++c) {
+      const uint32_t st = c % S, par = (c / S) & 1u;
+      mbar_wait(r.full + st, par);
+      const uint32_t b = r.tile[st];
+      if (b == kTileEnd) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(r.empty + st);
+        break;
+      }
+      const uint8_t* stage = r.buf + st * kStageBytes;
+      const uint64_t v0 = uint64_t(b) * kRedVecs;
+      const uint32_t nvt = v0 < nv ? uint32_t(min(uint64_t(kRedVecs), nv - v0)) : 0u;
+      const uint32_t tl = b == nb - 1 ? tail : 0u;
+      // a lane's two vectors of sub-block si: from the stage, except the
+      // block's partial tail vector (not in the stage: read from global)
+      auto lane_part = [&](uint32_t si) -> double {
+        const uint32_t v1 = 64 * si + lane, v2 = v1 + 32;
+        const uint32_t a1 = vec_elems(v1, nvt, tl), a2 = vec_elems(v2, nvt, tl);
+        auto get = [&](uint32_t v, uint32_t m) -> float4 {
+          if (m == 4) return as_f4(lds4(stage + 16 * v));
+          float e[4] = {0.f, 0.f, 0.f, 0.f};
+          for (uint32_t q = 0; q < m; ++q) e[q] = __uint_as_float(ld_cg1(xu + 4 * (v0 + v) + q));
+          return make_float4(e[0], e[1], e[2], e[3]);
+        };
+        return sub_lane(get(v1, a1), a1, get(v2, a2), a2);
+      };
+      // this warp's sub-blocks cw, cw + ncw, ...: two at a time; the stage is
+      // released right after the warp's last shared-memory read, before the
+      // butterflies
+      uint32_t si = cw, done = 0;
+      bool released = false;
+      for (;;) {
+        uint32_t id0 = kRedSubs, id1 = kRedSubs;
+        double l0 = 0.0, l1 = 0.0;
+        if (si < kRedSubs) { id0 = si; l0 = lane_part(si); si += ncw; }
+        if (si < kRedSubs) { id1 = si; l1 = lane_part(si); si += ncw; }
+        if (si >= kRedSubs && !released) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(r.empty + st);
+          released = true;
+        }
+        if (id0 < kRedSubs) {
+          const double sv = butterfly32(l0);
+          if (lane == 0) sm.sub[par][st][id0] = sv;
+          ++done;
+        }
+        if (id1 < kRedSubs) {
+          const double sv = butterfly32(l1);
+          if (lane == 0) sm.sub[par][st][id1] = sv;
+          ++done;
+        }
+        if (si >= kRedSubs) break;
+      }
+      uint32_t prev = 0;
+      if (lane == 0) {
+        __threadfence_block();                    // this warp's sums before its count
+        prev = atomicAdd(&sm.cnt[par][st], done);
+      }
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev + done == kRedSubs && lane == 0) { // this warp completed the block: fold it
+        __threadfence_block();
+        const volatile double* sv = sm.sub[par][st];
+        double v[kRedSubs];
 #pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = ld_cg4(x4 + v + u * T);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        s.x += __uint_as_float(r[u].x); s.y += __uint_as_float(r[u].y);
-        s.z += __uint_as_float(r[u].z); s.w += __uint_as_float(r[u].w);
+        for (uint32_t k = 0; k < kRedSubs; ++k) v[k] = sv[k];
+        st_f64(part + b, tree16(v));
+        sm.cnt[par][st] = 0;
       }
     }
-    for (; v < ve; v += T) {
-      uint4 r = ld_cg4(x4 + v);
-      s.x += __uint_as_float(r.x); s.y += __uint_as_float(r.y);
-      s.z += __uint_as_float(r.z); s.w += __uint_as_float(r.w);
-    }
-    acc = (s.x + s.y) + (s.z + s.w);
-    for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) acc += __uint_as_float(ld_cg1((const uint32_t*)x + i));
   }
-  acc = warp_sum(acc);
-  const uint32_t warp = t >> 5, lane = t & 31, nwarps = (T + 31) >> 5;
-  if (lane == 0) sm.part[warp] = acc;
-  wsync(T);
-  if (warp == 0) {
-    float v = lane < nwarps ? sm.part[lane] : 0.f;
-    v = warp_sum(v);
-    if (lane == 0) {
-      reinterpret_cast<float*>(d.out)[rank] = v;
-      uint32_t last = 0;
-      if (d.aux) {
-        // acq_rel RMW: releases this worker's partial, and the last arrival
-        // acquires every other worker's -- no separate fences
-        uint32_t prev;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
-        last = prev == count - 1;
-      }
-      sm.last = last;
-    }
+  wsync(T);                                                        // gshared visible; stream done
+  g = *r.gshared;
+  reduce_finish(d, count, ctr, sm, T);
+}
+
+// Static blocks, 128-bit (or scalar) loads straight from global memory: the
+// narrow-dispatch and misaligned path.  Worker rank r takes the r-th
+// contiguous run of blocks; its warps take the run's blocks round robin.
+__device__ __forceinline__ void reduce_static(const lk_desc& d, uint32_t rank, uint32_t count, uint32_t* ctr,
+                                              ReduceSmem& sm, uint32_t T) {
+  const float* x = reinterpret_cast<const float*>(d.in0);
+  double* part = reinterpret_cast<double*>(d.out);
+  const uint64_t nb = (d.n + kRedBlock - 1) / kRedBlock;
+  const uint64_t per = (nb + count - 1) / count;
+  const uint64_t b0 = min(nb, uint64_t(rank) * per), b1 = min(nb, b0 + per);
+  const bool vec = !(d.flags & LK_DF_SCALAR);
+  const uint32_t warp = threadIdx.x >> 5, nwarps = T >> 5;
+  for (uint64_t b = b0 + warp; b < b1; b += nwarps) {
+    const double p = block_sum_global(x, b, d.n, vec);
+    if ((threadIdx.x & 31) == 0) st_f64(part + b, p);
   }
-  wsync(T);
-  if (sm.last && warp == 0) {
-    const uint32_t* partials = reinterpret_cast<const uint32_t*>(d.out);
-    // the loads of a group are independent, so their L2 round trips overlap
-    // (one at a time they cost ~0.2 us each); the add order per lane is
-    // unchanged: r = lane, lane + 32, ...
-    double tot = 0.0;
-    for (uint32_t r0 = 0; r0 < count; r0 += 32 * 5) {
-      float v[5];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        const uint32_t r = r0 + 32 * k + lane;
-        v[k] = r < count ? __uint_as_float(ld_cg1(partials + r)) : 0.f;
-      }
-#pragma unroll
-      for (int k = 0; k < 5; ++k)
-        if (r0 + 32 * k + lane < count) tot += double(v[k]);
-    }
-    tot = warp_sum(tot);
-    if (lane == 0) {
-      *reinterpret_cast<double*>(d.aux) = tot;
-      *ctr = 0;
-    }
-  }
+  reduce_finish(d, count, ctr, sm, T);
 }
 
 // native.py:63-67 counts to `iterations`.  Each iteration here reads %clock
@@ -562,7 +768,8 @@ __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
 // every field access on the per-tile path into an LDL.
 __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
                                           uint32_t* ctr, ReduceSmem& rs, uint32_t T, Ring& ring, bool ring_on,
-                                          uint32_t& g, bool dyn = false) {
+                                          uint32_t& g, bool dyn = false, uint32_t red_share8 = 6,
+                                          uint32_t red_claim = kRedClaim) {
   const Part p = partition(d.n, rank, count);
   const bool tma = ring_on && !(d.flags & LK_DF_SCALAR);
   dyn = dyn && tma && T >= 64 && ring.tile != nullptr;
@@ -594,7 +801,10 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
       }
       break;
     }
-    case LK_KIND_BLOCK_REDUCE_F32: reduce_chunk<8>(d, p, rank, count, ctr, rs, T, ring, ring_on, g); break;
+    case LK_KIND_BLOCK_REDUCE_F32:
+      if (tma && T >= 64 && ring.tile != nullptr) reduce_dyn(d, rank, count, ctr, rs, T, ring, g, red_share8, red_claim);
+      else reduce_static(d, rank, count, ctr, rs, T);
+      break;
     default: break;
   }
 }
@@ -1196,6 +1406,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     sm.chan[0] = 0ull;              // {NOP, count 0}: nothing new on either channel
     sm.chan[1] = 0ull;
     sm.stop = 0;
+    reduce_smem_init(sm.red);
   }
   __syncthreads();                  // the only CTA-wide barrier: before the roles split
   if (threadIdx.x >= T) {           // three extra warps: host-cell poller, mailbox poller, gateway
@@ -1331,7 +1542,8 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     // ~110 GB/s that way against ~85 GB/s through the ring, which wins only
     // once enough SMs share the dispatch to load HBM (tools/tma_vs_lsu_count.py)
     run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T, ring,
-              ring_ok && sm.count >= a.tma_min_workers, g, (a.flags & LK_CF_DYNAMIC_TILES) != 0);
+              ring_ok && sm.count >= a.tma_min_workers, g, (a.flags & LK_CF_DYNAMIC_TILES) != 0, a.red_share8,
+              a.red_claim);
     wsync(T);
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();
@@ -1358,6 +1570,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
 __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, uint32_t* ctr, int use_tma) {
   __shared__ ReduceSmem rs;
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ uint32_t tile[kMaxStages], gsh;
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   if (single_thread_kind(d.kind)) {
     // the result goes to global memory (the counter line's spare word), which
@@ -1365,8 +1578,10 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
     if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) ctr[3] = busy_loop(d.iterations);
     return;
   }
-  Ring ring{dyn_smem, full, empty, kDefaultStages, nullptr, nullptr};   // static tiles only
+  Ring ring{dyn_smem, full, empty, kDefaultStages, tile, &gsh};
   uint32_t g = 0;
+  if (threadIdx.x == 0) reduce_smem_init(rs);
+  __syncthreads();
   if (use_tma) ring_init(ring, blockDim.x);
   run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, ring, use_tma != 0, g);
 }

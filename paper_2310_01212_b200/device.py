@@ -14,7 +14,8 @@ empty               --                            --
 busy_loop           --                            --
 vector_add_i32      (a, b) int32                  out int32 (may alias a/b)
 saxpy_f32           (x, y) float32                out float32 (y for in-place)
-block_reduce_f32    x float32                     partials float32[count];
+block_reduce_f32    x float32                     partials float64[ceil(n/4096)]
+                                                  (one per 4096-element block);
                                                   ``total_ref`` float64[1]
 hbm_stream          src (any, 4-B elements)       dst
 =================== ============================= ===========================
@@ -44,6 +45,15 @@ SINGLE_THREAD_KINDS = (EMPTY, BUSY_LOOP)
 
 # algorithmic HBM bytes per element
 BYTES_PER_ELEMENT = {VECTOR_ADD_I32: 12, SAXPY_F32: 12, BLOCK_REDUCE_F32: 4, HBM_STREAM: 8}
+# (block_reduce_f32 also writes 8 B per 4096 elements of block partials: +0.2%)
+
+
+REDUCE_BLOCK = 4096   # block_reduce_f32: elements per block partial
+
+
+def reduce_blocks(n: int) -> int:
+    """Block partials a block_reduce_f32 of n elements writes (float64 each)."""
+    return -(-int(n) // REDUCE_BLOCK)
 
 
 class DeviceBuffer:
@@ -213,6 +223,11 @@ class WorkDescriptor:
             nb = _nbytes(self.total_ref)
             if self.total_ref is not None and nb is not None and nb < 8:
                 raise ConfigError("block_reduce_f32: total_ref must hold one float64")
+            need = 8 * reduce_blocks(d.n)
+            nb = _nbytes(self.data_out_ref)
+            if nb is not None and nb < need:
+                raise ConfigError(f"block_reduce_f32: data_out_ref needs {need} bytes "
+                                  f"(one float64 per {REDUCE_BLOCK}-element block), got {nb}")
         d.in0 = _addr(ins[0])
         d.in1 = _addr(ins[1]) if len(ins) > 1 else 0
         d.out = _addr(self.data_out_ref)

@@ -12,7 +12,7 @@ import pytest
 
 from oracle import work as W
 from paper_2310_01212_b200 import native
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks
 
 pytestmark = pytest.mark.gpu
 
@@ -41,12 +41,16 @@ def test_baseline_kernel_same_results(tma, n):
     np.testing.assert_array_equal(dz.download(np.float32, n).view(np.uint32),
                                   W.saxpy_f32(1.5, x, y).view(np.uint32))
     xi = np.random.default_rng(9).integers(0, 8, n).astype(np.float32)
-    dxi, dp, dt = DeviceBuffer.from_array(xi), DeviceBuffer(4 * b.grid), DeviceBuffer(8)
+    dxi, dp, dt = DeviceBuffer.from_array(xi), DeviceBuffer(8 * max(1, reduce_blocks(n))), DeviceBuffer(8)
     b.launch(WorkDescriptor(slot=0, kind="block_reduce_f32", data_in_ref=dxi, data_out_ref=dp, total_ref=dt))
     b.wait()
-    np.testing.assert_array_equal(dp.download(np.float32, b.grid).astype(np.float64),
-                                  W.block_reduce_partials(xi, b.grid))
+    np.testing.assert_array_equal(dp.download(np.float64, reduce_blocks(n)), W.block_reduce_partials(xi))
     assert dt.download(np.float64, 1)[0] == W.block_reduce_total(xi)
+    xu = _f32(n, 21)
+    dxu = DeviceBuffer.from_array(xu)
+    b.launch(WorkDescriptor(slot=0, kind="block_reduce_f32", data_in_ref=dxu, data_out_ref=dp, total_ref=dt))
+    b.wait()   # the same bits as the persistent kernel's reduce: one definition
+    assert dt.download(np.float64, 1)[0] == W.block_reduce_total(xu)
     b.close()
 
 

@@ -14,7 +14,7 @@ from oracle import projection
 from oracle import protocol as O
 from oracle import work as W
 from paper_2310_01212_b200 import host, native
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks
 
 pytestmark = pytest.mark.gpu
 
@@ -83,14 +83,13 @@ def test_random_programs(seed):
                         dy.download(np.float32, n).view(np.uint32), W.saxpy_f32(alpha, x, y).view(np.uint32))
                 elif kind == "block_reduce_f32":
                     x = nrng.integers(0, 8, n).astype(np.float32)
-                    dx, dp, dt = DeviceBuffer.from_array(x), DeviceBuffer(4 * NW), DeviceBuffer(8)
+                    nbk = reduce_blocks(n)
+                    dx, dp, dt = DeviceBuffer.from_array(x), DeviceBuffer(8 * nbk), DeviceBuffer(8)
                     bufs += [dx, dp, dt]
                     w = WorkDescriptor(slot=slot, kind=kind, data_in_ref=dx, data_out_ref=dp, total_ref=dt)
-                    cnt = len(ids)
 
-                    def check(dp=dp, dt=dt, x=x, cnt=cnt):
-                        np.testing.assert_array_equal(dp.download(np.float32, cnt).astype(np.float64),
-                                                      W.block_reduce_partials(x, cnt))
+                    def check(dp=dp, dt=dt, x=x, nbk=nbk):
+                        np.testing.assert_array_equal(dp.download(np.float64, nbk), W.block_reduce_partials(x))
                         assert dt.download(np.float64, 1)[0] == W.block_reduce_total(x)
                 else:
                     src = nrng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)

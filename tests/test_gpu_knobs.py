@@ -13,7 +13,7 @@ from oracle import projection
 from oracle import protocol as O
 from oracle import work as W
 from paper_2310_01212_b200 import host, native
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks
 from paper_2310_01212_b200.errors import UsageError
 
 pytestmark = pytest.mark.gpu
@@ -87,15 +87,14 @@ def test_knob_program(name):
                                       W.saxpy_f32(-0.75, x, y).view(np.uint32))
 
         v = rng.integers(0, 16, n).astype(np.float32)
-        dv, dp, dt = DeviceBuffer.from_array(v), DeviceBuffer(4 * NW), DeviceBuffer(8)
+        dv, dp, dt = DeviceBuffer.from_array(v), DeviceBuffer(8 * reduce_blocks(n)), DeviceBuffer(8)
         bufs += [dv, dp, dt]
         for rep in range(2):   # the reduce counter re-arms
             s.trigger(full, WorkDescriptor(slot=4, kind="block_reduce_f32", data_in_ref=dv, data_out_ref=dp,
                                            total_ref=dt))
             s.wait(full)
             program.append((full, 4))
-            np.testing.assert_array_equal(dp.download(np.float32, NW).astype(np.float64),
-                                          W.block_reduce_partials(v, NW))
+            np.testing.assert_array_equal(dp.download(np.float64, reduce_blocks(n)), W.block_reduce_partials(v))
             assert dt.download(np.float64, 1)[0] == W.block_reduce_total(v)
 
         if s.cfg.num_slots == 8:

@@ -12,7 +12,7 @@ import pytest
 
 from oracle import work as W
 from paper_2310_01212_b200 import host, native
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks
 from paper_2310_01212_b200.errors import ConfigError
 
 pytestmark = pytest.mark.gpu
@@ -120,34 +120,71 @@ def test_saxpy_after_host_rewrite_is_coherent(session):
     np.testing.assert_array_equal(do.download(np.float32, n), W.saxpy_f32(-0.75, x2, y))
 
 
+def _reduce(session, mask, x, slot):
+    n = x.size
+    dx, dp, dt = DeviceBuffer.from_array(x), DeviceBuffer(8 * max(1, reduce_blocks(n))), DeviceBuffer(8)
+    run(session, mask, WorkDescriptor(slot=slot, kind="block_reduce_f32", data_in_ref=dx, data_out_ref=dp,
+                                      total_ref=dt))
+    parts = dp.download(np.float64, reduce_blocks(n))
+    tot = dt.download(np.float64, 1)[0]
+    for b in (dx, dp, dt):
+        b.free()
+    return parts, tot
+
+
 @pytest.mark.parametrize("workers", [1, 7, 148])
 def test_block_reduce_exact_on_small_integers(session, workers):
     n = 3_000_017
     x = np.random.default_rng(9).integers(0, 8, n).astype(np.float32)
-    dx, dp, dt = DeviceBuffer.from_array(x), DeviceBuffer(4 * 148), DeviceBuffer(8)
-    mask = host.full_mask(workers)
-    run(session, mask, WorkDescriptor(slot=30, kind="block_reduce_f32", data_in_ref=dx, data_out_ref=dp,
-                                      total_ref=dt))
-    parts = dp.download(np.float32, workers).astype(np.float64)
-    np.testing.assert_array_equal(parts, W.block_reduce_partials(x, workers))
-    assert dt.download(np.float64, 1)[0] == W.block_reduce_total(x)
+    parts, tot = _reduce(session, host.full_mask(workers), x, 30)
+    np.testing.assert_array_equal(parts, W.block_reduce_partials(x))
+    assert tot == W.block_reduce_total(x) == float(x.astype(np.float64).sum())
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4095, 4096, 4097, 4099, 8192 + 2, 1_048_573, 9_000_003])
+def test_block_reduce_bit_exact_any_size(session, n):
+    """Block partials and total bit-identical to the oracle's fixed order of
+    operations on U[-1,1) data, for sizes around the block and vector edges
+    (tail-only last blocks included)."""
+    x = _f32(n, 11)
+    parts, tot = _reduce(session, host.full_mask(session.num_workers), x, 32)
+    np.testing.assert_array_equal(parts.view(np.uint64), W.block_reduce_partials(x).view(np.uint64))
+    assert np.float64(tot).view(np.uint64) == np.float64(W.block_reduce_total(x)).view(np.uint64)
 
 
 def test_block_reduce_uniform_within_rtol(session):
     n = 16 << 20   # 64 MiB of fp32
     x = _f32(n, 10, 0.0, 1.0)
-    dx, dp, dt = DeviceBuffer.from_array(x), DeviceBuffer(4 * 148), DeviceBuffer(8)
     mask = host.full_mask(session.num_workers)
-    run(session, mask, WorkDescriptor(slot=31, kind="block_reduce_f32", data_in_ref=dx, data_out_ref=dp,
-                                      total_ref=dt))
-    want = W.block_reduce_partials(x, session.num_workers)
-    np.testing.assert_allclose(dp.download(np.float32, session.num_workers), want, rtol=RTOL_F32_REDUCE)
-    np.testing.assert_allclose(dt.download(np.float64, 1)[0], W.block_reduce_total(x), rtol=RTOL_F32_REDUCE)
-    # repeated reductions are deterministic (fixed combine order)
-    first = dt.download(np.float64, 1)[0]
-    run(session, mask, WorkDescriptor(slot=31, kind="block_reduce_f32", data_in_ref=dx, data_out_ref=dp,
-                                      total_ref=dt))
-    assert dt.download(np.float64, 1)[0] == first
+    parts, tot = _reduce(session, mask, x, 31)
+    np.testing.assert_array_equal(parts, W.block_reduce_partials(x))
+    np.testing.assert_allclose(tot, float(x.astype(np.float64).sum()), rtol=RTOL_F32_REDUCE)
+    assert tot == W.block_reduce_total(x)
+    # the result does not depend on the worker set or the schedule: any mask,
+    # any run, the same bits (dynamic block claiming)
+    for m in (mask, host.mask_of(range(0, session.num_workers, 3)), 0b1011):
+        p2, t2 = _reduce(session, m, x, 31)
+        assert t2 == tot
+        np.testing.assert_array_equal(p2, parts)
+
+
+def test_block_reduce_misaligned_input(session):
+    n = 100_003
+    base = _f32(n + 1, 13)
+    dbase = DeviceBuffer.from_array(base)
+    dp, dt = DeviceBuffer(8 * reduce_blocks(n)), DeviceBuffer(8)
+    run(session, host.full_mask(session.num_workers),
+        WorkDescriptor(slot=33, kind="block_reduce_f32", data_in_ref=dbase.ptr + 4, n=n, data_out_ref=dp,
+                       total_ref=dt))
+    np.testing.assert_array_equal(dp.download(np.float64, reduce_blocks(n)), W.block_reduce_partials(base[1:]))
+    assert dt.download(np.float64, 1)[0] == W.block_reduce_total(base[1:])
+
+
+def test_block_reduce_short_partials_buffer_refused(session):
+    x = DeviceBuffer(4 * 10_000)
+    with pytest.raises(ConfigError):
+        WorkDescriptor(slot=34, kind="block_reduce_f32", data_in_ref=x, data_out_ref=DeviceBuffer(8),
+                       total_ref=DeviceBuffer(8)).to_c()
 
 
 @pytest.mark.parametrize("passes", [1, 3])

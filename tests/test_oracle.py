@@ -7,6 +7,7 @@ import json
 import random
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 from oracle import cpu_session, projection
@@ -260,3 +261,58 @@ def test_product_state_machine_walks_match_the_oracle():
             else:
                 case = {"phase": want["phase"], "slot": want["slot"]}
     walk()
+
+
+def _reduce_scalar(x):
+    """A literal, loop-by-loop restatement of block_reduce_f32's order of
+    operations (lk_kernels.cu: block_sum_smem / block_sum_global /
+    reduce_finish) to pin the vectorised oracle on small inputs."""
+    n = len(x)
+    nb = -(-n // 4096)
+    parts = []
+    for b in range(nb):
+        subs = []
+        for sb in range(16):
+            lanes = []
+            for lane in range(32):
+                a = [np.float32(0.0)] * 4
+                for h in range(2):                      # vector 64s + l, then 64s + 32 + l
+                    v = 64 * sb + 32 * h + lane
+                    for c in range(4):
+                        e = b * 4096 + 4 * v + c
+                        if e < n:
+                            a[c] = np.float32(a[c] + x[e])   # fp32, round to nearest
+                lanes.append((float(a[0]) + float(a[1])) + (float(a[2]) + float(a[3])))
+            o = 16
+            while o >= 1:
+                lanes = [lanes[i] + lanes[i ^ o] for i in range(32)]
+                o //= 2
+            subs.append(lanes[0])
+        while len(subs) > 1:
+            subs = [subs[i] + subs[i + 1] for i in range(0, len(subs), 2)]
+        parts.append(subs[0])
+    s = [0.0] * 512
+    for i, p in enumerate(parts):
+        s[i % 512] = s[i % 512] + p
+    o = 256
+    while o >= 1:
+        s = [s[j] + s[j ^ o] for j in range(512)]
+        o //= 2
+    return parts, s[0]
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 4096, 4101, 9000])
+def test_block_reduce_oracle_matches_scalar_restatement(n):
+    from oracle import work as W
+    x = np.random.default_rng(n).uniform(-1, 1, n).astype(np.float32)
+    parts, tot = _reduce_scalar(x)
+    np.testing.assert_array_equal(W.block_reduce_partials(x), np.array(parts, dtype=np.float64))
+    assert W.block_reduce_total(x) == tot
+
+
+def test_block_reduce_oracle_exact_on_integers_and_close_on_uniform():
+    from oracle import work as W
+    x = np.random.default_rng(1).integers(0, 8, 1 << 20).astype(np.float32)
+    assert W.block_reduce_total(x) == float(x.astype(np.float64).sum())
+    u = np.random.default_rng(2).uniform(0, 1, 1 << 20).astype(np.float32)
+    assert abs(W.block_reduce_total(u) - float(u.astype(np.float64).sum())) <= 1e-8 * float(u.sum())   # fp32 lane sums of 32 values: far inside rtol 1e-6

@@ -16,7 +16,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2310_01212_b200 import native  # noqa: E402
-from paper_2310_01212_b200.device import BYTES_PER_ELEMENT, DeviceBuffer, WorkDescriptor  # noqa: E402
+from paper_2310_01212_b200.device import BYTES_PER_ELEMENT, DeviceBuffer, WorkDescriptor, reduce_blocks  # noqa: E402
 
 
 def main():
@@ -28,7 +28,7 @@ def main():
     n = (args.mib << 20) // 4
     base = native.LaunchSyncBaseline(device=0)
     x, y, o = DeviceBuffer(4 * n), DeviceBuffer(4 * n), DeviceBuffer(4 * n)
-    parts, tot = DeviceBuffer(4 * 148), DeviceBuffer(8)
+    parts, tot = DeviceBuffer(8 * reduce_blocks(n)), DeviceBuffer(8)
     works = {
         "saxpy_f32": WorkDescriptor(slot=0, kind="saxpy_f32", data_in_ref=(x, y), data_out_ref=y, alpha=1.5),
         "vector_add_i32": WorkDescriptor(slot=0, kind="vector_add_i32", data_in_ref=(x, y), data_out_ref=o, n=n),

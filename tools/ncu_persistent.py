@@ -14,7 +14,7 @@ import sys
 
 sys.path.insert(0, ".")
 from paper_2310_01212_b200 import native  # noqa: E402
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks  # noqa: E402
 
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 kind = sys.argv[2] if len(sys.argv) > 2 else ""
@@ -33,7 +33,7 @@ else:
             bufs += [x, y]
             works.append(WorkDescriptor(slot=1 + k, kind="saxpy_f32", data_in_ref=(x, y), data_out_ref=y, alpha=1.5))
         else:
-            x, part, tot = DeviceBuffer(4 * n), DeviceBuffer(4 * 160), DeviceBuffer(8)
+            x, part, tot = DeviceBuffer(4 * n), DeviceBuffer(8 * reduce_blocks(n)), DeviceBuffer(8)
             bufs += [x, part, tot]
             works.append(WorkDescriptor(slot=1 + k, kind="block_reduce_f32", data_in_ref=x, data_out_ref=part,
                                         total_ref=tot))

@@ -6,7 +6,7 @@ sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 
 from paper_2310_01212_b200 import host, native  # noqa: E402
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks  # noqa: E402
 
 native.pin_host_thread(0)
 for mode in ("gateway", "direct"):
@@ -16,7 +16,7 @@ for mode in ("gateway", "direct"):
     el = (64 << 20) // 4
     sets = []
     for k in range(8):
-        x, p, t = DeviceBuffer(4 * el), DeviceBuffer(4 * 160), DeviceBuffer(8)
+        x, p, t = DeviceBuffer(4 * el), DeviceBuffer(8 * reduce_blocks(el)), DeviceBuffer(8)
         sets.append((x, p, t, WorkDescriptor(slot=10 + k, kind="block_reduce_f32", data_in_ref=x, data_out_ref=p,
                                              total_ref=t)))
         s.register(sets[-1][3], full)

@@ -6,7 +6,7 @@ sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 
 from paper_2310_01212_b200 import host, native  # noqa: E402
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
+from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks  # noqa: E402
 
 native.pin_host_thread(0)
 s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway"))
@@ -16,7 +16,7 @@ for mib in (4, 16, 64):
     el = (mib << 20) // 4
     sets = []
     for k in range(16):
-        x, o, p, t = DeviceBuffer(4 * el), DeviceBuffer(4 * el), DeviceBuffer(4 * 160), DeviceBuffer(8)
+        x, o, p, t = DeviceBuffer(4 * el), DeviceBuffer(4 * el), DeviceBuffer(8 * reduce_blocks(el)), DeviceBuffer(8)
         sets.append((x, o, p, t))
     for kind in ("block_reduce_f32", "hbm_stream"):
         works = []
