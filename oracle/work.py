@@ -64,14 +64,12 @@ def _butterfly(v: np.ndarray, axis_len: int) -> np.ndarray:
 
 def block_reduce_partials(x: np.ndarray) -> np.ndarray:
     """Per-block fp64 sums, one per 4096-element block (ceil(n/4096) values).
-    A block is 16 sub-blocks of 64 float4 vectors.  In sub-block s, lane l
-    (0..31) adds vector 64s + l, then vector 64s + 32 + l, into one fp32
-    accumulator per component (starting at +0, round to nearest); lane value
-    (a0 + a1) + (a2 + a3) in fp64; a 32-lane fp64 xor butterfly gives the
-    sub-block sum; the block sum is the pairwise fp64 tree over the 16
-    sub-block sums in index order.  Missing elements of a short last block
-    add nothing (+0.0 is exact here: the accumulators start at +0.0 and can
-    never hold -0.0)."""
+    Block order of operations: lane l (0..31) owns the float4 vectors l + 32k
+    of the block, k ascending, into two fp32 accumulators per component, one
+    for even and one for odd k (round-to-nearest adds); a_c = even_c + odd_c
+    in fp32; lane value (a0 + a1) + (a2 + a3) in fp64; then a 32-lane fp64
+    xor butterfly.  Missing elements of a short last block add nothing (+0.0
+    is exact here: the accumulators start at +0.0 and can never hold -0.0)."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     n = x.size
     nb = -(-n // REDUCE_BLOCK)
@@ -79,15 +77,15 @@ def block_reduce_partials(x: np.ndarray) -> np.ndarray:
         return np.zeros(0, np.float64)
     pad = np.zeros(nb * REDUCE_BLOCK, np.float32)
     pad[:n] = x
-    blk = pad.reshape(nb, 16, 2, 32, 4)       # (block, sub, half, lane, component): element 4*(64s + 32h + l) + c
-    acc = (np.float32(0.0) + blk[:, :, 0]).astype(np.float32)
-    acc = (acc + blk[:, :, 1]).astype(np.float32)
-    a = acc.astype(np.float64)
-    lane = (a[..., 0] + a[..., 1]) + (a[..., 2] + a[..., 3])     # (block, sub, lane)
-    sub = _butterfly(lane, 32)[..., 0]                           # (block, sub)
-    while sub.shape[1] > 1:                                      # pairwise tree in index order
-        sub = sub[:, 0::2] + sub[:, 1::2]
-    return sub[:, 0]
+    blk = pad.reshape(nb, 32, 32, 4)          # (block, k, lane, component): element 4*(lane + 32k) + c
+    ev = np.zeros((nb, 32, 4), np.float32)
+    od = np.zeros((nb, 32, 4), np.float32)
+    for k in range(0, 32, 2):
+        ev = (ev + blk[:, k]).astype(np.float32)
+        od = (od + blk[:, k + 1]).astype(np.float32)
+    a = (ev + od).astype(np.float32).astype(np.float64)
+    lane = (a[..., 0] + a[..., 1]) + (a[..., 2] + a[..., 3])
+    return _butterfly(lane, 32)[:, 0]
 
 
 def block_reduce_combine(partials: np.ndarray) -> float:

@@ -873,7 +873,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   {   // block_reduce schedule (tuning overrides for tools/reduce_sizes.py)
     const char* e1 = getenv("LK_RED_SHARE8");
     const char* e2 = getenv("LK_RED_CLAIM");
-    a.red_share8 = e1 ? uint32_t(atoi(e1)) : 6u;
+    a.red_share8 = e1 ? uint32_t(atoi(e1)) : 2u;
     a.red_claim = e2 ? uint32_t(atoi(e2)) : 2u;
     if (a.red_share8 > 8) a.red_share8 = 8;
     if (a.red_claim < 1) a.red_claim = 1;

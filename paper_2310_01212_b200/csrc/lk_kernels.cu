@@ -127,11 +127,13 @@ constexpr uint32_t kDefaultStages = 6;
 
 struct Ring {
   uint8_t* buf;       // stages x kStageBytes, 128-B aligned, dynamic shared memory
-  uint64_t* full;     // stages mbarriers: 1 arrival (expect_tx) + tx bytes
-  uint64_t* empty;    // stages mbarriers: one arrival per consumer warp
+  uint64_t* full;     // 2 x kMaxStages mbarriers: [0, stages) the shared-consumer ring (maps): 1 arrival
+                      // (expect_tx) + tx bytes; [kMaxStages, +stages) the owner-warp ring (reduce)
+  uint64_t* empty;    // same layout: one arrival per consumer warp (maps) / the stage's owner warp (reduce)
   uint32_t stages;    // <= kMaxStages
   uint32_t* tile;     // stages: global tile index a stage holds (dynamic schedule), shared memory
   uint32_t* gshared;  // the ring count after a dynamic stream, for threads that did not count it
+  uint32_t* gred;     // shared memory: positions the owner-warp ring has used (persists across dispatches)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -178,7 +180,10 @@ __device__ __forceinline__ void ring_init(Ring& r, uint32_t T) {
     for (uint32_t k = 0; k < r.stages; ++k) {
       mbar_init(r.full + k, 1);
       mbar_init(r.empty + k, ring_consumer_warps(T));   // one arrival per consumer warp
+      mbar_init(r.full + kMaxStages + k, 1);
+      mbar_init(r.empty + kMaxStages + k, 1);           // the stage's owner warp
     }
+    if (r.gred) *r.gred = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   wsync(T);
@@ -414,36 +419,25 @@ __device__ __forceinline__ void map_tma_dyn(const lk_desc& d, uint32_t rank, uin
 // block_reduce_f32 is defined on fixed 4096-element blocks (oracle/work.py:
 // block_reduce_partials / block_reduce_combine), independent of the mask,
 // the worker count, the thread count, the schedule and the payload path:
-//   sub-block s (0..15) of a block = its float4 vectors [64s, 64s + 64);
-//     lane l (0..31) adds vectors 64s + l, then 64s + 32 + l, into one fp32
-//     accumulator per component (from +0); lane value (a0 + a1) + (a2 + a3)
-//     in fp64; a 32-lane fp64 xor butterfly gives the sub-block's sum;
-//   out[b]  = pairwise fp64 tree over the 16 sub-block sums, in index order;
+//   out[b]  = sum of block b: lane l of one warp owns the float4 vectors
+//             l + 32k (k ascending) into two fp32 accumulators per component
+//             (even / odd k), a_c = even + odd, lane value (a0 + a1) + (a2 + a3)
+//             in fp64, then a 32-lane fp64 xor butterfly;
 //   *aux    = fp64 combine of out[0, nb): virtual lane j of 512 adds
 //             out[j], out[j + 512], ... in order, then a 512-lane butterfly.
-// So any worker may sum any block and any warp any sub-block: blocks are
-// handed out dynamically (a static share per worker, the rest claimed from a
-// pool), which absorbs dispatch skew and slow SMs without changing a bit of
-// the result, while every consumer warp still reads only two vectors per lane
-// of each ring stage, as the map kinds do.
+// So any worker may sum any block: blocks are handed out dynamically (a
+// static share per worker, the rest claimed from a pool), which absorbs
+// dispatch skew and slow SMs without changing a bit of the result.
 constexpr uint32_t kRedBlock = 4096;              // elements per block = one 16-KiB ring stage
 constexpr uint32_t kRedVecs = kRedBlock / 4;      // float4 vectors per block
-constexpr uint32_t kRedSubs = 16;                 // sub-blocks per block (64 vectors each)
 constexpr uint32_t kRedVLanes = 512;              // virtual lanes of the combine
 constexpr uint32_t kRedClaim = 2;                 // blocks per pool claim
 static_assert(kRedBlock * 4 == kStageBytes, "a reduce block is one ring stage");
 
 struct ReduceSmem {
-  double comb[2 * kRedVLanes];             // the combine's two butterfly buffers
-  double sub[2][kMaxStages][kRedSubs];     // sub-block sums of a stage, by position parity
-  uint32_t cnt[2][kMaxStages];             // sub-blocks of a stage summed so far, by position parity
+  double comb[2 * kRedVLanes];   // the combine's two butterfly buffers
   uint32_t last;
 };
-
-// Called once per kernel by thread 0, before the CTA's first barrier.
-__device__ __forceinline__ void reduce_smem_init(ReduceSmem& sm) {
-  for (uint32_t k = 0; k < kMaxStages; ++k) sm.cnt[0][k] = sm.cnt[1][k] = 0;
-}
 
 __device__ __forceinline__ double butterfly32(double v) {
 #pragma unroll
@@ -451,32 +445,95 @@ __device__ __forceinline__ double butterfly32(double v) {
   return v;
 }
 
-__device__ __forceinline__ float4 as_f4(uint4 r) {
-  return make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z), __uint_as_float(r.w));
+// Lane accumulators are fp32, two per component -- even k and odd k, 16
+// sequential adds each (short FADD chains, no conversions) -- folded as
+// a_c = even_c + odd_c, then lane value (a0 + a1) + (a2 + a3) in fp64.
+struct RedAcc {
+  float e[4], o[4];
+};
+
+__device__ __forceinline__ void acc4(float (&a)[4], uint4 r) {
+  a[0] = __fadd_rn(a[0], __uint_as_float(r.x));
+  a[1] = __fadd_rn(a[1], __uint_as_float(r.y));
+  a[2] = __fadd_rn(a[2], __uint_as_float(r.z));
+  a[3] = __fadd_rn(a[3], __uint_as_float(r.w));
 }
 
-// A lane's part of a sub-block: its two vectors (either may be absent in a
-// short last block), `m1`/`m2` = elements present in each (0..4).
-__device__ __forceinline__ double sub_lane(float4 u, uint32_t m1, float4 w, uint32_t m2) {
-  float a[4] = {0.f, 0.f, 0.f, 0.f};
-  const float uu[4] = {u.x, u.y, u.z, u.w}, ww[4] = {w.x, w.y, w.z, w.w};
+__device__ __forceinline__ void acc_k(RedAcc& a, uint32_t k, uint4 r) {
+  if (k & 1) acc4(a.o, r); else acc4(a.e, r);
+}
+
+// The trailing n % 4 elements belong to vector `nvt` of the last block: the
+// lane's last vector (k = nvt / 32), so they are added after its loop.
+__device__ __forceinline__ void acc_tail(RedAcc& a, uint32_t nvt, const float* x, uint64_t first, uint32_t tail) {
+  float* h = ((nvt >> 5) & 1) ? a.o : a.e;
+  for (uint32_t c = 0; c < tail; ++c)
+    h[c] = __fadd_rn(h[c], __uint_as_float(ld_cg1(reinterpret_cast<const uint32_t*>(x) + first + c)));
+}
+
+__device__ __forceinline__ double block_fold(const RedAcc& a) {
+  double v[4];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    if (uint32_t(c) < m1) a[c] = __fadd_rn(a[c], uu[c]);
-    if (uint32_t(c) < m2) a[c] = __fadd_rn(a[c], ww[c]);
+  for (int c = 0; c < 4; ++c) v[c] = double(__fadd_rn(a.e[c], a.o[c]));
+  return butterfly32((v[0] + v[1]) + (v[2] + v[3]));
+}
+
+// A block's lane sums from a ring stage (nvt full vectors in shared memory).
+__device__ __forceinline__ RedAcc block_acc_smem(const uint8_t* stage, uint32_t nvt) {
+  const uint32_t lane = threadIdx.x & 31;
+  RedAcc a = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  if (nvt == kRedVecs) {
+#pragma unroll 4
+    for (uint32_t k = 0; k < 32; k += 2) {
+      const uint4 r0 = lds4(stage + 16 * (lane + 32 * k)), r1 = lds4(stage + 16 * (lane + 32 * (k + 1)));
+      acc4(a.e, r0);
+      acc4(a.o, r1);
+    }
+  } else {
+    for (uint32_t k = 0; k < 32; ++k) {
+      const uint32_t v = lane + 32 * k;
+      if (v < nvt) acc_k(a, k, lds4(stage + 16 * v));
+    }
   }
-  return (double(a[0]) + double(a[1])) + (double(a[2]) + double(a[3]));
+  return a;
 }
 
-// Elements of vector v (0..1023) of a block holding nvt full vectors plus
-// `tail` trailing elements.
-__device__ __forceinline__ uint32_t vec_elems(uint32_t v, uint32_t nvt, uint32_t tail) {
-  return v < nvt ? 4u : (v == nvt ? tail : 0u);
-}
-
-__device__ __forceinline__ double tree16(const double* s) {
-  return (((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]))) +
-         (((s[8] + s[9]) + (s[10] + s[11])) + ((s[12] + s[13]) + (s[14] + s[15])));
+// One block straight from global memory (LSU path; `vec`: 16-B aligned x).
+__device__ __forceinline__ double block_sum_global(const float* x, uint64_t b, uint64_t n, bool vec) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t e0 = b * kRedBlock;
+  const uint64_t ne = min(uint64_t(kRedBlock), n - e0);
+  const uint32_t nvt = uint32_t(ne >> 2), tail = uint32_t(ne & 3);
+  RedAcc a = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  const uint32_t* xu = reinterpret_cast<const uint32_t*>(x) + e0;
+  if (vec && nvt == kRedVecs) {
+    const uint4* x4 = reinterpret_cast<const uint4*>(xu);
+#pragma unroll
+    for (uint32_t k0 = 0; k0 < 32; k0 += 8) {
+      uint4 r[8];
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) r[u] = ld_cg4(x4 + lane + 32 * (k0 + u));
+#pragma unroll
+      for (uint32_t u = 0; u < 8; u += 2) {
+        acc4(a.e, r[u]);
+        acc4(a.o, r[u + 1]);
+      }
+    }
+  } else {
+    for (uint32_t k = 0; k < 32; ++k) {
+      const uint32_t v = lane + 32 * k;
+      if (v >= nvt) break;
+      uint4 r;
+      if (vec) {
+        r = ld_cg4(reinterpret_cast<const uint4*>(xu) + v);
+      } else {
+        r = make_uint4(ld_cg1(xu + 4 * v), ld_cg1(xu + 4 * v + 1), ld_cg1(xu + 4 * v + 2), ld_cg1(xu + 4 * v + 3));
+      }
+      acc_k(a, k, r);
+    }
+  }
+  if (tail && lane == (nvt & 31)) acc_tail(a, nvt, x, e0 + 4ull * nvt, tail);
+  return block_fold(a);
 }
 
 __device__ __forceinline__ void st_f64(double* p, double v) {
@@ -486,42 +543,6 @@ __device__ __forceinline__ double ld_cg_f64(const double* p) {
   double v;
   asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
-}
-
-// One block straight from global memory by one warp (LSU path; `vec`: x is
-// 16-B aligned).  Same sub-block sums and tree as the ring path.
-__device__ __forceinline__ double block_sum_global(const float* x, uint64_t b, uint64_t n, bool vec) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t e0 = b * kRedBlock;
-  const uint64_t ne = min(uint64_t(kRedBlock), n - e0);
-  const uint32_t nvt = uint32_t(ne >> 2), tail = uint32_t(ne & 3);
-  const uint32_t* xu = reinterpret_cast<const uint32_t*>(x) + e0;
-  auto load = [&](uint32_t v, uint32_t m) -> float4 {
-    if (m == 4 && vec) return as_f4(ld_cg4(reinterpret_cast<const uint4*>(xu) + v));
-    float e[4] = {0.f, 0.f, 0.f, 0.f};
-    for (uint32_t c = 0; c < m; ++c) e[c] = __uint_as_float(ld_cg1(xu + 4 * v + c));
-    return make_float4(e[0], e[1], e[2], e[3]);
-  };
-  // four sub-blocks at a time (8 loads in flight per lane), folded as they
-  // come: quad k = ((s0 + s1) + (s2 + s3)) of sub-blocks 4k..4k+3, and the
-  // block = (quad0 + quad1) + (quad2 + quad3) -- the same tree as tree16
-  double quad[4];
-#pragma unroll
-  for (uint32_t k = 0; k < 4; ++k) {
-    double l[4];
-#pragma unroll
-    for (uint32_t q = 0; q < 4; ++q) {
-      const uint32_t v1 = 64 * (4 * k + q) + lane, v2 = v1 + 32;
-      const uint32_t m1 = vec_elems(v1, nvt, tail), m2 = vec_elems(v2, nvt, tail);
-      const float4 u = m1 ? load(v1, m1) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 w = m2 ? load(v2, m2) : make_float4(0.f, 0.f, 0.f, 0.f);
-      l[q] = sub_lane(u, m1, w, m2);
-    }
-#pragma unroll
-    for (uint32_t q = 0; q < 4; ++q) l[q] = butterfly32(l[q]);
-    quad[k] = (l[0] + l[1]) + (l[2] + l[3]);
-  }
-  return (quad[0] + quad[1]) + (quad[2] + quad[3]);
 }
 
 // Arrival count and, in the last worker to arrive, the combine of every
@@ -589,20 +610,18 @@ __device__ __forceinline__ void reduce_finish(const lk_desc& d, uint32_t count, 
   }
 }
 
-// Dynamic blocks through the TMA ring (T >= 64).  Lane 0 of warp 0 produces:
-// a static share of blocks by rank first, then pool claims of `claim_n`
-// blocks, the next claim in flight while the current one's copies are issued.
-// Consumer warp cw takes sub-blocks cw, cw + ncw, ... of every stage: reads
-// its two vectors per lane, releases the stage, then sums; the warp whose
-// sub-block completes the stage's count folds the 16 sums into out[block].
-// Sub-block sums live in shared memory by stage and position parity: a stage
-// is refilled only after every warp has passed it, so the next use of the
-// same parity cannot start before this one's fold is done.
+// Dynamic blocks through the owner-warp ring (needs stages + 1 warps).  Lane
+// 0 of warp 0 produces: a static share of blocks by rank first, then pool
+// claims of `claim_n` blocks, the next claim in flight while the current
+// one's copies are issued; then one end marker per stage.  Warp 1 + s owns
+// ring stage s: it alone waits on that stage's barriers (its own phase
+// sequence, count-1 release), reads the block, releases the stage, then folds
+// and stores the block sum.  Other warps sit on the closing barrier.
 __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint32_t count, uint32_t* ctr,
-                                           ReduceSmem& sm, uint32_t T, Ring& r, uint32_t& g, uint32_t share8,
+                                           ReduceSmem& sm, uint32_t T, Ring& r, uint32_t share8,
                                            uint32_t claim_n) {
+  const float* x = reinterpret_cast<const float*>(d.in0);
   const uint4* x4 = reinterpret_cast<const uint4*>(d.in0);
-  const uint32_t* xu = reinterpret_cast<const uint32_t*>(d.in0);
   double* part = reinterpret_cast<double*>(d.out);
   const uint64_t nv = d.n >> 2;                                   // full vectors, all blocks
   const uint32_t tail = uint32_t(d.n & 3);
@@ -612,20 +631,23 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
   const uint32_t fair = nb / count;
   const uint32_t share = nb >= 4 * count ? (share8 * fair) / 8 : fair;
   const uint32_t pool0 = share * count;
-  const uint32_t c0 = g, S = r.stages;
+  const uint32_t S = r.stages;
+  uint64_t* const fullr = r.full + kMaxStages;
+  uint64_t* const emptyr = r.empty + kMaxStages;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    uint32_t f = c0;
+    uint32_t f = *r.gred;
     auto fill = [&](uint32_t b) {                                  // b = block or kTileEnd
       const uint32_t st = f % S;
-      mbar_wait(r.empty + st, ((f / S) & 1u) ^ 1u);
+      mbar_wait(emptyr + st, ((f / S) & 1u) ^ 1u);
       r.tile[st] = b;
       if (b == kTileEnd) {
-        mbar_arrive(r.full + st);                                  // wake consumers, no bytes
+        mbar_arrive(fullr + st);                                   // wake the owner, no bytes
       } else {
         const uint64_t v0 = uint64_t(b) * kRedVecs;
         const uint32_t bytes = v0 < nv ? uint32_t(min(uint64_t(kRedVecs), nv - v0)) * 16u : 0u;
-        mbar_expect_tx(r.full + st, bytes);                        // 0 bytes: a tail-only block
-        if (bytes) bulk_g2s(r.buf + st * kStageBytes, x4 + v0, bytes, r.full + st);
+        mbar_expect_tx(fullr + st, bytes);                         // 0 bytes: a tail-only block
+        if (bytes) bulk_g2s(r.buf + st * kStageBytes, x4 + v0, bytes, fullr + st);
       }
       ++f;
     };
@@ -638,84 +660,31 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
       for (uint32_t k = 0; k < claim_n && b + k < nb; ++k) fill(b + k);
       claim = next;
     }
-    fill(kTileEnd);
-    *r.gshared = f;
-  } else if (threadIdx.x >= 32) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t cw = (threadIdx.x >> 5) - 1, ncw = (T >> 5) - 1;
-    for (uint32_t c = c0;; ++c) {
-      const uint32_t st = c % S, par = (c / S) & 1u;
-      mbar_wait(r.full + st, par);
+    for (uint32_t k = 0; k < S; ++k) fill(kTileEnd);               // every owner sees one end marker
+    *r.gred = f;                                                   // read by all after the closing barrier
+  } else if (warp >= 1 && warp <= S) {
+    const uint32_t st = warp - 1;
+    const uint32_t c0 = *r.gred;
+    uint32_t p = c0 + (st + S - c0 % S) % S;                       // this stage's first position
+    for (;; p += S) {
+      mbar_wait(fullr + st, (p / S) & 1u);
       const uint32_t b = r.tile[st];
       if (b == kTileEnd) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(r.empty + st);
+        if (lane == 0) mbar_arrive(emptyr + st);
         break;
       }
-      const uint8_t* stage = r.buf + st * kStageBytes;
       const uint64_t v0 = uint64_t(b) * kRedVecs;
       const uint32_t nvt = v0 < nv ? uint32_t(min(uint64_t(kRedVecs), nv - v0)) : 0u;
-      const uint32_t tl = b == nb - 1 ? tail : 0u;
-      // a lane's two vectors of sub-block si: from the stage, except the
-      // block's partial tail vector (not in the stage: read from global)
-      auto lane_part = [&](uint32_t si) -> double {
-        const uint32_t v1 = 64 * si + lane, v2 = v1 + 32;
-        const uint32_t a1 = vec_elems(v1, nvt, tl), a2 = vec_elems(v2, nvt, tl);
-        auto get = [&](uint32_t v, uint32_t m) -> float4 {
-          if (m == 4) return as_f4(lds4(stage + 16 * v));
-          float e[4] = {0.f, 0.f, 0.f, 0.f};
-          for (uint32_t q = 0; q < m; ++q) e[q] = __uint_as_float(ld_cg1(xu + 4 * (v0 + v) + q));
-          return make_float4(e[0], e[1], e[2], e[3]);
-        };
-        return sub_lane(get(v1, a1), a1, get(v2, a2), a2);
-      };
-      // this warp's sub-blocks cw, cw + ncw, ...: two at a time; the stage is
-      // released right after the warp's last shared-memory read, before the
-      // butterflies
-      uint32_t si = cw, done = 0;
-      bool released = false;
-      for (;;) {
-        uint32_t id0 = kRedSubs, id1 = kRedSubs;
-        double l0 = 0.0, l1 = 0.0;
-        if (si < kRedSubs) { id0 = si; l0 = lane_part(si); si += ncw; }
-        if (si < kRedSubs) { id1 = si; l1 = lane_part(si); si += ncw; }
-        if (si >= kRedSubs && !released) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(r.empty + st);
-          released = true;
-        }
-        if (id0 < kRedSubs) {
-          const double sv = butterfly32(l0);
-          if (lane == 0) sm.sub[par][st][id0] = sv;
-          ++done;
-        }
-        if (id1 < kRedSubs) {
-          const double sv = butterfly32(l1);
-          if (lane == 0) sm.sub[par][st][id1] = sv;
-          ++done;
-        }
-        if (si >= kRedSubs) break;
-      }
-      uint32_t prev = 0;
-      if (lane == 0) {
-        __threadfence_block();                    // this warp's sums before its count
-        prev = atomicAdd(&sm.cnt[par][st], done);
-      }
-      prev = __shfl_sync(0xffffffffu, prev, 0);
-      if (prev + done == kRedSubs && lane == 0) { // this warp completed the block: fold it
-        __threadfence_block();
-        const volatile double* sv = sm.sub[par][st];
-        double v[kRedSubs];
-#pragma unroll
-        for (uint32_t k = 0; k < kRedSubs; ++k) v[k] = sv[k];
-        st_f64(part + b, tree16(v));
-        sm.cnt[par][st] = 0;
-      }
+      RedAcc acc = block_acc_smem(r.buf + st * kStageBytes, nvt);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(emptyr + st);                      // stage read: release it first
+      if (b == nb - 1 && tail && lane == (nvt & 31)) acc_tail(acc, nvt, x, nv << 2, tail);
+      const double ps = block_fold(acc);
+      if (lane == 0) st_f64(part + b, ps);
     }
   }
-  wsync(T);                                                        // gshared visible; stream done
-  g = *r.gshared;
-  reduce_finish(d, count, ctr, sm, T);
+  reduce_finish(d, count, ctr, sm, T);                             // (its first barrier publishes *r.gred)
 }
 
 // Static blocks, 128-bit (or scalar) loads straight from global memory: the
@@ -768,7 +737,7 @@ __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
 // every field access on the per-tile path into an LDL.
 __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
                                           uint32_t* ctr, ReduceSmem& rs, uint32_t T, Ring& ring, bool ring_on,
-                                          uint32_t& g, bool dyn = false, uint32_t red_share8 = 6,
+                                          uint32_t& g, bool dyn = false, uint32_t red_share8 = 2,
                                           uint32_t red_claim = kRedClaim) {
   const Part p = partition(d.n, rank, count);
   const bool tma = ring_on && !(d.flags & LK_DF_SCALAR);
@@ -802,7 +771,8 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
       break;
     }
     case LK_KIND_BLOCK_REDUCE_F32:
-      if (tma && T >= 64 && ring.tile != nullptr) reduce_dyn(d, rank, count, ctr, rs, T, ring, g, red_share8, red_claim);
+      if (tma && T >= 32 * (ring.stages + 1) && ring.gred != nullptr)
+        reduce_dyn(d, rank, count, ctr, rs, T, ring, red_share8, red_claim);
       else reduce_static(d, rank, count, ctr, rs, T);
       break;
     default: break;
@@ -1390,8 +1360,8 @@ struct PersistSmem {
   lk_desc desc;
   uint32_t cmd, rank, count, slot;
   ReduceSmem red;
-  uint64_t full[kMaxStages], empty[kMaxStages];
-  uint32_t tile[kMaxStages], ring_g;
+  uint64_t full[2 * kMaxStages], empty[2 * kMaxStages];
+  uint32_t tile[kMaxStages], ring_g, ring_gr;
   unsigned long long chan[2];      // HYBRID: latest direct-cell value, latest mailbox value
   lk_desc cdesc;                   // this worker's last fetched descriptor (LK_HINT_CACHED)
   unsigned long long cmask[4];     // ... and its slot's trigger mask
@@ -1406,7 +1376,6 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     sm.chan[0] = 0ull;              // {NOP, count 0}: nothing new on either channel
     sm.chan[1] = 0ull;
     sm.stop = 0;
-    reduce_smem_init(sm.red);
   }
   __syncthreads();                  // the only CTA-wide barrier: before the roles split
   if (threadIdx.x >= T) {           // three extra warps: host-cell poller, mailbox poller, gateway
@@ -1423,7 +1392,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     return;
   }
   extern __shared__ __align__(128) uint8_t dyn_smem[];
-  Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages, sm.tile, &sm.ring_g};
+  Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages, sm.tile, &sm.ring_g, &sm.ring_gr};
   const bool ring_ok = a.use_tma != 0;
   uint32_t g = 0;
   if (ring_ok) ring_init(ring, T);
@@ -1569,8 +1538,8 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
 // ---------------------------------------------------------------- baseline
 __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, uint32_t* ctr, int use_tma) {
   __shared__ ReduceSmem rs;
-  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
-  __shared__ uint32_t tile[kMaxStages], gsh;
+  __shared__ uint64_t full[2 * kMaxStages], empty[2 * kMaxStages];
+  __shared__ uint32_t tile[kMaxStages], gsh, gred;
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   if (single_thread_kind(d.kind)) {
     // the result goes to global memory (the counter line's spare word), which
@@ -1578,10 +1547,8 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
     if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) ctr[3] = busy_loop(d.iterations);
     return;
   }
-  Ring ring{dyn_smem, full, empty, kDefaultStages, tile, &gsh};
+  Ring ring{dyn_smem, full, empty, kDefaultStages, tile, &gsh, &gred};
   uint32_t g = 0;
-  if (threadIdx.x == 0) reduce_smem_init(rs);
-  __syncthreads();
   if (use_tma) ring_init(ring, blockDim.x);
   run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, ring, use_tma != 0, g);
 }

@@ -271,26 +271,22 @@ def _reduce_scalar(x):
     nb = -(-n // 4096)
     parts = []
     for b in range(nb):
-        subs = []
-        for sb in range(16):
-            lanes = []
-            for lane in range(32):
-                a = [np.float32(0.0)] * 4
-                for h in range(2):                      # vector 64s + l, then 64s + 32 + l
-                    v = 64 * sb + 32 * h + lane
-                    for c in range(4):
-                        e = b * 4096 + 4 * v + c
-                        if e < n:
-                            a[c] = np.float32(a[c] + x[e])   # fp32, round to nearest
-                lanes.append((float(a[0]) + float(a[1])) + (float(a[2]) + float(a[3])))
-            o = 16
-            while o >= 1:
-                lanes = [lanes[i] + lanes[i ^ o] for i in range(32)]
-                o //= 2
-            subs.append(lanes[0])
-        while len(subs) > 1:
-            subs = [subs[i] + subs[i + 1] for i in range(0, len(subs), 2)]
-        parts.append(subs[0])
+        lanes = []
+        for lane in range(32):
+            h = [[np.float32(0.0)] * 4, [np.float32(0.0)] * 4]   # even-k and odd-k accumulators
+            for k in range(32):
+                v = lane + 32 * k
+                for c in range(4):
+                    e = b * 4096 + 4 * v + c
+                    if e < n:
+                        h[k & 1][c] = np.float32(h[k & 1][c] + x[e])   # fp32, round to nearest
+            a = [float(np.float32(h[0][c] + h[1][c])) for c in range(4)]
+            lanes.append((a[0] + a[1]) + (a[2] + a[3]))
+        o = 16
+        while o >= 1:
+            lanes = [lanes[i] + lanes[i ^ o] for i in range(32)]
+            o //= 2
+        parts.append(lanes[0])
     s = [0.0] * 512
     for i, p in enumerate(parts):
         s[i % 512] = s[i % 512] + p
