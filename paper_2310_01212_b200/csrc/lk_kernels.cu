@@ -165,6 +165,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Generic-proxy writes (earlier dispatches' st.global outputs, ordered before
+// this thread by the CTA barriers) made visible to the async proxy before this
+// dispatch's cp.async.bulk reads: an in-place saxpy re-reads its own y.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ uint4 lds4(const uint8_t* p) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -741,6 +747,7 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
                                           uint32_t red_claim = kRedClaim) {
   const Part p = partition(d.n, rank, count);
   const bool tma = ring_on && !(d.flags & LK_DF_SCALAR);
+  if (tma && threadIdx.x == 0) fence_proxy_async();   // the producer issues every bulk copy
   dyn = dyn && tma && T >= 64 && ring.tile != nullptr;
   if (dyn) {   // the pool's atomics cost ~1 us: only worth it with >= 8 tiles per worker
     const uint64_t tile_v = (d.kind == LK_KIND_HBM_STREAM) ? kStageBytes / 16 : kStageBytes / 32;

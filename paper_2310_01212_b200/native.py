@@ -42,12 +42,13 @@ POLL_MODES = {"direct": _lib.POLL_DIRECT, "gateway": _lib.POLL_GATEWAY, "hybrid"
 class NativeConfig:
     """Session configuration (reference fields first, native.py:44-60).
 
+    ``num_workers`` defaults to 4 like the reference's (native.py:46);
     ``num_workers=None`` means one worker per SM (148 on B200).  The spin
     settings govern the *host* spin in lk_wait; device workers always spin in
     hardware, optionally backing off with ``poll_backoff_ns`` of __nanosleep.
     """
 
-    num_workers: Optional[int] = None
+    num_workers: Optional[int] = 4
     pin_to_cores: bool = False
     spin_strategy: str = SPIN_THEN_YIELD
     spin_yield_threshold: int = 10_000
@@ -269,7 +270,7 @@ class NativeSession:
 
     @classmethod
     def start(cls, cfg: Optional[NativeConfig] = None) -> tuple["NativeSession", PhaseTiming]:
-        cfg = cfg or NativeConfig()
+        cfg = cfg or NativeConfig()   # the reference's default: 4 workers
         lib = _lib.load()
         _warn_lazy_loading()
         t0 = time.perf_counter_ns()
@@ -731,7 +732,7 @@ def profile_run(cfg: Optional[NativeConfig] = None, rounds: int = 20000, works=(
     under ncu (--replay-mode application).  No `works`: round-robin empty
     tasks; else full-mask dispatches of works[r % len(works)] (payload
     WorkDescriptors).  Returns the rounds' host wall time in ns."""
-    cfg = cfg or NativeConfig()
+    cfg = cfg or NativeConfig(num_workers=None)
     ds = [as_work(w).to_c() for w in works]
     arr = (_lib.lk_desc * max(1, len(ds)))(*ds)
     ns = C.c_uint64()

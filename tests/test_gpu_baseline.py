@@ -68,7 +68,7 @@ def test_baseline_runs_beside_a_partitioned_session():
     baseline launches (and synchronizes) while the persistent kernel is
     resident, both produce the oracle's results, and the session keeps
     answering in between."""
-    session, _ = native.NativeSession.start(native.NativeConfig(sm_partition=16, record_trace=True))
+    session, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, sm_partition=16, record_trace=True))
     try:
         b = native.LaunchSyncBaseline(beside=session)
         assert b.grid == session.partition_info[1]

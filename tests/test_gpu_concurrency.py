@@ -25,7 +25,7 @@ def test_concurrent_host_threads_on_disjoint_workers(mode):
     still validates."""
     import threading
     from oracle import protocol as O
-    s, _ = native.NativeSession.start(native.NativeConfig(poll_mode=mode, record_trace=True,
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode=mode, record_trace=True,
                                                           trace_capacity=4096))
     try:
         n = s.num_workers

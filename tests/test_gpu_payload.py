@@ -36,7 +36,7 @@ def session(request):
     except Exception:
         pass
     path, mode = request.param.split("-")
-    s, _ = native.NativeSession.start(native.NativeConfig(spin_yield_threshold=200, poll_mode=mode,
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_yield_threshold=200, poll_mode=mode,
                                                           tma_payload=path != "lsu",
                                                           tma_min_workers=1 if path in ("ring", "dyn") else 49,
                                                           dynamic_tiles=path == "dyn"))

@@ -18,7 +18,7 @@ for d in (150, 300, 600):
 res = {k: [] for k in variants}
 for trial in range(3):
     for name, kw in variants.items():
-        s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, **kw))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, **kw))
         n = s.num_workers
         s.register(WorkDescriptor(slot=0, kind="empty"))
         masks = [1 << i for i in range(n)]

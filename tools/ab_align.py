@@ -16,7 +16,7 @@ native.pin_host_thread(0)
 res = {}
 for trial in range(3):
     for name, kw in (("free", {}), ("align", dict(align_polls=True))):
-        s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, **kw))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, **kw))
         n = s.num_workers
         w = WorkDescriptor(slot=0, kind="empty")
         s.register(w)

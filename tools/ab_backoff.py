@@ -14,7 +14,7 @@ vals = [int(x) for x in sys.argv[1:]] or [0, 50, 100, 200, 400]
 res = {}
 for trial in range(3):
     for b in vals:
-        s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, poll_backoff_ns=b))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, poll_backoff_ns=b))
         n = s.num_workers
         s.register(WorkDescriptor(slot=0, kind="empty"))
         masks = [1 << i for i in range(n)]

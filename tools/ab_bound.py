@@ -13,7 +13,7 @@ from paper_2310_01212_b200.device import WorkDescriptor  # noqa: E402
 
 native.pin_host_thread(0)
 os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[-1]})
-s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN))
 n = s.num_workers
 w = WorkDescriptor(slot=0, kind="empty")
 rr = [1 << i for i in range(n)]

@@ -9,7 +9,7 @@ from paper_2310_01212_b200 import native  # noqa: E402
 from paper_2310_01212_b200.device import WorkDescriptor  # noqa: E402
 
 native.pin_host_thread(0)
-s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN))
 n = s.num_workers
 masks = [1 << i for i in range(n)]
 for trial in range(3):

@@ -13,7 +13,7 @@ res = {}
 for trial in range(3):
     for k in (1, 2, 4):
         for sp in ((300,) if k == 1 else (150, 300)):
-            s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, poll_mode="gateway",
+            s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, poll_mode="gateway",
                                                                   poll_replicas=k, poll_spacing_ns=sp))
             n = s.num_workers
             s.register(WorkDescriptor(slot=0, kind="empty"))

@@ -16,7 +16,7 @@ idles = [int(x) for x in sys.argv[1:]] or [0, 300, 600]
 res = {}
 for trial in range(3):
     for idle in idles:
-        s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, idle_delay_ns=idle))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, idle_delay_ns=idle))
         n = s.num_workers
         w = WorkDescriptor(slot=0, kind="empty")
         s.register(w)

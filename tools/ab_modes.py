@@ -15,7 +15,7 @@ modes = sys.argv[1:] or ["direct", "hybrid"]
 res = {m: [] for m in modes}
 for trial in range(4):
     for m in modes:
-        s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, poll_mode=m))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, poll_mode=m))
         s.register(WorkDescriptor(slot=0, kind="empty"))
         rr = [1 << i for i in range(s.num_workers)]
         s.bench_roundtrip(rr, 0, 5000)

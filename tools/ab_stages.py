@@ -12,7 +12,7 @@ stages = [int(x) for x in sys.argv[1:]] or [6, 8, 12]
 res = {k: {} for k in stages}
 for trial in range(3):
     for st in stages:
-        s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", ring_stages=st))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", ring_stages=st))
         for kind in ("saxpy_f32", "block_reduce_f32"):
             r = bench.measure_payload(s, kind, [64], 20, 4 * bench.L2_BYTES)
             res[st].setdefault(kind, []).append(r["64MiB"]["gbs_device"])

@@ -13,7 +13,7 @@ res = {}
 for trial in range(3):
     for mode in ("direct", "gateway"):
         for stride in (128, 64, 16):
-            s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, poll_mode=mode,
+            s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, poll_mode=mode,
                                                                   status_stride=stride))
             n = s.num_workers
             s.register(WorkDescriptor(slot=0, kind="empty"))

@@ -12,7 +12,7 @@ native.pin_host_thread(0)
 res = {True: {}, False: {}}
 for trial in range(3):
     for dyn in (True, False):
-        s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", dynamic_tiles=dyn))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", dynamic_tiles=dyn))
         r = bench.measure_payload(s, "saxpy_f32", [16, 64], 20, 4 * bench.L2_BYTES)
         s.dispose()
         s.close()

@@ -15,7 +15,7 @@ native.pin_host_thread(0)
 
 
 def run(label, rounds=14800, **kw):
-    s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, timeline=True, **kw))
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, timeline=True, **kw))
     n = s.num_workers
     s.register(WorkDescriptor(slot=0, kind="empty"))
     masks = [1 << i for i in range(n)]

@@ -8,7 +8,7 @@ from paper_2310_01212_b200 import native  # noqa: E402
 
 native.pin_host_thread(0)
 for mode in sys.argv[1:] or ["direct", "hybrid", "gateway"]:
-    s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, poll_mode=mode))
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, poll_mode=mode))
     r = bench.measure_interference(s, 16, 50000, 512)
     s.dispose()
     s.close()

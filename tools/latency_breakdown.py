@@ -16,7 +16,7 @@ native.pin_host_thread(0)
 
 
 def breakdown(label, rounds=20000, timeline=True, **kw):
-    s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, timeline=timeline, **kw))
+    s, _ = native.NativeSession.start(native.NativeConfig(**{"num_workers": None, **kw}, spin_strategy=native.PURE_SPIN, timeline=timeline))
     n = s.num_workers
     s.register(WorkDescriptor(slot=0, kind="empty"))
     masks = [1 << i for i in range(n)]

@@ -21,7 +21,7 @@ kind = sys.argv[2] if len(sys.argv) > 2 else ""
 payload = kind in ("saxpy", "reduce")
 native.pin_host_thread(0)
 if not payload:
-    ns = native.profile_run(native.NativeConfig(), rounds)
+    ns = native.profile_run(native.NativeConfig(num_workers=None), rounds)
     print(f"profile run: {rounds} round-robin empty tasks in {ns / 1e6:.1f} ms = "
           f"{rounds / (ns / 1e9) / 1e3:.1f}k tasks/s", flush=True)
 else:
@@ -37,7 +37,7 @@ else:
             bufs += [x, part, tot]
             works.append(WorkDescriptor(slot=1 + k, kind="block_reduce_f32", data_in_ref=x, data_out_ref=part,
                                         total_ref=tot))
-    ns = native.profile_run(native.NativeConfig(), rounds, works)
+    ns = native.profile_run(native.NativeConfig(num_workers=None), rounds, works)
     alg = (12 if kind == "saxpy" else 4) * n
     print(f"profile run: {rounds} full-mask {works[0].kind} dispatches (64 MiB/vector) in {ns / 1e6:.2f} ms = "
           f"{rounds * alg / ns:.1f} GB/s including handshakes; algorithmic bytes/dispatch {alg}", flush=True)

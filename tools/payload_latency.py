@@ -11,7 +11,7 @@ from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E
 
 native.pin_host_thread(0)
 mode = sys.argv[1] if len(sys.argv) > 1 else "direct"
-s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN, poll_mode=mode))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, poll_mode=mode))
 print("poll mode", mode)
 n = s.num_workers
 full = host.full_mask(n)

@@ -9,7 +9,7 @@ from paper_2310_01212_b200 import native  # noqa: E402
 native.pin_host_thread(0)
 stages = [int(x) for x in sys.argv[1:]] or [6, 12]
 for st in stages:
-    s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", ring_stages=st))
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", ring_stages=st))
     for kind in ("saxpy_f32", "block_reduce_f32", "hbm_stream"):
         if kind == "hbm_stream":
             continue

@@ -11,7 +11,7 @@ from paper_2310_01212_b200 import _lib, native  # noqa: E402
 from paper_2310_01212_b200.device import WorkDescriptor  # noqa: E402
 
 native.pin_host_thread(0)
-s, _ = native.NativeSession.start(native.NativeConfig())
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None))
 n = s.num_workers
 w = WorkDescriptor(slot=0, kind="empty")
 s.register(w, 1)

@@ -10,7 +10,7 @@ from paper_2310_01212_b200 import host, native, protocol  # noqa: E402
 from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E402
 
 out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/gpu_trace.txt"
-s, _ = native.NativeSession.start(native.NativeConfig(record_trace=True, trace_capacity=512))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, record_trace=True, trace_capacity=512))
 n = s.num_workers
 x = DeviceBuffer.from_array(np.arange(1 << 16, dtype=np.float32))
 y = DeviceBuffer(4 << 16)

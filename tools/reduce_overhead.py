@@ -9,7 +9,7 @@ from paper_2310_01212_b200 import host, native  # noqa: E402
 from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks  # noqa: E402
 
 native.pin_host_thread(0)
-s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway"))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway"))
 n = s.num_workers
 full = host.full_mask(n)
 for mib in (4, 16, 64):

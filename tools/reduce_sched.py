@@ -20,7 +20,7 @@ res = {}
 for trial in range(2):
     for sh, cl, stg in combos:
         os.environ["LK_RED_SHARE8"], os.environ["LK_RED_CLAIM"] = str(sh), str(cl)
-        s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", ring_stages=stg))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", ring_stages=stg))
         r = bench.measure_payload(s, "block_reduce_f32", sizes, 12, 4 * bench.L2_BYTES)
         for mib in sizes:
             res.setdefault((sh, cl, stg, mib), []).append(r[f"{mib}MiB"]["gbs_device"])

@@ -17,7 +17,7 @@ sizes = [16, 64, 256, 1024]
 res = {}
 for trial in range(2):
     for st in stages:
-        s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", ring_stages=st))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", ring_stages=st))
         r = bench.measure_payload(s, "block_reduce_f32", sizes, 12, 4 * bench.L2_BYTES)
         for mib in sizes:
             res.setdefault((st, mib), []).append(r[f"{mib}MiB"]["gbs_device"])

@@ -13,7 +13,7 @@ from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E
 
 native.pin_host_thread(0)
 for st, tma in ((6, True), (12, True), (6, False)):
-    s, _ = native.NativeSession.start(native.NativeConfig(ring_stages=st, tma_payload=tma, tma_min_workers=1))
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, ring_stages=st, tma_payload=tma, tma_min_workers=1))
     out = []
     for n in (65536, 1 << 20):
         a, b, o = DeviceBuffer(4 * n), DeviceBuffer(4 * n), DeviceBuffer(4 * n)

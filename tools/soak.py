@@ -14,7 +14,7 @@ from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E
 
 minutes = float(sys.argv[1]) if len(sys.argv) > 1 else 5.0
 native.pin_host_thread(0)
-s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN))
 n = s.num_workers
 empty = WorkDescriptor(slot=0, kind="empty")
 s.register(empty)

@@ -10,7 +10,7 @@ from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor  # noqa: E
 
 native.pin_host_thread(0)
 mode = sys.argv[1] if len(sys.argv) > 1 else "gateway"
-s, _ = native.NativeSession.start(native.NativeConfig(poll_mode=mode))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode=mode))
 n = s.num_workers
 full = host.full_mask(n)
 el = (64 << 20) // 4

@@ -18,7 +18,7 @@ def pct(a, q):
 
 
 def run(label, rounds=20000, mode="rr", **kw):
-    cfg = native.NativeConfig(spin_strategy=native.PURE_SPIN, **kw)
+    cfg = native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN, **kw)
     s, _ = native.NativeSession.start(cfg)
     n = s.num_workers
     s.register(WorkDescriptor(slot=0, kind="empty"))

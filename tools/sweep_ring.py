@@ -8,7 +8,7 @@ from paper_2310_01212_b200 import native  # noqa: E402
 
 native.pin_host_thread(0)
 for tma, stages in ((False, 12), (True, 4), (True, 6), (True, 8), (True, 12)):
-    s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", tma_payload=tma, ring_stages=stages))
+    s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", tma_payload=tma, ring_stages=stages))
     out = {}
     for kind in ("saxpy_f32", "block_reduce_f32"):
         r = bench.measure_payload(s, kind, [4, 64], 20, 4 * bench.L2_BYTES)

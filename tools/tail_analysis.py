@@ -16,7 +16,7 @@ os.sched_setaffinity(0, {cores[-1]})
 if "fifo" in sys.argv:
     os.sched_setscheduler(0, os.SCHED_FIFO, os.sched_param(50))
     print("SCHED_FIFO 50")
-s, _ = native.NativeSession.start(native.NativeConfig(spin_strategy=native.PURE_SPIN))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN))
 n = s.num_workers
 s.register(WorkDescriptor(slot=0, kind="empty"))
 masks = [1 << i for i in range(n)]

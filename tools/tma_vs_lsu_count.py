@@ -15,7 +15,7 @@ counts = [1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 148]
 res = {}
 for trial in range(2):
     for tma in (True, False):
-        s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", tma_payload=tma, tma_min_workers=1))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", tma_payload=tma, tma_min_workers=1))
         for c in counts:
             n = c * (1 << 18)
             mask = host.mask_of(range(c))

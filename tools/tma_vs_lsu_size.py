@@ -10,7 +10,7 @@ native.pin_host_thread(0)
 res = {}
 for trial in range(2):
     for path in ("ring", "lsu"):
-        s, _ = native.NativeSession.start(native.NativeConfig(poll_mode="gateway", tma_payload=path == "ring"))
+        s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, poll_mode="gateway", tma_payload=path == "ring"))
         for kind in ("saxpy_f32", "block_reduce_f32"):
             r = bench.measure_payload(s, kind, [16, 64, 256, 1024], 8, 4 * bench.L2_BYTES)
             for k, v in r.items():
