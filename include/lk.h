@@ -74,9 +74,17 @@ extern "C" {
 #define LK_HINT_EMPTY  1u   /* the slot holds no work (EMPTY, or busy_loop of 0 iterations): no descriptor fetch */
 #define LK_HINT_CACHED 2u   /* every masked worker last fetched this slot at its current stage version:
                                reuse the cached descriptor (and trigger mask), no fetch */
+#define LK_HINT_SYSMEM 4u   /* the slot's payload touches host-mapped memory: the worker makes the poll
+                               that saw the value an acquire at system scope (fence.acq_rel.sys) */
 
 /* descriptor flags */
 #define LK_DF_SCALAR   1u   /* pointers not 16-B aligned: scalar path */
+#define LK_DF_HOSTMEM  2u   /* set by the runtime at staging (cudaPointerGetAttributes), never by the
+                               caller: a payload pointer is host-mapped pinned memory (lk_host_alloc,
+                               cudaHostAlloc).  The worker reads it with sys-scope LSU loads (no TMA,
+                               no stale L2 line) and publishes FINISHED with st.release.sys, so the
+                               outputs are in host memory before the host can see FINISHED.
+                               block_reduce_f32's partials (out) must be device memory. */
 
 /*
  * Work descriptor, 64 B POD, device-resident per slot.
@@ -172,6 +180,9 @@ typedef struct lk_config {
                                     acquire poll), so register/trigger/wait make no CUDA call at all: a
                                     session stays usable while a profiler that serialises launches (ncu)
                                     holds the runtime inside the persistent kernel's launch */
+#define LK_CF_FULL_BOARD  1024u  /* DIRECT: every to_gpu write also re-stores every other worker's cell
+                                    unchanged, shipping the whole mailbox board (the paper's workaround
+                                    for deferred small transfers; measured, not needed) */
 #define LK_CF_LAZY_ACK      16u  /* lk_wait returns once the NOP ack is written; the next trigger or
                                     dispose touching that worker waits for its republished NOP */
 
@@ -379,6 +390,14 @@ int lk_sm_count(int device, int* n);
 /* device memory helpers (payload buffers when the caller has no allocator) */
 int lk_dev_alloc(int device, uint64_t bytes, uint64_t* ptr);
 int lk_dev_free(uint64_t ptr);
+/* Mapped pinned host memory (cudaHostAlloc Mapped|Portable) for zero-copy
+ * payloads: pass the returned address as an lk_desc pointer and the workers
+ * read/write it over the link (LK_DF_HOSTMEM).  Replaces the reference's
+ * Copyin/Copyout phases (P/host.py:212-224) for small transfers.  Allocate and
+ * free it outside a live session's hot loop: cudaHostAlloc/cudaFreeHost are
+ * driver calls of ~10-100 us. */
+int lk_host_alloc(int device, uint64_t bytes, void** host);
+int lk_host_free(void* host);
 int lk_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes);
 int lk_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes);
 const char* lk_strerror(int code);

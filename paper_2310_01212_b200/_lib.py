@@ -36,6 +36,7 @@ KIND_IDS = {
     "hbm_stream": 5,
 }
 DF_SCALAR = 1
+DF_HOSTMEM = 2
 CF_ACQUIRE_POLL = 1
 CF_FENCE_ALWAYS = 2
 CF_LSU_PAYLOAD = 4
@@ -46,6 +47,7 @@ CF_DYNAMIC_TILES = 64
 CF_NO_ACK_DELAY = 128
 CF_ACK_FIXED = 256
 CF_HOST_DESC = 512
+CF_FULL_BOARD = 1024
 FLOOR_SYNC = 0
 FLOOR_QUERY = 1
 FLOOR_GRAPH = 2
@@ -53,6 +55,7 @@ POLL_DIRECT = 0
 POLL_GATEWAY = 1
 POLL_HYBRID = 2
 HINT_EMPTY = 1
+HINT_SYSMEM = 4
 
 WERR_NAMES = {
     0: "none",
@@ -176,6 +179,8 @@ SIGNATURES = {
     "lk_sm_count": (I32, [I32, C.POINTER(C.c_int)]),
     "lk_dev_alloc": (I32, [I32, U64, PU64]),
     "lk_dev_free": (I32, [U64]),
+    "lk_host_alloc": (I32, [I32, U64, C.POINTER(P)]),
+    "lk_host_free": (I32, [P]),
     "lk_memcpy_h2d": (I32, [U64, P, U64]),
     "lk_memcpy_d2h": (I32, [P, U64, U64]),
     "lk_strerror": (C.c_char_p, [I32]),

@@ -269,7 +269,9 @@ struct lk_session {
   // NOP has not been seen yet; the next trigger/dispose touching them waits
   std::vector<uint64_t> ack_pending;                      // nwords, under mu
   std::vector<uint8_t> registered;                        // per slot
-  std::vector<lk_desc> reg_desc;                          // host copy per slot
+  std::vector<lk_desc> reg_desc;                          // host copy per slot (as staged)
+  std::vector<lk_desc> reg_in;                            // ... and as the caller passed it
+  std::vector<uint64_t> stage_mask;                       // scratch for stage_locked
   // descriptor caching (LK_HINT_CACHED): a slot's stage version goes up with
   // every upload; each worker's last fetched (slot, version)
   std::vector<uint32_t> slot_ver;                         // per slot
@@ -318,12 +320,35 @@ struct lk_session {
     unsigned long long* c = to_gpu + uint64_t(i) * dreps * cell_u64;
     for (uint32_t k = 0; k < dreps; ++k) __atomic_store_n(c + k * cell_u64, v, __ATOMIC_RELEASE);
   }
+  // LK_CF_FULL_BOARD (DIRECT): the paper's workaround for the driver that
+  // deferred single-word mailbox transfers indefinitely (
+  // P/link.py:104-122, workaround_full_board): every write ships the whole
+  // board.  Ascending over all workers, the targets get their new value and
+  // every other cell is stored again unchanged (same seq: the worker ignores
+  // it), so the link carries the full mailbox each time.
+  void full_board_write(const std::vector<uint32_t>& ids, uint32_t w, uint32_t hint) {
+    size_t j = 0;
+    for (uint32_t i = 0; i < nw; ++i) {
+      if (j < ids.size() && ids[j] == i) {
+        host_write(i, w, hint);
+        ++j;
+        continue;
+      }
+      unsigned long long* c = to_gpu + uint64_t(i) * dreps * cell_u64;
+      const unsigned long long v = __atomic_load_n(c, __ATOMIC_RELAXED);
+      for (uint32_t k = 0; k < dreps; ++k) __atomic_store_n(c + k * cell_u64, v, __ATOMIC_RELEASE);
+    }
+  }
   // One logical write of `w` to every worker in ids (ascending), i.e. the
   // reference's `for i in sm_ids: _host_write(i, word)` (native.py:224-225).
   // GATEWAY: a single ring event carries the word and the worker mask.
   // Returns false if the ring stayed full past the timeout.
   bool post(const std::vector<uint32_t>& ids, uint32_t w, uint32_t hint = 0) {
     if (!gateway || (hybrid && ids.size() <= LK_HYBRID_DIRECT_MAX)) {
+      if (cfg.flags & LK_CF_FULL_BOARD) {
+        full_board_write(ids, w, hint);
+        return true;
+      }
       for (uint32_t i : ids) host_write(i, w, hint);
       return true;
     }
@@ -538,16 +563,44 @@ void lk_session::release_claim() {
   }
 }
 static uint8_t g_claimed[kMaxDevices];
+static int g_live = 0;                        // claimed devices
+// cudaFreeHost synchronizes the device: with a persistent kernel resident it
+// would wait for that kernel to exit -- forever when the caller is the thread
+// that would dispose it (a garbage-collected session object of an earlier
+// test, a HostBuffer dropped mid-session).  Pinned frees are therefore
+// deferred while any session holds a device claim, and made once none does.
+static std::vector<void*> g_pinned_graveyard;  // under g_claim_mu
+
+static void free_pinned(void* p) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> g(g_claim_mu);
+    if (g_live > 0) {
+      g_pinned_graveyard.push_back(p);
+      return;
+    }
+  }
+  cudaFreeHost(p);
+}
 
 static bool claim_device(int dev) {
   std::lock_guard<std::mutex> g(g_claim_mu);
   if (dev < 0 || dev >= kMaxDevices || g_claimed[dev]) return false;
   g_claimed[dev] = 1;
+  ++g_live;
   return true;
 }
 static void release_device(int dev) {
-  std::lock_guard<std::mutex> g(g_claim_mu);
-  if (dev >= 0 && dev < kMaxDevices) g_claimed[dev] = 0;
+  std::vector<void*> drain;
+  {
+    std::lock_guard<std::mutex> g(g_claim_mu);
+    if (dev >= 0 && dev < kMaxDevices && g_claimed[dev]) {
+      g_claimed[dev] = 0;
+      --g_live;
+    }
+    if (g_live == 0) drain.swap(g_pinned_graveyard);
+  }
+  for (void* p : drain) cudaFreeHost(p);
 }
 
 // ------------------------------------------------------------------ profile runs
@@ -713,6 +766,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->scratch.assign(s->nwords, 0);
   s->ack_pending.assign(s->nwords, 0);
   s->reg_desc.resize(cfg.num_slots);
+  s->reg_in.resize(cfg.num_slots);
   s->slot_ver.assign(cfg.num_slots, 0);
   s->wslot.assign(s->nw, 0xFFFFFFFFu);
   s->wver.assign(s->nw, 0);
@@ -723,7 +777,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->t_create = t0;
 
   auto cleanup = [&](int rc) {
-    if (s->host_block) cudaFreeHost(s->host_block);
+    if (s->host_block) free_pinned(s->host_block);
     if (s->dev_block) dev_free(s->dev_block);
     if (s->stream) {
       CtxScope cs(s->part.ca);
@@ -1031,8 +1085,35 @@ static inline bool multi_worker_kind(uint32_t kind) {
 // device: payload pointers must be 4-B aligned (element size) and non-null,
 // pointers that are not 16-B aligned take the scalar path (cp.async.bulk and
 // ld.global.v4 would fault on them), and the reduce's total is a double.
-static int normalise_desc(const lk_desc* in, lk_desc* out) {
+// Every payload pointer is classified with cudaPointerGetAttributes: device
+// memory of the session's GPU, or host-mapped pinned memory (LK_DF_HOSTMEM:
+// sys-scope loads, sys-scope release before FINISHED).  Anything else -- an
+// unregistered host address, another GPU's memory -- would fault the resident
+// kernel and with it the context, so it is refused here.
+static int classify_ptr(uint64_t p, int device, const char* what, bool* host) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, reinterpret_cast<const void*>(p));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LK_E_USAGE, "%s pointer 0x%llx: %s", what, (unsigned long long)p, cudaGetErrorString(e));
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    if (at.device != device)
+      return fail(LK_E_USAGE, "%s pointer 0x%llx is memory of device %d, the session runs on device %d", what,
+                  (unsigned long long)p, at.device, device);
+    return LK_OK;
+  }
+  if (at.type == cudaMemoryTypeHost && at.devicePointer == reinterpret_cast<void*>(p)) {
+    *host = true;
+    return LK_OK;
+  }
+  return fail(LK_E_USAGE, "%s pointer 0x%llx is neither device memory nor mapped pinned host memory "
+              "(lk_host_alloc)", what, (unsigned long long)p);
+}
+
+static int normalise_desc(int device, const lk_desc* in, lk_desc* out) {
   *out = *in;
+  out->flags &= LK_DF_SCALAR;   // LK_DF_HOSTMEM is the runtime's to set
   if (!multi_worker_kind(in->kind)) return LK_OK;
   const bool two = in->kind == LK_KIND_VECTOR_ADD_I32 || in->kind == LK_KIND_SAXPY_F32;
   if (in->n && (!in->in0 || !in->out || (two && !in->in1)))
@@ -1041,19 +1122,34 @@ static int normalise_desc(const lk_desc* in, lk_desc* out) {
   if (any & 3) return fail(LK_E_USAGE, "payload pointers must be 4-byte aligned");
   if (in->aux & 7) return fail(LK_E_USAGE, "the reduce total pointer must be 8-byte aligned");
   if (any & 15) out->flags |= LK_DF_SCALAR;
+  if (in->n) {
+    bool host = false, out_host = false;
+    int rc = classify_ptr(in->in0, device, "input", &host);
+    if (!rc && two) rc = classify_ptr(in->in1, device, "second input", &host);
+    if (!rc) rc = classify_ptr(in->out, device, "output", &out_host);
+    if (!rc && in->kind == LK_KIND_BLOCK_REDUCE_F32 && in->aux) rc = classify_ptr(in->aux, device, "total", &host);
+    if (rc) return rc;
+    if (out_host && in->kind == LK_KIND_BLOCK_REDUCE_F32)
+      return fail(LK_E_USAGE, "block_reduce_f32 block partials (out) must be device memory; "
+                  "the total (aux) may be host-mapped");
+    if (host || out_host) out->flags |= LK_DF_HOSTMEM;
+  }
   return LK_OK;
 }
 
 static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* din, const uint64_t* mask, uint32_t nwords) {
+  std::vector<uint64_t>& m = s->stage_mask;
+  m.assign(s->nwords, 0);
+  if (mask && multi_worker_kind(din->kind))
+    for (uint32_t k = 0; k < nwords && k < s->nwords; ++k) m[k] = mask[k];
+  // the caller's descriptor as last staged: re-staging the same one is free
+  // (no pointer classification, no upload)
+  if (s->registered[slot] && memcmp(&s->reg_in[slot], din, sizeof(lk_desc)) == 0 && s->reg_mask[slot] == m)
+    return LK_OK;
   lk_desc dn;
-  int nrc = normalise_desc(din, &dn);
+  int nrc = normalise_desc(s->device, din, &dn);
   if (nrc) return nrc;
   const lk_desc* d = &dn;
-  std::vector<uint64_t> m(s->nwords, 0);
-  if (mask && multi_worker_kind(d->kind))
-    for (uint32_t k = 0; k < nwords && k < s->nwords; ++k) m[k] = mask[k];
-  if (s->registered[slot] && memcmp(&s->reg_desc[slot], d, sizeof(lk_desc)) == 0 && s->reg_mask[slot] == m)
-    return LK_OK;
   if (s->host_desc) {
     // plain stores into the mapped table; the WORK word that names the slot
     // is written later with release semantics, and the worker polls it with
@@ -1071,7 +1167,8 @@ static int stage_locked(lk_session* s, uint32_t slot, const lk_desc* din, const 
   s->registered[slot] = 1;
   ++s->slot_ver[slot];   // workers' cached copies of this slot are stale now
   s->reg_desc[slot] = *d;
-  s->reg_mask[slot] = std::move(m);
+  s->reg_in[slot] = *din;
+  s->reg_mask[slot] = m;
   return LK_OK;
 }
 
@@ -1129,7 +1226,7 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
     bool same = true;
     for (uint32_t k = 0; k < s->nwords; ++k) same &= rm[k] == (k < nwords ? mask[k] : 0ull);
     if (!same) {
-      const lk_desc cur = s->reg_desc[slot];
+      const lk_desc cur = s->reg_in[slot];
       rc = stage_locked(s, slot, &cur, mask, nwords);
       if (rc) return rc;
     }
@@ -1140,6 +1237,7 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   const lk_desc& rd = s->reg_desc[slot];
   const bool no_work = rd.kind == LK_KIND_EMPTY || (rd.kind == LK_KIND_BUSY_LOOP && rd.iterations == 0);
   uint32_t hint = no_work ? LK_HINT_EMPTY : 0u;
+  if (rd.flags & LK_DF_HOSTMEM) hint |= LK_HINT_SYSMEM;
   const uint32_t ver = s->slot_ver[slot];
   if (!no_work) {   // every masked worker fetched this slot version last: it may reuse its copy
     bool cached = true;
@@ -1355,7 +1453,7 @@ extern "C" int lk_destroy(lk_session* s) {
   }
   s->join_launcher();
   cudaSetDevice(s->device);
-  cudaFreeHost(s->host_block);
+  free_pinned(s->host_block);
   dev_free(s->dev_block);
   {
     CtxScope cs(s->part.ca);
@@ -1535,7 +1633,7 @@ extern "C" int lk_clock_offset(int device, uint32_t rounds, int64_t* offset_ns, 
   cudaError_t ce = lk_launch_clocksync(flag, const_cast<unsigned long long*>(echo), rounds, st);
   if (ce != cudaSuccess) {
     cudaStreamDestroy(st);
-    cudaFreeHost(cells);
+    free_pinned(cells);
     return fail(LK_E_CUDA, "clocksync launch: %s", cudaGetErrorString(ce));
   }
   uint64_t best = ~0ull;
@@ -1557,7 +1655,7 @@ extern "C" int lk_clock_offset(int device, uint32_t rounds, int64_t* offset_ns, 
   }
   LK_CUDA(cudaStreamSynchronize(st));
   cudaStreamDestroy(st);
-  cudaFreeHost(cells);
+  free_pinned(cells);
   *offset_ns = off;
   if (best_rtt_ns) *best_rtt_ns = best;
   return LK_OK;
@@ -1708,7 +1806,7 @@ extern "C" int lk_pingpong(int device, uint64_t rounds, uint64_t* rt_ns) {
   if (rc == LK_OK) {
     LK_CUDA(cudaStreamSynchronize(st));
     cudaStreamDestroy(st);
-    cudaFreeHost(cells);
+    free_pinned(cells);
   }
   return rc;
 }
@@ -1717,6 +1815,8 @@ extern "C" int lk_pingpong(int device, uint64_t rounds, uint64_t* rt_ns) {
 struct lk_baseline {
   CUcontext ctx = nullptr;   // green context B of a partitioned session, else the primary
   int device;
+  lk_desc last_in{}, last_norm{};   // the caller's last descriptor and its normalised form
+  bool have_last = false;
   uint32_t threads;
   cudaStream_t stream;
   uint32_t* d_ctr;
@@ -1726,6 +1826,30 @@ struct lk_baseline {
 };
 
 static int baseline_create(int device, uint32_t threads, CUcontext ctx, lk_baseline** out);
+
+// The baseline's own device (the primary context's case; a green context
+// names its device itself) and the descriptor as the launch takes it:
+// normalised like a staged one (LK_DF_SCALAR / LK_DF_HOSTMEM, pointer checks),
+// cached so a loop re-launching one descriptor classifies its pointers once.
+struct BaseScope {
+  CtxScope cs;
+  explicit BaseScope(lk_baseline* b) : cs(b->ctx) {
+    if (!b->ctx) cudaSetDevice(b->device);
+  }
+};
+
+static int baseline_desc(lk_baseline* b, const lk_desc* d, const lk_desc** out) {
+  if (!b->have_last || memcmp(&b->last_in, d, sizeof(lk_desc)) != 0) {
+    lk_desc n;
+    int rc = normalise_desc(b->device, d, &n);
+    if (rc) return rc;
+    b->last_in = *d;
+    b->last_norm = n;
+    b->have_last = true;
+  }
+  *out = &b->last_norm;
+  return LK_OK;
+}
 
 extern "C" int lk_baseline_create(int device, uint32_t threads, lk_baseline** out) {
   return baseline_create(device, threads, nullptr, out);
@@ -1760,10 +1884,13 @@ static int baseline_create(int device, uint32_t threads, CUcontext ctx, lk_basel
   return LK_OK;
 }
 
-extern "C" int lk_baseline_launch(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t* launch_ns) {
-  if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
-  CtxScope cs(b->ctx);
+extern "C" int lk_baseline_launch(lk_baseline* b, const lk_desc* din, uint32_t grid, uint64_t* launch_ns) {
+  if (!b || !din || grid == 0) return fail(LK_E_USAGE, "bad argument");
+  BaseScope cs(b);
   if (b->in_flight) return fail(LK_E_USAGE, "previous task not yet joined");
+  const lk_desc* d = nullptr;
+  int rc = baseline_desc(b, din, &d);
+  if (rc) return rc;
   const uint64_t t0 = now_ns();
   cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
   const uint64_t t1 = now_ns();
@@ -1775,7 +1902,7 @@ extern "C" int lk_baseline_launch(lk_baseline* b, const lk_desc* d, uint32_t gri
 
 extern "C" int lk_baseline_wait(lk_baseline* b, uint64_t* wait_ns) {
   if (!b) return fail(LK_E_USAGE, "null argument");
-  CtxScope cs(b->ctx);
+  BaseScope cs(b);
   if (!b->in_flight) return fail(LK_E_USAGE, "no task in flight");
   const uint64_t t0 = now_ns();
   LK_CUDA(cudaStreamSynchronize(b->stream));
@@ -1784,10 +1911,13 @@ extern "C" int lk_baseline_wait(lk_baseline* b, uint64_t* wait_ns) {
   return LK_OK;
 }
 
-extern "C" int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid, uint64_t rounds,
+extern "C" int lk_baseline_bench(lk_baseline* b, const lk_desc* din, uint32_t grid, uint64_t rounds,
                                  uint64_t* launch_ns, uint64_t* total_ns) {
-  if (!b || !d || grid == 0) return fail(LK_E_USAGE, "bad argument");
-  CtxScope cs(b->ctx);
+  if (!b || !din || grid == 0) return fail(LK_E_USAGE, "bad argument");
+  BaseScope cs(b);
+  const lk_desc* d = nullptr;
+  int rc = baseline_desc(b, din, &d);
+  if (rc) return rc;
   for (uint64_t k = 0; k < rounds; ++k) {
     const uint64_t t0 = now_ns();
     cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
@@ -1801,10 +1931,13 @@ extern "C" int lk_baseline_bench(lk_baseline* b, const lk_desc* d, uint32_t grid
   return LK_OK;
 }
 
-extern "C" int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* d, uint32_t grid, uint32_t reps,
+extern "C" int lk_baseline_time_kernel(lk_baseline* b, const lk_desc* din, uint32_t grid, uint32_t reps,
                                        float* avg_ms) {
-  if (!b || !d || !avg_ms || reps == 0) return fail(LK_E_USAGE, "bad argument");
-  CtxScope cs(b->ctx);
+  if (!b || !din || !avg_ms || reps == 0) return fail(LK_E_USAGE, "bad argument");
+  BaseScope cs(b);
+  const lk_desc* d = nullptr;
+  int rc = baseline_desc(b, din, &d);
+  if (rc) return rc;
   LK_CUDA(cudaEventRecord(b->e0, b->stream));
   for (uint32_t k = 0; k < reps; ++k) {
     cudaError_t ce = lk_launch_work(*d, grid, b->threads, b->d_ctr, b->stream, b->use_tma);
@@ -1884,7 +2017,7 @@ extern "C" int lk_baseline_set_tma(lk_baseline* b, int on) {
 extern "C" int lk_baseline_destroy(lk_baseline* b) {
   if (!b) return LK_OK;
   {
-    CtxScope cs(b->ctx);
+    BaseScope cs(b);
     cudaStreamSynchronize(b->stream);
     cudaStreamDestroy(b->stream);
     cudaEventDestroy(b->e0);
@@ -1941,6 +2074,16 @@ extern "C" int lk_sm_count(int device, int* n) {
   return LK_OK;
 }
 
+// The device whose memory `p` is (else the calling thread's device), made
+// current so the copy goes to that device's service stream.
+static void set_device_of(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+      (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged))
+    cudaSetDevice(at.device);
+  cudaGetLastError();
+}
+
 extern "C" int lk_dev_alloc(int device, uint64_t bytes, uint64_t* ptr) {
   if (!ptr) return fail(LK_E_USAGE, "null argument");
   LK_CUDA(cudaSetDevice(device));
@@ -1951,11 +2094,39 @@ extern "C" int lk_dev_alloc(int device, uint64_t bytes, uint64_t* ptr) {
 }
 
 extern "C" int lk_dev_free(uint64_t ptr) {
+  set_device_of(reinterpret_cast<const void*>(ptr));
   LK_CUDA(dev_free(reinterpret_cast<void*>(ptr)));
   return LK_OK;
 }
 
+// Mapped pinned host memory for zero-copy payloads (LK_DF_HOSTMEM): the
+// persistent kernel reads and writes it over the link with no cudaMemcpy.
+// Portable: every device's sessions may use it.  The device address equals
+// the host address (UVA), so it goes into lk_desc as is.
+extern "C" int lk_host_alloc(int device, uint64_t bytes, void** host) {
+  if (!host) return fail(LK_E_USAGE, "null argument");
+  LK_CUDA(cudaSetDevice(device));
+  void* p = nullptr;
+  LK_CUDA(cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocMapped | cudaHostAllocPortable));
+  void* d = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&d, p, 0);
+  if (e != cudaSuccess || d != p) {
+    free_pinned(p);
+    return fail(LK_E_CUDA, "host allocation has no identical device mapping (UVA)");
+  }
+  memset(p, 0, bytes);
+  *host = p;
+  return LK_OK;
+}
+
+extern "C" int lk_host_free(void* host) {
+  if (!host) return LK_OK;
+  free_pinned(host);
+  return LK_OK;
+}
+
 extern "C" int lk_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes) {
+  set_device_of(reinterpret_cast<const void*>(dst));
   cudaStream_t st = svc_stream();
   LK_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice, st));
   LK_CUDA(cudaStreamSynchronize(st));
@@ -1963,6 +2134,7 @@ extern "C" int lk_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes) {
 }
 
 extern "C" int lk_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes) {
+  set_device_of(reinterpret_cast<const void*>(src));
   cudaStream_t st = svc_stream();
   LK_CUDA(cudaMemcpyAsync(dst, reinterpret_cast<const void*>(src), bytes, cudaMemcpyDeviceToHost, st));
   LK_CUDA(cudaStreamSynchronize(st));

@@ -106,6 +106,18 @@ __device__ __forceinline__ unsigned long long ld_cg64(const unsigned long long* 
   asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+// Payload load policies.  Device buffers: ld.global.cg (L2, the coherence
+// point for every SM).  Host-mapped buffers (LK_DF_HOSTMEM): ld.relaxed.sys,
+// which may not be served from a line the GPU cached on an earlier dispatch
+// of the same buffer -- the host may have rewritten it since.
+struct LdCg {
+  static __device__ __forceinline__ uint4 v4(const uint4* p) { return ld_cg4(p); }
+  static __device__ __forceinline__ uint32_t s1(const uint32_t* p) { return ld_cg1(p); }
+};
+struct LdSys {
+  static __device__ __forceinline__ uint4 v4(const uint4* p) { return ld_sys4(p); }
+  static __device__ __forceinline__ uint32_t s1(const uint32_t* p) { return ld_relaxed_sys(p); }
+};
 __device__ __forceinline__ void st4(uint4* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w) : "memory");
@@ -261,15 +273,16 @@ __device__ __forceinline__ uint4 vop(const Op& op, uint4 x, uint4 y) {
   return make_uint4(op.s(x.x, y.x), op.s(x.y, y.y), op.s(x.z, y.z), op.s(x.w, y.w));
 }
 
-// out[i] = op(in0[i], in1[i]) over [p.b, p.e), all threads of the CTA.
-template <int U, bool kTwo, class Op>
+// out[i] = op(in0[i], in1[i]) over [p.b, p.e), all threads of the CTA (LSU path;
+// Ld = LdSys for host-mapped buffers).
+template <int U, bool kTwo, class Op, class Ld = LdCg>
 __device__ __forceinline__ void map_chunk(const lk_desc& d, Part p, const Op& op, uint32_t T) {
   const uint32_t t = threadIdx.x;
   const uint32_t* a = reinterpret_cast<const uint32_t*>(d.in0);
   const uint32_t* c = reinterpret_cast<const uint32_t*>(d.in1);
   uint32_t* o = reinterpret_cast<uint32_t*>(d.out);
   if (d.flags & LK_DF_SCALAR) {
-    for (uint64_t i = p.b + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
+    for (uint64_t i = p.b + t; i < p.e; i += T) o[i] = op.s(Ld::s1(a + i), kTwo ? Ld::s1(c + i) : 0u);
     return;
   }
   const uint4* a4 = reinterpret_cast<const uint4*>(a);
@@ -281,14 +294,14 @@ __device__ __forceinline__ void map_chunk(const lk_desc& d, Part p, const Op& op
     uint4 x[U], y[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      x[u] = ld_cg4(a4 + v + u * T);
-      if (kTwo) y[u] = ld_cg4(c4 + v + u * T);
+      x[u] = Ld::v4(a4 + v + u * T);
+      if (kTwo) y[u] = Ld::v4(c4 + v + u * T);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) st4(o4 + v + u * T, vop(op, x[u], kTwo ? y[u] : x[u]));
   }
-  for (; v < ve; v += T) st4(o4 + v, vop(op, ld_cg4(a4 + v), kTwo ? ld_cg4(c4 + v) : make_uint4(0, 0, 0, 0)));
-  for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
+  for (; v < ve; v += T) st4(o4 + v, vop(op, Ld::v4(a4 + v), kTwo ? Ld::v4(c4 + v) : make_uint4(0, 0, 0, 0)));
+  for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(Ld::s1(a + i), kTwo ? Ld::s1(c + i) : 0u);
 }
 
 // map_chunk through the TMA ring: tiles of kStageBytes/2 per input (2 inputs)
@@ -471,10 +484,11 @@ __device__ __forceinline__ void acc_k(RedAcc& a, uint32_t k, uint4 r) {
 
 // The trailing n % 4 elements belong to vector `nvt` of the last block: the
 // lane's last vector (k = nvt / 32), so they are added after its loop.
+template <class Ld = LdCg>
 __device__ __forceinline__ void acc_tail(RedAcc& a, uint32_t nvt, const float* x, uint64_t first, uint32_t tail) {
   float* h = ((nvt >> 5) & 1) ? a.o : a.e;
   for (uint32_t c = 0; c < tail; ++c)
-    h[c] = __fadd_rn(h[c], __uint_as_float(ld_cg1(reinterpret_cast<const uint32_t*>(x) + first + c)));
+    h[c] = __fadd_rn(h[c], __uint_as_float(Ld::s1(reinterpret_cast<const uint32_t*>(x) + first + c)));
 }
 
 __device__ __forceinline__ double block_fold(const RedAcc& a) {
@@ -505,6 +519,7 @@ __device__ __forceinline__ RedAcc block_acc_smem(const uint8_t* stage, uint32_t 
 }
 
 // One block straight from global memory (LSU path; `vec`: 16-B aligned x).
+template <class Ld = LdCg>
 __device__ __forceinline__ double block_sum_global(const float* x, uint64_t b, uint64_t n, bool vec) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t e0 = b * kRedBlock;
@@ -518,7 +533,7 @@ __device__ __forceinline__ double block_sum_global(const float* x, uint64_t b, u
     for (uint32_t k0 = 0; k0 < 32; k0 += 8) {
       uint4 r[8];
 #pragma unroll
-      for (uint32_t u = 0; u < 8; ++u) r[u] = ld_cg4(x4 + lane + 32 * (k0 + u));
+      for (uint32_t u = 0; u < 8; ++u) r[u] = Ld::v4(x4 + lane + 32 * (k0 + u));
 #pragma unroll
       for (uint32_t u = 0; u < 8; u += 2) {
         acc4(a.e, r[u]);
@@ -531,14 +546,14 @@ __device__ __forceinline__ double block_sum_global(const float* x, uint64_t b, u
       if (v >= nvt) break;
       uint4 r;
       if (vec) {
-        r = ld_cg4(reinterpret_cast<const uint4*>(xu) + v);
+        r = Ld::v4(reinterpret_cast<const uint4*>(xu) + v);
       } else {
-        r = make_uint4(ld_cg1(xu + 4 * v), ld_cg1(xu + 4 * v + 1), ld_cg1(xu + 4 * v + 2), ld_cg1(xu + 4 * v + 3));
+        r = make_uint4(Ld::s1(xu + 4 * v), Ld::s1(xu + 4 * v + 1), Ld::s1(xu + 4 * v + 2), Ld::s1(xu + 4 * v + 3));
       }
       acc_k(a, k, r);
     }
   }
-  if (tail && lane == (nvt & 31)) acc_tail(a, nvt, x, e0 + 4ull * nvt, tail);
+  if (tail && lane == (nvt & 31)) acc_tail<Ld>(a, nvt, x, e0 + 4ull * nvt, tail);
   return block_fold(a);
 }
 
@@ -696,6 +711,7 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
 // Static blocks, 128-bit (or scalar) loads straight from global memory: the
 // narrow-dispatch and misaligned path.  Worker rank r takes the r-th
 // contiguous run of blocks; its warps take the run's blocks round robin.
+template <class Ld = LdCg>
 __device__ __forceinline__ void reduce_static(const lk_desc& d, uint32_t rank, uint32_t count, uint32_t* ctr,
                                               ReduceSmem& sm, uint32_t T) {
   const float* x = reinterpret_cast<const float*>(d.in0);
@@ -706,7 +722,7 @@ __device__ __forceinline__ void reduce_static(const lk_desc& d, uint32_t rank, u
   const bool vec = !(d.flags & LK_DF_SCALAR);
   const uint32_t warp = threadIdx.x >> 5, nwarps = T >> 5;
   for (uint64_t b = b0 + warp; b < b1; b += nwarps) {
-    const double p = block_sum_global(x, b, d.n, vec);
+    const double p = block_sum_global<Ld>(x, b, d.n, vec);
     if ((threadIdx.x & 31) == 0) st_f64(part + b, p);
   }
   reduce_finish(d, count, ctr, sm, T);
@@ -746,7 +762,10 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
                                           uint32_t& g, bool dyn = false, uint32_t red_share8 = 2,
                                           uint32_t red_claim = kRedClaim) {
   const Part p = partition(d.n, rank, count);
-  const bool tma = ring_on && !(d.flags & LK_DF_SCALAR);
+  // host-mapped buffers go through the LSU with sys-scope loads: bulk copies
+  // would read them through L2 lines an earlier dispatch may have left behind
+  const bool host = (d.flags & LK_DF_HOSTMEM) != 0;
+  const bool tma = ring_on && !(d.flags & (LK_DF_SCALAR | LK_DF_HOSTMEM));
   if (tma && threadIdx.x == 0) fence_proxy_async();   // the producer issues every bulk copy
   dyn = dyn && tma && T >= 64 && ring.tile != nullptr;
   if (dyn) {   // the pool's atomics cost ~1 us: only worth it with >= 8 tiles per worker
@@ -757,11 +776,13 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
     case LK_KIND_VECTOR_ADD_I32:
       if (dyn) map_tma_dyn<true>(d, rank, count, OpAddI32{}, T, ring, g, ctr + 1);
       else if (tma) map_tma<true>(d, p, OpAddI32{}, T, ring, g);
+      else if (host) map_chunk<4, true, OpAddI32, LdSys>(d, p, OpAddI32{}, T);
       else map_chunk<4, true>(d, p, OpAddI32{}, T);
       break;
     case LK_KIND_SAXPY_F32:
       if (dyn) map_tma_dyn<true>(d, rank, count, OpSaxpy{d.alpha}, T, ring, g, ctr + 1);
       else if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, ring, g);
+      else if (host) map_chunk<4, true, OpSaxpy, LdSys>(d, p, OpSaxpy{d.alpha}, T);
       else map_chunk<4, true>(d, p, OpSaxpy{d.alpha}, T);
       break;
     case LK_KIND_HBM_STREAM: {
@@ -771,6 +792,8 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
           map_tma_dyn<false>(d, rank, count, OpCopy{}, T, ring, g, ctr + 1);
         } else if (tma) {
           map_tma<false>(d, p, OpCopy{}, T, ring, g);
+        } else if (host) {
+          map_chunk<8, false, OpCopy, LdSys>(d, p, OpCopy{}, T);
         } else {
           map_chunk<8, false>(d, p, OpCopy{}, T);
         }
@@ -780,6 +803,7 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
     case LK_KIND_BLOCK_REDUCE_F32:
       if (tma && T >= 32 * (ring.stages + 1) && ring.gred != nullptr)
         reduce_dyn(d, rank, count, ctr, rs, T, ring, red_share8, red_claim);
+      else if (host) reduce_static<LdSys>(d, rank, count, ctr, rs, T);
       else reduce_static(d, rank, count, ctr, rs, T);
       break;
     default: break;
@@ -847,6 +871,13 @@ __device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* 
   return v;
 }
 
+// The host wrote a host-mapped payload's inputs before the WORK value that
+// names it (release on the host side); the poll that saw the value is a
+// relaxed load, so a sys-scope fence after it makes it the acquire that the
+// payload's sys-scope loads are ordered behind (LK_HINT_SYSMEM only: device
+// payloads are staged through the copy engine and a stream sync).
+__device__ __forceinline__ void acquire_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 // A to_gpu value is {word:32, seq:24, hint:8}; seq is the host's per-worker
 // write index mod 2^24 (serial-number compare: a worker is never 2^23 writes
 // behind, every write waits on its handshake) and is widened back to 32 bits
@@ -858,6 +889,7 @@ __device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool ti
   e.seq += delta;
   e.cur = uint32_t(c);
   e.hint = uint32_t(c >> 56);
+  if (e.hint & LK_HINT_SYSMEM) acquire_sys();
   e.dirty = true;
   e.c_seen = clock64();
   if (timeline) e.t_seen = globaltimer();
@@ -1026,6 +1058,7 @@ __device__ __forceinline__ bool accept_chan(Elected& e, unsigned long long c, ui
   e.seq = e.dseq + e.rseq;
   e.cur = uint32_t(c);
   e.hint = uint32_t(c >> 56);
+  if (e.hint & LK_HINT_SYSMEM) acquire_sys();
   e.dirty = true;
   e.c_seen = clock64();
   if (timeline) e.t_seen = globaltimer();
@@ -1312,6 +1345,7 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
       if (__all_sync(0xffffffffu, mine)) {
         const uint32_t word = uint32_t(w0 >> 32);
         const uint32_t hint = uint32_t(__shfl_sync(0xffffffffu, w, 5)) & 0xFFu;
+        if (hint & LK_HINT_SYSMEM) acquire_sys();   // the event is the host's release: pass it on
         // the four 48-bit mask words stay in registers: a runtime index into
         // an array would put it in local memory
         const unsigned long long mm = (1ull << kRingMaskBits) - 1;
@@ -1529,8 +1563,10 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
       // before FINISHED is posted: a gpu-scope fence (~L2 round trip).  A
       // sys-scope release would also wait for this thread's earlier posted
       // host writes (WORKING) to cross PCIe (~1.5 us, tools/probe_costs.cu);
-      // LK_CF_FENCE_ALWAYS asks for it (outputs in host-mapped memory).
-      const bool sys = (a.flags & LK_CF_FENCE_ALWAYS) != 0;
+      // Host-mapped buffers (LK_DF_HOSTMEM) and LK_CF_FENCE_ALWAYS take it: the
+      // st.release.sys is cumulative over the barrier, so every thread's
+      // output stores are visible to the host before it can see FINISHED.
+      const bool sys = (a.flags & LK_CF_FENCE_ALWAYS) != 0 || (d.flags & LK_DF_HOSTMEM) != 0;
       if (!sys) asm volatile("fence.acq_rel.gpu;" ::: "memory");
       publish(a, wid, e, o.publish, sys);
       write_timeline(a, wid, e, t_begin, t_end, c_begin, clock64(), true);

@@ -20,8 +20,11 @@ block_reduce_f32    x float32                     partials float64[ceil(n/4096)]
 hbm_stream          src (any, 4-B elements)       dst
 =================== ============================= ===========================
 
-A buffer is a torch CUDA tensor, a :class:`DeviceBuffer`, or a raw device
-address (int).  ``n`` defaults to the element count of the first input.
+A buffer is a torch CUDA tensor, a :class:`DeviceBuffer`, a
+:class:`HostBuffer` (mapped pinned host memory, zero-copy), or a raw address
+(int) of either kind; the runtime classifies every pointer when it stages the
+descriptor and refuses anything else.  ``n`` defaults to the element count of
+the first input.
 """
 from __future__ import annotations
 
@@ -98,12 +101,72 @@ class DeviceBuffer:
             pass
 
 
+class HostBuffer:
+    """Mapped pinned host memory (``lk_host_alloc``: cudaHostAlloc Mapped |
+    Portable) that the persistent workers read and write over the link:
+    a zero-copy payload buffer.  It replaces the reference's Copyin/Copyout
+    phases (P/host.py:212-224) for small transfers, where a cudaMemcpy's fixed
+    cost dwarfs the bytes (P/link.py:84-122).
+
+    The runtime classifies the pointer when the descriptor is staged
+    (LK_DF_HOSTMEM): the worker reads it with sys-scope loads and publishes
+    FINISHED with a sys-scope release, so once ``wait`` returns the outputs
+    are in ``array()``.  The device address is the host address (UVA).
+    Write inputs before ``trigger`` and read outputs after ``wait``: the
+    protocol's handshake is the synchronisation."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        lib = _lib.load()
+        host = C.c_void_p()
+        _lib.check(lib.lk_host_alloc(device, nbytes, C.byref(host)))
+        self.ptr = int(host.value)
+        self.nbytes = nbytes
+        self.device = device
+
+    @classmethod
+    def from_array(cls, arr: np.ndarray, device: int = 0) -> "HostBuffer":
+        buf = cls(arr.nbytes, device)
+        buf.upload(arr)
+        return buf
+
+    def array(self, dtype, count: Optional[int] = None) -> np.ndarray:
+        """A numpy view of the buffer (no copy)."""
+        if not self.ptr:
+            raise UsageError("host buffer freed")
+        dt = np.dtype(dtype)
+        count = self.nbytes // dt.itemsize if count is None else count
+        if count * dt.itemsize > self.nbytes:
+            raise UsageError("view larger than the host buffer")
+        raw = (C.c_char * (count * dt.itemsize)).from_address(self.ptr)
+        return np.frombuffer(raw, dtype=dt, count=count)
+
+    def upload(self, arr: np.ndarray) -> None:
+        a = np.ascontiguousarray(arr)
+        if a.nbytes > self.nbytes:
+            raise UsageError("array larger than the host buffer")
+        C.memmove(self.ptr, a.ctypes.data, a.nbytes)
+
+    def download(self, dtype, count: Optional[int] = None) -> np.ndarray:
+        return self.array(dtype, count).copy()
+
+    def free(self) -> None:
+        if self.ptr:
+            _lib.load().lk_host_free(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def _addr(ref) -> int:
     if ref is None:
         return 0
     if isinstance(ref, int):
         return ref
-    if isinstance(ref, DeviceBuffer):
+    if isinstance(ref, (DeviceBuffer, HostBuffer)):
         return ref.ptr
     if hasattr(ref, "data_ptr"):
         if hasattr(ref, "is_cuda") and not ref.is_cuda:
@@ -116,7 +179,7 @@ def _addr(ref) -> int:
 
 
 def _numel(ref) -> Optional[int]:
-    if isinstance(ref, DeviceBuffer):
+    if isinstance(ref, (DeviceBuffer, HostBuffer)):
         return ref.nbytes // 4
     if hasattr(ref, "numel"):
         return int(ref.numel())
@@ -125,7 +188,7 @@ def _numel(ref) -> Optional[int]:
 
 def _nbytes(ref) -> Optional[int]:
     """Size of a payload buffer in bytes, or None for a raw address."""
-    if isinstance(ref, DeviceBuffer):
+    if isinstance(ref, (DeviceBuffer, HostBuffer)):
         return ref.nbytes
     if hasattr(ref, "numel") and hasattr(ref, "element_size"):
         return int(ref.numel()) * int(ref.element_size())

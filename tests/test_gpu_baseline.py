@@ -12,7 +12,7 @@ import pytest
 
 from oracle import work as W
 from paper_2310_01212_b200 import native
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks
+from paper_2310_01212_b200.device import DeviceBuffer, HostBuffer, WorkDescriptor, reduce_blocks
 
 pytestmark = pytest.mark.gpu
 
@@ -110,3 +110,18 @@ def test_launch_floor_modes_run(mode):
 def test_launch_floor_spin_schedule():
     total, _ = native.launch_floor(0, "kernel_sync", 200, spin_sched=True)
     assert np.median(total) > 0
+
+
+def test_launch_sync_baseline_with_host_buffers():
+    """Zero-copy buffers through the conventional launch (LK_DF_HOSTMEM
+    classified at launch, like a staged descriptor)."""
+    n = 4100
+    a, b = _i32(n, 7), _i32(n, 8)
+    ha, hb, ho = HostBuffer.from_array(a), HostBuffer.from_array(b), HostBuffer(4 * n)
+    base = native.LaunchSyncBaseline()
+    try:
+        base.launch(WorkDescriptor(slot=0, kind="vector_add_i32", data_in_ref=(ha, hb), data_out_ref=ho))
+        base.wait()
+    finally:
+        base.close()
+    np.testing.assert_array_equal(ho.array(np.int32, n), W.vector_add_i32(a, b))
