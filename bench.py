@@ -431,6 +431,83 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def thread_driver_rows(rows):
+    """Aggregate per-GPU rows of the --threads run: whole-job tasks/s = all
+    GPUs' rounds / the slowest GPU's time (the max-over-ranks rule)."""
+    t = max(r["elapsed_s"] for r in rows)
+    units = sum(r["rounds"] for r in rows)
+    return units / t, t, units
+
+
+def run_threads_arm(args):
+    """configs[4] in the north star's form: ONE process, one LK session per
+    visible GPU, each driven by its own host thread pinned to a core local to
+    its GPU's NUMA node (P/native.py:70-79's pinning concept), all timed
+    between two thread barriers.  Independent instances: no collective, no
+    shared state but the barrier."""
+    from paper_2310_01212_b200 import native
+    from paper_2310_01212_b200.device import WorkDescriptor
+    ndev = native.device_count()
+    gpus = args.gpus if args.gpus and args.gpus <= ndev else ndev
+    start_bar = threading.Barrier(gpus)
+    end_bar = threading.Barrier(gpus)
+    rows = [None] * gpus
+    errs = []
+    taken = set()
+    lock = threading.Lock()
+
+    def drive(d):
+        try:
+            native.init_device(d)
+            native.pin_host_thread(d)
+            local_cores = sorted(os.sched_getaffinity(0))
+            with lock:   # one core per thread, highest-numbered free one of the GPU's set
+                core = next((c for c in reversed(local_cores) if c not in taken), local_cores[-1])
+                taken.add(core)
+            os.sched_setaffinity(0, {core})
+            cfg = native.NativeConfig(num_workers=args.workers, device=d, spin_strategy=native.PURE_SPIN)
+            s, _ = native.NativeSession.start(cfg)
+            try:
+                s.register(WorkDescriptor(slot=0, kind="empty"))
+                rr = [1 << i for i in range(s.num_workers)]
+                for _ in range(args.warmup):
+                    s.bench_roundtrip(rr, 0, args.rounds)
+                start_bar.wait()
+                t0 = time.perf_counter_ns()
+                done = [s.bench_roundtrip(rr, 0, args.rounds)[1] for _ in range(args.steps)]
+                el = (time.perf_counter_ns() - t0) / 1e9
+                end_bar.wait()
+                done = np.concatenate(done)
+                rows[d] = {"device": d, "core": core, "workers": s.num_workers, "rounds": int(done.size),
+                           "elapsed_s": el, "tasks_per_s": round(done.size / el, 1),
+                           "trigger_to_done": lat_summary(done)}
+                s.dispose()
+            finally:
+                s.close()
+        except Exception as exc:   # report; abort the barriers so the other threads do not wait forever
+            errs.append(f"gpu {d}: {exc!r}")
+            start_bar.abort()
+            end_bar.abort()
+
+    ths = [threading.Thread(target=drive, args=(d,)) for d in range(gpus)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errs:
+        print(json.dumps({"metric": METRIC, "error": errs}), flush=True)
+        return
+    value, t_max, units = thread_driver_rows(rows)
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "tasks/s", "n_gpus": gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * t_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "configs[4]: independent LK instances, one per GPU, one NUMA-pinned host "
+                                   "thread each, in one process (configs[1] loop on every GPU)",
+                       "parallelism": f"threads{gpus}", "rounds_per_step": args.rounds},
+            "gpu_launches": gpus, "per_gpu": rows}
+    print(json.dumps(line), flush=True)
+
+
 METRIC = "trigger->done round trips per second (empty task, 148 persistent workers)"
 # extras printed at the end of the JSON line, next to the latency headline
 HEADLINE_EXTRAS = ("single_worker", "full_mask", "interference", "interference_green", "pingpong_floor",
@@ -670,6 +747,107 @@ def measure_small_transfer(device, reps):
     return {"h2d_4B_memcpy": lat_summary(up), "d2h_4B_memcpy": lat_summary(down),
             "note": "cudaMemcpyAsync + stream sync of 4 bytes through the Python API (DeviceBuffer "
                     "upload/download); compare the mailbox word round trip in latency_us"}
+
+
+def measure_zero_copy(cfg, device, sizes, reps):
+    """The paper's small-transfer case on B200 (P/link.py:
+    84-122; P/host.py:212-224): one int32 vector add of `b` bytes per input
+    on ONE worker, inputs from the host and the result back to the host, per
+    task, end to end:
+      lk_zero_copy   HostBuffer in/out (LK_DF_HOSTMEM), trigger+wait only
+                     (closed loop in C: lk_bench_roundtrip)
+      lk_copies      DeviceBuffers: 2 cudaMemcpy H2D + trigger+wait + 1 D2H
+      launch_copies  the conventional flow: 2 H2D + launch + sync + D2H
+      launch_zero_copy  launch + sync with the HostBuffers
+    Then the mailbox-only single-worker sync against the paper's full-board
+    workaround (LK_CF_FULL_BOARD: every write re-ships all 148 cells)."""
+    from paper_2310_01212_b200 import native
+    from paper_2310_01212_b200.device import DeviceBuffer, HostBuffer, WorkDescriptor
+    rng = np.random.default_rng(0)
+    bufs = {}
+    for b in sizes:
+        n = max(1, b // 4)
+        a = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+        c = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+        bufs[b] = (n, a, c, HostBuffer.from_array(a, device), HostBuffer.from_array(c, device),
+                   HostBuffer(4 * n, device), DeviceBuffer(4 * n, device), DeviceBuffer(4 * n, device),
+                   DeviceBuffer(4 * n, device))
+    out = {"sizes_bytes": list(sizes), "reps": reps}
+    zcfg = dataclasses.replace(cfg, poll_mode="direct", full_board=False)
+    s, _ = native.NativeSession.start(zcfg)
+    rows = {}
+    ok = True
+    for k, b in enumerate(sizes):
+        n, a, c, ha, hc, ho, da, dc, do = bufs[b]
+        zw = WorkDescriptor(slot=700 + k, kind="vector_add_i32", data_in_ref=(ha, hc), data_out_ref=ho)
+        s.register(zw, 1)
+        s.bench_roundtrip([1], 700 + k, 200)
+        _, zdone, zcyc = s.bench_roundtrip([1], 700 + k, reps)
+        ok &= bool(np.array_equal(ho.array(np.int32, n), a + c))
+        cw = WorkDescriptor(slot=720 + k, kind="vector_add_i32", data_in_ref=(da, dc), data_out_ref=do)
+        res = np.empty(n, np.int32)
+        lat = []
+        for r in range(reps // 4 + 50):
+            t0 = time.perf_counter_ns()
+            da.upload(a)
+            dc.upload(c)
+            s.trigger(1, cw)
+            s.wait(1)
+            res[:] = do.download(np.int32, n)
+            if r >= 50:
+                lat.append(time.perf_counter_ns() - t0)
+        ok &= bool(np.array_equal(res, a + c))
+        s.timings.clear()
+        rows[b] = {"lk_zero_copy": lat_summary(zcyc), "lk_zero_copy_trigger_to_done": lat_summary(zdone),
+                   "lk_copies": lat_summary(lat)}
+    s.dispose()
+    s.close()
+    base = native.LaunchSyncBaseline(device=device, grid=1)
+    for k, b in enumerate(sizes):
+        n, a, c, ha, hc, ho, da, dc, do = bufs[b]
+        cw = WorkDescriptor(slot=0, kind="vector_add_i32", data_in_ref=(da, dc), data_out_ref=do)
+        zw = WorkDescriptor(slot=0, kind="vector_add_i32", data_in_ref=(ha, hc), data_out_ref=ho)
+        lat, zl = [], []
+        res = np.empty(n, np.int32)
+        for r in range(reps // 4 + 50):
+            t0 = time.perf_counter_ns()
+            da.upload(a)
+            dc.upload(c)
+            base.launch(cw, 1)
+            base.wait()
+            res[:] = do.download(np.int32, n)
+            t1 = time.perf_counter_ns()
+            base.launch(zw, 1)
+            base.wait()
+            t2 = time.perf_counter_ns()
+            if r >= 50:
+                lat.append(t1 - t0)
+                zl.append(t2 - t1)
+        ok &= bool(np.array_equal(res, a + c)) and bool(np.array_equal(ho.array(np.int32, n), a + c))
+        rows[b]["launch_copies"] = lat_summary(lat)
+        rows[b]["launch_zero_copy"] = lat_summary(zl)
+    base.close()
+    out["per_size"] = rows
+    out["results_exact"] = ok
+    # mailbox bytes only vs the full board, single-worker round robin over every worker
+    board = {}
+    for name, fb in (("mailbox_word", False), ("full_board", True)):
+        bs, _ = native.NativeSession.start(dataclasses.replace(cfg, poll_mode="direct", full_board=fb))
+        bs.register(WorkDescriptor(slot=0, kind="empty"))
+        m = [1 << i for i in range(bs.num_workers)]
+        bs.bench_roundtrip(m, 0, 2000)
+        _, d, cy = bs.bench_roundtrip(m, 0, reps)
+        board[name] = {"trigger_to_done": lat_summary(d), "round_trip": lat_summary(cy)}
+        bs.dispose()
+        bs.close()
+    board["note"] = ("the paper had to ship the whole mailbox board for a single-SM trigger because the "
+                     "driver deferred tiny transfers (PAPER.md:157-160); mapped sys-scope stores are never "
+                     "deferred, so the single 8-B word completes and the board costs only extra stores")
+    out["single_sm_sync"] = board
+    out["note"] = ("per task, host->device inputs and device->host result included; lk_zero_copy from C "
+                   "(lk_bench_roundtrip), the copy flows through the Python API (DeviceBuffer.upload/"
+                   "download: cudaMemcpyAsync + stream sync)")
+    return out
 
 
 def measure_multi_driver(session, drivers, rounds):
@@ -971,6 +1149,15 @@ def run_lk_arm(args, world, rank, local):
         isession.dispose()
         isession.close()
 
+    # zero-copy payloads vs cudaMemcpy for small transfers, and the full-board
+    # mailbox workaround
+    if rank == 0 and not args.no_zero_copy:
+        try:
+            extras["zero_copy"] = measure_zero_copy(cfg, device, [4, 64, 1024, 4096, 16384, 65536],
+                                                    args.zc_reps)
+        except Exception as exc:
+            extras["zero_copy"] = {"error": repr(exc)}
+
     # conventional launch+sync baseline, same host thread
     base = {}
     b1 = native.LaunchSyncBaseline(device=device)
@@ -1152,6 +1339,11 @@ def main():
     ap.add_argument("--no-table2", action="store_true")
     ap.add_argument("--no-lazy", action="store_true")
     ap.add_argument("--no-green", action="store_true")
+    ap.add_argument("--no-zero-copy", action="store_true")
+    ap.add_argument("--threads", action="store_true",
+                    help="configs[4] in one process: a session per visible GPU (or --gpus of them), one "
+                         "NUMA-pinned host thread each")
+    ap.add_argument("--zc-reps", type=int, default=4000)
     ap.add_argument("--lazy-rounds", type=int, default=200_000)
     ap.add_argument("--drivers", type=int, default=4, help="host threads for the multi-driver throughput extra")
     ap.add_argument("--driver-rounds", type=int, default=100_000)
@@ -1165,6 +1357,10 @@ def main():
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference_arm(args, world, rank)
+    elif args.threads:
+        if world > 1:
+            raise SystemExit("--threads drives every GPU from one process; do not launch it under torchrun")
+        run_threads_arm(args)
     else:
         run_lk_arm(args, world, rank, local)
     if world > 1:

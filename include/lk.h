@@ -162,7 +162,10 @@ typedef struct lk_config {
 #define LK_POLL_HYBRID  2u
 #define LK_HYBRID_DIRECT_MAX 8u
 
-#define LK_CF_ACQUIRE_POLL   1u  /* poll with ld.acquire.sys instead of ld.relaxed.sys */
+#define LK_CF_ACQUIRE_POLL   1u  /* (the default; kept for ABI compatibility) every poll of a to_gpu cell or
+                                    event-ring entry is ld.acquire.sys, mailbox polls ld.acquire.gpu */
+#define LK_CF_RELAXED_POLL 2048u /* polls with ld.relaxed.sys / .gpu instead; a host-mapped payload
+                                    (LK_HINT_SYSMEM) then costs a fence.acq_rel.sys (~1.5 us) */
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
 #define LK_CF_LSU_PAYLOAD    4u  /* payload items with 128-bit LSU loads instead of the TMA bulk ring */
 #define LK_CF_TIMELINE       8u  /* GATEWAY: stamp forward times into the device timeline (+1 L2 load per value) */

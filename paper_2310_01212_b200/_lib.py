@@ -48,6 +48,7 @@ CF_NO_ACK_DELAY = 128
 CF_ACK_FIXED = 256
 CF_HOST_DESC = 512
 CF_FULL_BOARD = 1024
+CF_RELAXED_POLL = 2048
 FLOOR_SYNC = 0
 FLOOR_QUERY = 1
 FLOOR_GRAPH = 2

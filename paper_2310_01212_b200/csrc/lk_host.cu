@@ -696,8 +696,13 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.tma_min_workers == 0) cfg.tma_min_workers = 49;
   if ((cfg.flags & LK_CF_HOST_DESC) && cfg.poll_mode != LK_POLL_DIRECT)
     return fail(LK_E_CONFIG, "host-resident descriptors (LK_CF_HOST_DESC) need DIRECT polling");
-  // the WORK word's poll must be an acquire for the host-written descriptor to be visible after it
-  if (cfg.flags & LK_CF_HOST_DESC) cfg.flags |= LK_CF_ACQUIRE_POLL;
+  // polls are acquires (ld.acquire.sys: LDG.STRONG.SYS + CCTL.IVALL, no membar;
+  // within noise of relaxed polls, tools/ab_acquire.py) unless the caller asks
+  // for relaxed ones; host-written descriptors need the acquire
+  if (cfg.flags & LK_CF_RELAXED_POLL) cfg.flags &= ~LK_CF_ACQUIRE_POLL;
+  else cfg.flags |= LK_CF_ACQUIRE_POLL;
+  if ((cfg.flags & LK_CF_HOST_DESC) && (cfg.flags & LK_CF_RELAXED_POLL))
+    return fail(LK_E_CONFIG, "host-resident descriptors (LK_CF_HOST_DESC) need acquire polls");
   if (cfg.ack_delay_ns > 100000 || cfg.idle_delay_ns > 100000)
     return fail(LK_E_CONFIG, "ack_delay_ns and idle_delay_ns must be at most 100000");
 
@@ -1531,6 +1536,7 @@ extern "C" int lk_kernel_alive(lk_session* s, uint32_t* alive) {
 extern "C" int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n) {
   if (!s || !t) return fail(LK_E_USAGE, "null argument");
   const uint32_t m = std::min(n, s->nw);
+  LK_CUDA(cudaSetDevice(s->device));
   LK_CUDA(cudaMemcpyAsync(t, s->d_spans, size_t(m) * 8 * LK_TIMELINE_WORDS, cudaMemcpyDeviceToHost,
                           s->copy_stream));
   LK_CUDA(cudaStreamSynchronize(s->copy_stream));
@@ -1684,6 +1690,7 @@ struct MergedRec {
 static int build_trace(lk_session* s, std::vector<MergedRec>& outv) {
   if (!s->cfg.record_trace) return fail(LK_E_USAGE, "session was started without record_trace");
   std::vector<uint32_t> cnt(s->nw);
+  LK_CUDA(cudaSetDevice(s->device));
   LK_CUDA(cudaMemcpyAsync(cnt.data(), s->d_tcnt, 4 * size_t(s->nw), cudaMemcpyDeviceToHost, s->copy_stream));
   LK_CUDA(cudaStreamSynchronize(s->copy_stream));
   for (uint32_t i = 0; i < s->nw; ++i)

@@ -73,6 +73,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu64(const unsigned lo
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t ld_relaxed_gpu32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -872,24 +877,25 @@ __device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* 
 }
 
 // The host wrote a host-mapped payload's inputs before the WORK value that
-// names it (release on the host side); the poll that saw the value is a
-// relaxed load, so a sys-scope fence after it makes it the acquire that the
-// payload's sys-scope loads are ordered behind (LK_HINT_SYSMEM only: device
-// payloads are staged through the copy engine and a stream sync).
+// names it (release on the host side).  A poll with ld.acquire.sys
+// (LK_CF_ACQUIRE_POLL; LDG.STRONG.SYS + CCTL.IVALL, no membar) is already the
+// acquire the payload's loads are ordered behind.  A relaxed poll, or a value
+// forwarded through the gateway or a channel poller, gets a sys-scope fence
+// after it instead (LK_HINT_SYSMEM only: MEMBAR.SYS costs ~1.5 us).
 __device__ __forceinline__ void acquire_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 // A to_gpu value is {word:32, seq:24, hint:8}; seq is the host's per-worker
 // write index mod 2^24 (serial-number compare: a worker is never 2^23 writes
 // behind, every write waits on its handshake) and is widened back to 32 bits
 // here, so trace records carry the host's full write index.
-__device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool timeline) {
+__device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool timeline, bool acquired = false) {
   const uint32_t sq = uint32_t(c >> 32) & 0xFFFFFFu;
   const uint32_t delta = (sq - e.seq) & 0xFFFFFFu;
   if (delta == 0 || delta >= 0x800000u) return false;
   e.seq += delta;
   e.cur = uint32_t(c);
   e.hint = uint32_t(c >> 56);
-  if (e.hint & LK_HINT_SYSMEM) acquire_sys();
+  if ((e.hint & LK_HINT_SYSMEM) && !acquired) acquire_sys();
   e.dirty = true;
   e.c_seen = clock64();
   if (timeline) e.t_seen = globaltimer();
@@ -1144,7 +1150,7 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
     for (bool fresh = false; !fresh;) {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        if (accept(e, v[k], timeline)) {
+        if (accept(e, v[k], timeline, acquire)) {
           const uint32_t f = fast_step(a, wid, e);
           if (f == kFastBegin) return LK_ACT_BEGIN;
           fresh = f == kFastNone;          // settled in place: keep polling
@@ -1190,7 +1196,7 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
         if (((uint32_t(v >> 32) - e.seq) & 0xFFFFFFu) == 0) c = x;
         hx = false;
       }
-      if (accept(e, c, timeline)) {
+      if (accept(e, c, timeline, acquire)) {
         const uint32_t f = fast_step(a, wid, e);
         if (f == kFastBegin) return LK_ACT_BEGIN;
         if (f == kFastNone) break;                  // general path
@@ -1220,11 +1226,12 @@ __device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t 
 __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t wid, Elected& e) {
   const unsigned long long* mb = a.dmb + uint64_t(wid) * a.dmb_u64;
   const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
+  const bool acq = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
   for (;;) {
     const uint32_t act = settle(a, wid, e);
     if (act != LK_ACT_NONE) return act;
     for (;;) {
-      if (accept(e, ld_relaxed_gpu64(mb), timeline)) {
+      if (accept(e, acq ? ld_acquire_gpu64(mb) : ld_relaxed_gpu64(mb), timeline, acq)) {
         if (timeline) e.t_fwd = ld_relaxed_gpu64(mb + 1);
         const uint32_t f = fast_step(a, wid, e);
         if (f == kFastBegin) return LK_ACT_BEGIN;
@@ -1319,6 +1326,7 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = a.nw, N = a.ring_entries;
   const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
+  const bool acq = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
   uint32_t wseq[6];                               // per-worker write counts, workers lane + 32q
 #pragma unroll
   for (int q = 0; q < 6; ++q) wseq[q] = 0;
@@ -1326,7 +1334,7 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
   unsigned long long v[K];
   auto issue = [&](int k) {
     if (lane < 6)
-      v[k] = ld_cell(a.ring + (uint64_t(k) * N + (expect - 1) % N) * 8 + lane, false);
+      v[k] = ld_cell(a.ring + (uint64_t(k) * N + (expect - 1) % N) * 8 + lane, acq);
   };
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -1345,7 +1353,13 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
       if (__all_sync(0xffffffffu, mine)) {
         const uint32_t word = uint32_t(w0 >> 32);
         const uint32_t hint = uint32_t(__shfl_sync(0xffffffffu, w, 5)) & 0xFFu;
-        if (hint & LK_HINT_SYSMEM) acquire_sys();   // the event is the host's release: pass it on
+        // a host-mapped payload: the entry's acquire load synchronised with the
+        // host's release; a gpu-scope release fence before the forwarding
+        // stores passes it on to the workers' acquire polls of their mailboxes
+        if (hint & LK_HINT_SYSMEM) {
+          if (acq) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          else acquire_sys();
+        }
         // the four 48-bit mask words stay in registers: a runtime index into
         // an array would put it in local memory
         const unsigned long long mm = (1ull << kRingMaskBits) - 1;

@@ -67,7 +67,7 @@ class NativeConfig:
     poll_spacing_ns: int = 300
     num_slots: int = 1024
     trace_capacity: int = 65536
-    acquire_poll: bool = False
+    acquire_poll: bool = True       # polls are ld.acquire.sys (False: relaxed; tools/ab_acquire.py)
     fence_always: bool = False
     tma_payload: bool = True        # payload tiles via the TMA bulk ring (False: 128-bit LSU loads)
     ring_stages: int = 6            # TMA ring depth, 16-KiB stages (2..12)
@@ -87,6 +87,8 @@ class NativeConfig:
     host_descriptors: bool = False  # descriptor table in pinned mapped host memory (direct mode):
                                     # trigger/wait/register make no CUDA call, so the session works
                                     # while a serialising profiler (ncu) holds the kernel's launch
+    full_board: bool = False        # direct mode: every mailbox write ships the whole board (the
+                                    # paper's workaround for deferred small transfers)
 
     def __post_init__(self) -> None:
         if self.num_workers is not None and self.num_workers < 1:
@@ -126,7 +128,7 @@ class NativeConfig:
         c.ack_delay_ns = self.ack_delay_ns
         c.idle_delay_ns = self.idle_delay_ns
         c.tma_min_workers = self.tma_min_workers
-        c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else 0)
+        c.flags = ((_lib.CF_ACQUIRE_POLL if self.acquire_poll else _lib.CF_RELAXED_POLL)
                    | (_lib.CF_FENCE_ALWAYS if self.fence_always else 0)
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)
                    | (_lib.CF_TIMELINE if self.timeline else 0)
@@ -135,7 +137,8 @@ class NativeConfig:
                    | (_lib.CF_DYNAMIC_TILES if self.dynamic_tiles else 0)
                    | (0 if self.ack_delay_ns else _lib.CF_NO_ACK_DELAY)
                    | (0 if self.ack_adaptive else _lib.CF_ACK_FIXED)
-                   | (_lib.CF_HOST_DESC if self.host_descriptors else 0))
+                   | (_lib.CF_HOST_DESC if self.host_descriptors else 0)
+                   | (_lib.CF_FULL_BOARD if self.full_board else 0))
         return c
 
 
@@ -147,6 +150,12 @@ def init_device(device: int = 0) -> None:
     p = C.c_uint64()
     _lib.check(lib.lk_dev_alloc(device, 1, C.byref(p)))
     _lib.check(lib.lk_dev_free(p.value))
+
+
+def device_count() -> int:
+    """Visible CUDA devices (lk_device_count); 0 without a GPU."""
+    n = C.c_int()
+    return n.value if _lib.load().lk_device_count(C.byref(n)) == 0 else 0
 
 
 def under_profiler() -> bool:

@@ -72,3 +72,22 @@ def test_reference_arm_under_torchrun_two_ranks():
     assert line["impl"] == "reference" and line["n_gpus"] == 2
     assert line["cpu_baseline"]["kind"] in ("reference", "port")
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
+
+
+def test_thread_driver_aggregate_is_rounds_over_slowest_thread():
+    """bench.py --threads: whole-job tasks/s over the per-GPU host threads."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    rows = [{"rounds": 1000, "elapsed_s": 0.5}, {"rounds": 1000, "elapsed_s": 1.0},
+            {"rounds": 2000, "elapsed_s": 0.8}]
+    v, t, u = bench.thread_driver_rows(rows)
+    assert (v, t, u) == (4000.0, 1.0, 4000)
+
+
+def test_threads_flag_refused_under_torchrun():
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+           "--threads", "--gpus", "2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode != 0 and "--threads drives every GPU from one process" in r.stderr

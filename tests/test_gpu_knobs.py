@@ -30,7 +30,7 @@ KNOBS = {
     "threads64": dict(threads_per_worker=64),
     "threads544": dict(threads_per_worker=544),
     "backoff": dict(poll_backoff_ns=400),
-    "acquire-poll": dict(acquire_poll=True),
+    "relaxed-poll": dict(acquire_poll=False),
     "fence-always": dict(fence_always=True),
     "replicas2": dict(poll_replicas=2, poll_spacing_ns=150),
     "replicas8": dict(poll_replicas=8),
