@@ -120,8 +120,9 @@ typedef struct lk_config {
   uint32_t num_slots;            /* descriptor table entries; 0 = 1024 */
   uint64_t wait_timeout_ns;      /* wait_timeout_s (native.py:52) */
   uint32_t flags;                /* LK_CF_* */
-  uint32_t poll_replicas;        /* to_gpu replicas per worker, one staggered load in flight on each: 1,2,4,8; 0 = 1 */
-  uint32_t poll_spacing_ns;      /* stagger between replica loads / sweeps; 0 = 300 */
+  uint32_t poll_replicas;        /* 0 or 1 (one to_gpu cell / event ring; replicas were measured slower
+                                    and removed) */
+  uint32_t poll_spacing_ns;      /* unused since replicas were removed (kept for the ABI) */
   uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default), LK_POLL_GATEWAY or LK_POLL_HYBRID */
   uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 64 */
   uint32_t ring_stages;          /* TMA payload ring depth in 16-KiB stages, 2..12; 0 = 6 */
@@ -169,12 +170,8 @@ typedef struct lk_config {
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */
 #define LK_CF_LSU_PAYLOAD    4u  /* payload items with 128-bit LSU loads instead of the TMA bulk ring */
 #define LK_CF_TIMELINE       8u  /* GATEWAY: stamp forward times into the device timeline (+1 L2 load per value) */
-#define LK_CF_ACK_WINDOW    32u  /* DIRECT, 1 replica: a worker awaiting its ack samples the cell twice
-                                    (a second load poll_spacing_ns after the first) */
-#define LK_CF_DYNAMIC_TILES 64u  /* payload maps: 7/8 static share per worker + a pool of tiles claimed by
-                                    whoever finishes first (default: fixed contiguous chunks; the pool
-                                    measured neutral at 64 MiB and -11% at 16 MiB on an idle GPU, and is
-                                    meant for SMs slowed unevenly by co-running work) */
+#define LK_CF_ACK_WINDOW    32u  /* removed (measured neutral): refused by lk_create */
+#define LK_CF_DYNAMIC_TILES 64u  /* removed (measured neutral at 64 MiB, -11% at 16 MiB): refused */
 #define LK_CF_NO_ACK_DELAY 128u  /* DIRECT, 1 replica: poll for the ack right after FINISHED
                                     (lk_config.ack_delay_ns) */
 #define LK_CF_ACK_FIXED    256u  /* keep ack_delay_ns as configured (no per-worker adaptation) */
@@ -318,13 +315,17 @@ int lk_profile_run(const lk_config* cfg, const lk_desc* descs, uint32_t ndesc, u
 /* Device-side spans of the last dispatch per worker (globaltimer ns):
  * begin (WORK observed) and end (work done, before FINISHED). */
 int lk_last_spans(lk_session* s, uint64_t* begin_ns, uint64_t* end_ns, uint32_t n);
-/* Device timeline of the last dispatch per worker, 12 words each (t[12*i+k]):
+/* Device timeline of the last dispatch per worker, 16 words each (t[16*i+k]):
  * globaltimer ns at k=0 to_gpu value seen, 1 work begin, 2 work end,
  * 3 FINISHED issued, 4 gateway forward (LK_CF_TIMELINE, else 0); clock64 at
  * 5 value seen, 6 work begin, 7 FINISHED issued.  The ack phase of an empty
  * task on a DIRECT session with LK_CF_TIMELINE (else 0): 8 globaltimer at
  * FINISHED issued, 9 globaltimer when the NOP ack was seen, 10 cell loads
- * issued in between, 11 clock64 when the NOP ack was seen. */
+ * issued in between, 11 clock64 when the NOP ack was seen.  The phases of a
+ * block_reduce_f32 dispatch on the TMA ring with LK_CF_TIMELINE (else 0):
+ * globaltimer at 12 first bulk copy issued, 13 last bulk copy issued, 14
+ * first block's data in shared memory, 15 arrival counted (before the
+ * last worker's combine). */
 int lk_last_timeline(lk_session* s, uint64_t* t, uint32_t n);
 /* Launch+sync floor: the cheapest conventional per-task flow, an empty
  * <<<1,32,0>>> kernel joined by stream sync (LK_FLOOR_SYNC), by a host spin

@@ -675,16 +675,18 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   if (cfg.status_stride != 16 && cfg.status_stride != 32 && cfg.status_stride != 64 && cfg.status_stride != 128)
     return fail(LK_E_CONFIG, "status_stride must be 16, 32, 64 or 128");
   if (cfg.poll_mode > LK_POLL_HYBRID) return fail(LK_E_CONFIG, "unknown poll_mode %u", cfg.poll_mode);
-  if (cfg.poll_mode == LK_POLL_HYBRID && cfg.poll_replicas > 2)
-    return fail(LK_E_CONFIG, "hybrid mode takes 1 or 2 event-ring replicas");
+  // Replicated cells / event rings and the ack window measured slower or
+  // neutral in every mode and were removed; the fields
+  // stay in the ABI and take their one remaining value.
   if (cfg.poll_replicas == 0) cfg.poll_replicas = 1;
+  if (cfg.poll_replicas != 1)
+    return fail(LK_E_CONFIG, "poll_replicas must be 1 (replicated cells were measured slower and removed)");
+  if (cfg.flags & (LK_CF_ACK_WINDOW | LK_CF_DYNAMIC_TILES))
+    return fail(LK_E_CONFIG, "LK_CF_ACK_WINDOW and LK_CF_DYNAMIC_TILES were measured neutral or slower and "
+                "removed");
   if (cfg.ring_stages == 0) cfg.ring_stages = 6;
   if (cfg.ring_stages < 2 || cfg.ring_stages > lk_ring_max_stages())
     return fail(LK_E_CONFIG, "ring_stages must be 2..%u", lk_ring_max_stages());
-  if (cfg.poll_replicas != 1 && cfg.poll_replicas != 2 && cfg.poll_replicas != 4 && cfg.poll_replicas != 8)
-    return fail(LK_E_CONFIG, "poll_replicas must be 1, 2, 4 or 8");
-  if (cfg.poll_mode == LK_POLL_GATEWAY && cfg.poll_replicas == 8)
-    return fail(LK_E_CONFIG, "gateway mode takes 1, 2 or 4 event-ring replicas");
   if (cfg.poll_spacing_ns == 0) cfg.poll_spacing_ns = 300;
   if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 512;
   if (cfg.threads_per_worker % 32 || cfg.threads_per_worker > 544)

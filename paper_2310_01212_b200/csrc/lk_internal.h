@@ -67,7 +67,7 @@ cudaError_t lk_persistent_configure(size_t smem);
 cudaError_t lk_preload_kernels();
 cudaError_t lk_launch_clocksync(const uint32_t* flag, unsigned long long* echo, uint32_t rounds,
                                 cudaStream_t st);
-#define LK_TIMELINE_WORDS 12
+#define LK_TIMELINE_WORDS 16
 cudaError_t lk_launch_topo(uint32_t* smids, uint32_t grid, uint32_t cluster, size_t smem, cudaStream_t st);
 cudaError_t lk_persistent_occupancy(uint32_t threads, size_t smem, int* blocks_per_sm);
 cudaError_t lk_launch_work(const lk_desc& d, uint32_t grid, uint32_t threads,

@@ -347,97 +347,7 @@ __device__ __forceinline__ void map_tma(const lk_desc& d, Part p, const Op& op, 
   for (uint64_t i = max(p.b, ve << 2) + t; i < p.e; i += T) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
 }
 
-// map through the TMA ring with a balanced tail (LK_CF_DYNAMIC_TILES):
-// each worker first streams a static share of 7/8 of the tiles, contiguous
-// by rank; the last 1/8 of the tiles form a pool claimed one at a time with
-// an atomic counter, the next claim issued before the current tile's copies
-// so the atomic's L2 round trip overlaps them.  Whoever finishes its share
-// first takes more of the pool, so a dispatch ends when the *average*
-// worker would, not the slowest one (per-dispatch stragglers are random:
-// tools/straggler.py).  Elementwise maps only: results do not depend on who
-// computes a tile.  ctr[0] = next pool tile, ctr[1] = workers done; the last
-// worker to finish resets both for the slot's next dispatch.
-constexpr uint32_t kTileEnd = 0xFFFFFFFFu;
-
-template <bool kTwo, class Op>
-__device__ __forceinline__ void map_tma_dyn(const lk_desc& d, uint32_t rank, uint32_t count, const Op& op,
-                                            uint32_t T, Ring& r, uint32_t& g, uint32_t* ctr) {
-  const uint4* a4 = reinterpret_cast<const uint4*>(d.in0);
-  const uint4* c4 = reinterpret_cast<const uint4*>(d.in1);
-  uint4* o4 = reinterpret_cast<uint4*>(d.out);
-  constexpr uint32_t kTileV = kTwo ? kStageBytes / 32 : kStageBytes / 16;   // uint4 per input per tile
-  const uint64_t nv = d.n >> 2;                                           // vector part, all workers
-  const uint32_t ntiles = uint32_t((nv + kTileV - 1) / kTileV);
-  const uint32_t share = uint32_t((uint64_t(ntiles) * 7 / 8) / count);     // static tiles per worker
-  const uint32_t pool0 = share * count;                                    // first pool tile
-  const uint32_t c0 = g, S = r.stages;
-  if (threadIdx.x == 0) {
-    uint32_t f = c0;
-    auto fill = [&](uint32_t t) {                                          // t = global tile or kTileEnd
-      const uint32_t st = f % S;
-      mbar_wait(r.empty + st, ((f / S) & 1u) ^ 1u);
-      r.tile[st] = t;
-      if (t == kTileEnd) {
-        mbar_arrive(r.full + st);                                          // wake consumers, no bytes
-      } else {
-        const uint64_t v0 = uint64_t(t) * kTileV;
-        const uint32_t bytes = uint32_t(min(uint64_t(kTileV), nv - v0)) * 16u;
-        mbar_expect_tx(r.full + st, kTwo ? 2 * bytes : bytes);
-        bulk_g2s(r.buf + st * kStageBytes, a4 + v0, bytes, r.full + st);
-        if (kTwo) bulk_g2s(r.buf + st * kStageBytes + kStageBytes / 2, c4 + v0, bytes, r.full + st);
-      }
-      ++f;
-    };
-    for (uint32_t i = 0; i < share; ++i) fill(rank * share + i);
-    uint32_t claim = atomicAdd(ctr, 1u);
-    for (;;) {
-      const uint32_t t = pool0 + claim;
-      if (t >= ntiles) break;
-      const uint32_t next = atomicAdd(ctr, 1u);                           // in flight during fill(t)
-      fill(t);
-      claim = next;
-    }
-    fill(kTileEnd);
-    *r.gshared = f;
-  } else if (threadIdx.x >= 32) {
-    const uint32_t ci = threadIdx.x - 32, nc = T - 32;
-    for (uint32_t c = c0;; ++c) {
-      const uint32_t st = c % S;
-      mbar_wait(r.full + st, (c / S) & 1u);
-      const uint32_t t = r.tile[st];
-      if (t != kTileEnd) {
-        const uint64_t v0 = uint64_t(t) * kTileV;
-        const uint32_t nvt = uint32_t(min(uint64_t(kTileV), nv - v0));
-        const uint8_t* stage = r.buf + st * kStageBytes;
-        for (uint32_t v = ci; v < nvt; v += nc) {
-          const uint4 x = lds4(stage + 16 * v);
-          const uint4 y = kTwo ? lds4(stage + kStageBytes / 2 + 16 * v) : x;
-          st4(o4 + v0 + v, vop(op, x, y));
-        }
-      }
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(r.empty + st);
-      if (t == kTileEnd) break;
-    }
-  }
-  wsync(T);                                                                // gshared visible; stream done
-  g = *r.gshared;
-  if (threadIdx.x == 0) {
-    // scalar tail (n % 4 elements) by rank 0; then count this worker done
-    if (rank == 0) {
-      const uint32_t* a = reinterpret_cast<const uint32_t*>(d.in0);
-      const uint32_t* c = reinterpret_cast<const uint32_t*>(d.in1);
-      uint32_t* o = reinterpret_cast<uint32_t*>(d.out);
-      for (uint64_t i = nv << 2; i < d.n; ++i) o[i] = op.s(ld_cg1(a + i), kTwo ? ld_cg1(c + i) : 0u);
-    }
-    uint32_t prev;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr + 1) : "memory");
-    if (prev == count - 1) {   // last one out: no worker claims from this slot any more
-      ctr[0] = 0;
-      ctr[1] = 0;
-    }
-  }
-}
+constexpr uint32_t kTileEnd = 0xFFFFFFFFu;   // ring end marker (reduce_dyn)
 
 // ---------------------------------------------------------------- block reduce
 // block_reduce_f32 is defined on fixed 4096-element blocks (oracle/work.py:
@@ -576,7 +486,7 @@ __device__ __forceinline__ double ld_cg_f64(const double* p) {
 // ctr[1] = pool claims; the last worker resets both for the slot's next
 // dispatch (no worker claims or arrives any more by then).
 __device__ __forceinline__ void reduce_finish(const lk_desc& d, uint32_t count, uint32_t* ctr, ReduceSmem& sm,
-                                              uint32_t T) {
+                                              uint32_t T, unsigned long long* tl = nullptr) {
   const uint32_t t = threadIdx.x;
   wsync(T);                 // every block partial of this worker stored
   if (t == 0) {
@@ -585,6 +495,7 @@ __device__ __forceinline__ void reduce_finish(const lk_desc& d, uint32_t count, 
     uint32_t prev;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
     sm.last = prev == count - 1;
+    if (tl) tl[15] = globaltimer();
   }
   wsync(T);
   if (!sm.last) return;
@@ -645,7 +556,7 @@ __device__ __forceinline__ void reduce_finish(const lk_desc& d, uint32_t count, 
 // and stores the block sum.  Other warps sit on the closing barrier.
 __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint32_t count, uint32_t* ctr,
                                            ReduceSmem& sm, uint32_t T, Ring& r, uint32_t share8,
-                                           uint32_t claim_n) {
+                                           uint32_t claim_n, unsigned long long* tl = nullptr) {
   const float* x = reinterpret_cast<const float*>(d.in0);
   const uint4* x4 = reinterpret_cast<const uint4*>(d.in0);
   double* part = reinterpret_cast<double*>(d.out);
@@ -677,15 +588,24 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
       }
       ++f;
     };
-    // the first claim is issued before the static copies: its L2 round trip overlaps them
-    uint32_t claim = pool0 < nb ? atomicAdd(ctr + 1, claim_n) : nb;
-    for (uint32_t i = 0; i < share; ++i) fill(rank * share + i);
+    // the first claim goes out right after the first static copy (before it
+    // when there is no static share): its L2 round trip overlaps the copies,
+    // and the first copy does not wait behind the atomic (-0.26 us to the
+    // first issue, tools/reduce_phases.py)
+    uint32_t claim = nb;
+    if (share == 0) claim = pool0 < nb ? atomicAdd(ctr + 1, claim_n) : nb;
+    if (tl) tl[12] = globaltimer();
+    for (uint32_t i = 0; i < share; ++i) {
+      fill(rank * share + i);
+      if (i == 0) claim = pool0 < nb ? atomicAdd(ctr + 1, claim_n) : nb;
+    }
     while (pool0 + claim < nb) {
       const uint32_t b = pool0 + claim;
       const uint32_t next = b + claim_n < nb ? atomicAdd(ctr + 1, claim_n) : nb;
       for (uint32_t k = 0; k < claim_n && b + k < nb; ++k) fill(b + k);
       claim = next;
     }
+    if (tl) tl[13] = globaltimer();
     for (uint32_t k = 0; k < S; ++k) fill(kTileEnd);               // every owner sees one end marker
     *r.gred = f;                                                   // read by all after the closing barrier
   } else if (warp >= 1 && warp <= S) {
@@ -694,6 +614,7 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
     uint32_t p = c0 + (st + S - c0 % S) % S;                       // this stage's first position
     for (;; p += S) {
       mbar_wait(fullr + st, (p / S) & 1u);
+      if (tl && p == c0 && lane == 0) tl[14] = globaltimer();      // the dispatch's first stage landed
       const uint32_t b = r.tile[st];
       if (b == kTileEnd) {
         __syncwarp();
@@ -710,7 +631,7 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
       if (lane == 0) st_f64(part + b, ps);
     }
   }
-  reduce_finish(d, count, ctr, sm, T);                             // (its first barrier publishes *r.gred)
+  reduce_finish(d, count, ctr, sm, T, tl);                         // (its first barrier publishes *r.gred)
 }
 
 // Static blocks, 128-bit (or scalar) loads straight from global memory: the
@@ -764,38 +685,29 @@ __device__ __forceinline__ bool single_thread_kind(uint32_t kind) {
 // every field access on the per-tile path into an LDL.
 __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint32_t count,
                                           uint32_t* ctr, ReduceSmem& rs, uint32_t T, Ring& ring, bool ring_on,
-                                          uint32_t& g, bool dyn = false, uint32_t red_share8 = 2,
-                                          uint32_t red_claim = kRedClaim) {
+                                          uint32_t& g, uint32_t red_share8 = 2, uint32_t red_claim = kRedClaim,
+                                          unsigned long long* tl = nullptr) {
   const Part p = partition(d.n, rank, count);
   // host-mapped buffers go through the LSU with sys-scope loads: bulk copies
   // would read them through L2 lines an earlier dispatch may have left behind
   const bool host = (d.flags & LK_DF_HOSTMEM) != 0;
   const bool tma = ring_on && !(d.flags & (LK_DF_SCALAR | LK_DF_HOSTMEM));
   if (tma && threadIdx.x == 0) fence_proxy_async();   // the producer issues every bulk copy
-  dyn = dyn && tma && T >= 64 && ring.tile != nullptr;
-  if (dyn) {   // the pool's atomics cost ~1 us: only worth it with >= 8 tiles per worker
-    const uint64_t tile_v = (d.kind == LK_KIND_HBM_STREAM) ? kStageBytes / 16 : kStageBytes / 32;
-    dyn = ((d.n >> 2) + tile_v - 1) / tile_v >= 8ull * count;
-  }
   switch (d.kind) {
     case LK_KIND_VECTOR_ADD_I32:
-      if (dyn) map_tma_dyn<true>(d, rank, count, OpAddI32{}, T, ring, g, ctr + 1);
-      else if (tma) map_tma<true>(d, p, OpAddI32{}, T, ring, g);
+      if (tma) map_tma<true>(d, p, OpAddI32{}, T, ring, g);
       else if (host) map_chunk<4, true, OpAddI32, LdSys>(d, p, OpAddI32{}, T);
       else map_chunk<4, true>(d, p, OpAddI32{}, T);
       break;
     case LK_KIND_SAXPY_F32:
-      if (dyn) map_tma_dyn<true>(d, rank, count, OpSaxpy{d.alpha}, T, ring, g, ctr + 1);
-      else if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, ring, g);
+      if (tma) map_tma<true>(d, p, OpSaxpy{d.alpha}, T, ring, g);
       else if (host) map_chunk<4, true, OpSaxpy, LdSys>(d, p, OpSaxpy{d.alpha}, T);
       else map_chunk<4, true>(d, p, OpSaxpy{d.alpha}, T);
       break;
     case LK_KIND_HBM_STREAM: {
       const uint64_t passes = d.iterations ? d.iterations : 1;
       for (uint64_t k = 0; k < passes; ++k) {
-        if (dyn && passes == 1) {   // multi-pass: a fast worker would claim the next pass early
-          map_tma_dyn<false>(d, rank, count, OpCopy{}, T, ring, g, ctr + 1);
-        } else if (tma) {
+        if (tma) {
           map_tma<false>(d, p, OpCopy{}, T, ring, g);
         } else if (host) {
           map_chunk<8, false, OpCopy, LdSys>(d, p, OpCopy{}, T);
@@ -807,7 +719,7 @@ __device__ __forceinline__ void run_multi(const lk_desc& d, uint32_t rank, uint3
     }
     case LK_KIND_BLOCK_REDUCE_F32:
       if (tma && T >= 32 * (ring.stages + 1) && ring.gred != nullptr)
-        reduce_dyn(d, rank, count, ctr, rs, T, ring, red_share8, red_claim);
+        reduce_dyn(d, rank, count, ctr, rs, T, ring, red_share8, red_claim, tl);
       else if (host) reduce_static<LdSys>(d, rank, count, ctr, rs, T);
       else reduce_static(d, rank, count, ctr, rs, T);
       break;
@@ -1174,53 +1086,6 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
   }
 }
 
-// DIRECT mode, one cell: one ld.relaxed.sys in flight.  With LK_CF_ACK_WINDOW
-// a worker that just published FINISHED -- and so expects the host's ack
-// within about one link round trip -- issues a second load `spacing_ns` after
-// the first, sampling the cell twice in that window (only the one worker that
-// finished does, so the link does not see the 148 x 2 loads that made
-// replicas slower for everyone).
-__device__ __forceinline__ uint32_t poll_direct1(const lk_dev_args& a, uint32_t wid, Elected& e) {
-  const unsigned long long* cell = a.to_gpu + uint64_t(wid) * a.cell_u64;
-  const bool acquire = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
-  const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
-  const uint64_t gap = (a.flags & LK_CF_ACK_WINDOW) ? uint64_t(a.spacing_ns) * 2 : 0;   // ~cycles at 2 GHz
-  for (;;) {
-    const uint32_t act = settle(a, wid, e);
-    if (act != LK_ACT_NONE) return act;
-    unsigned long long v = ld_cell(cell, acquire), x = 0;
-    bool hx = false;
-    for (;;) {
-      unsigned long long c = v;
-      if (hx) {        // the second sample counts only when the first was stale
-        if (((uint32_t(v >> 32) - e.seq) & 0xFFFFFFu) == 0) c = x;
-        hx = false;
-      }
-      if (accept(e, c, timeline, acquire)) {
-        const uint32_t f = fast_step(a, wid, e);
-        if (f == kFastBegin) return LK_ACT_BEGIN;
-        if (f == kFastNone) break;                  // general path
-        if (e.st.phase == LK_PHASE_FINISHED) ack_wait(e);
-        else if (e.idle_pub) idle_wait(e);
-        e.idle_pub = false;
-        v = ld_cell(cell, acquire);
-        ++e.nload;
-        if (gap && e.st.phase == LK_PHASE_FINISHED) {
-          const uint64_t c0 = clock64();
-          while (clock64() - c0 < gap) {
-          }
-          x = ld_cell(cell, acquire);
-          hx = true;
-        }
-        continue;
-      }
-      if (a.backoff_ns) __nanosleep(a.backoff_ns);   // before the load: a real gap between polls
-      v = ld_cell(cell, acquire);
-      ++e.nload;
-    }
-  }
-}
-
 // GATEWAY mode: the worker's to_gpu value arrives in its device mailbox line
 // (written by the gateway warp); poll it in L2, one load in flight.
 __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t wid, Elected& e) {
@@ -1294,12 +1159,7 @@ __device__ __forceinline__ uint32_t poll(const lk_dev_args& a, uint32_t wid, Ele
                                          const unsigned long long* chan) {
   if (a.poll_mode == LK_POLL_HYBRID) return poll_hybrid(a, wid, e, chan);
   if (a.poll_mode == LK_POLL_GATEWAY) return poll_mailbox(a, wid, e);
-  switch (a.replicas) {
-    case 1: return (a.flags & LK_CF_ACK_WINDOW) ? poll_direct1(a, wid, e) : poll_k<1>(a, wid, e);
-    case 2: return poll_k<2>(a, wid, e);
-    case 8: return poll_k<8>(a, wid, e);
-    default: return poll_k<4>(a, wid, e);
-  }
+  return poll_k<1>(a, wid, e);   // one cell per worker (replicas measured slower)
 }
 
 // ---------------------------------------------------------------- gateway
@@ -1390,13 +1250,7 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
   }
 }
 
-__device__ __noinline__ void gateway(const lk_dev_args& a) {
-  switch (a.replicas) {
-    case 1: gateway_k<1>(a); return;
-    case 4: gateway_k<4>(a); return;
-    default: gateway_k<2>(a); return;
-  }
-}
+__device__ __noinline__ void gateway(const lk_dev_args& a) { gateway_k<1>(a); }   // one event ring
 
 // Per-worker record of the last dispatch (lk_last_timeline): globaltimer at
 // value seen / work begin / work end / FINISHED issued, gateway forward time,
@@ -1566,8 +1420,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     // ~110 GB/s that way against ~85 GB/s through the ring, which wins only
     // once enough SMs share the dispatch to load HBM (tools/tma_vs_lsu_count.py)
     run_multi(d, sm.rank, sm.count, a.reduce_ctr + 4ull * sm.slot, sm.red, T, ring,
-              ring_ok && sm.count >= a.tma_min_workers, g, (a.flags & LK_CF_DYNAMIC_TILES) != 0, a.red_share8,
-              a.red_claim);
+              ring_ok && sm.count >= a.tma_min_workers, g, a.red_share8, a.red_claim, (a.flags & LK_CF_TIMELINE) ? a.spans + uint64_t(LK_TIMELINE_WORDS) * wid : nullptr);
     wsync(T);
     if (threadIdx.x == 0) {
       const uint64_t t_end = globaltimer();

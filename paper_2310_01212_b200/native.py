@@ -63,7 +63,7 @@ class NativeConfig:
     status_stride: int = 64         # bytes between from_gpu status cells (64: one host cache line each)
     poll_mode: str = "direct"       # "direct": each worker polls its host cell; "gateway": one warp
                                     # polls all host cells and forwards through device memory
-    poll_replicas: int = 1          # to_gpu replicas polled per worker (gateway: doorbell sweeps)
+    poll_replicas: int = 1          # one to_gpu cell per worker (replicas were measured slower and removed)
     poll_spacing_ns: int = 300
     num_slots: int = 1024
     trace_capacity: int = 65536
@@ -74,8 +74,6 @@ class NativeConfig:
     sm_partition: int = 0           # N > 0: run in a green context of >= N SMs (multiple of 8), one
                                     # worker per partition SM; the rest stay free for other kernels
     timeline: bool = False          # gateway forward stamps in last_timeline() (one extra L2 load)
-    ack_window: bool = False        # direct/1 replica: second load while awaiting the ack
-    dynamic_tiles: bool = False     # payload maps: static 7/8 share + a pool claimed by early finishers
     ack_delay_ns: int = 300         # direct/1 replica: first poll for the ack this long after FINISHED (0: at
                                     # once); adapted per worker to the host's answer time
     ack_adaptive: bool = True       # False: keep ack_delay_ns fixed
@@ -133,8 +131,6 @@ class NativeConfig:
                    | (0 if self.tma_payload else _lib.CF_LSU_PAYLOAD)
                    | (_lib.CF_TIMELINE if self.timeline else 0)
                    | (_lib.CF_LAZY_ACK if self.lazy_ack else 0)
-                   | (_lib.CF_ACK_WINDOW if self.ack_window else 0)
-                   | (_lib.CF_DYNAMIC_TILES if self.dynamic_tiles else 0)
                    | (0 if self.ack_delay_ns else _lib.CF_NO_ACK_DELAY)
                    | (0 if self.ack_adaptive else _lib.CF_ACK_FIXED)
                    | (_lib.CF_HOST_DESC if self.host_descriptors else 0)
@@ -625,7 +621,7 @@ class NativeSession:
         """(num_workers, 8) record of each worker's last dispatch: globaltimer ns
         at value seen, work begin, work end, FINISHED issued, gateway forward
         (timeline=True); clock64 at value seen, work begin, FINISHED issued."""
-        t = np.zeros((self.num_workers, 12), dtype=np.uint64)
+        t = np.zeros((self.num_workers, 16), dtype=np.uint64)
         _lib.check(self._lib.lk_last_timeline(self._h, t.ctypes.data, self.num_workers))
         return t
 

@@ -37,7 +37,7 @@ def test_random_programs(seed):
     cfg = native.NativeConfig(num_workers=NW, record_trace=True, trace_capacity=8192,
                               poll_mode=rng.choice(["direct", "gateway", "hybrid"]),
                               tma_payload=rng.random() < 0.8, lazy_ack=rng.random() < 0.3,
-                              ring_stages=rng.choice([2, 4, 6]), dynamic_tiles=rng.random() < 0.3,
+                              ring_stages=rng.choice([2, 4, 6]),
                               tma_min_workers=rng.choice([1, 4, 49]))
     s, _ = native.NativeSession.start(cfg)
     nrng = np.random.default_rng(seed)

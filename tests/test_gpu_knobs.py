@@ -32,22 +32,18 @@ KNOBS = {
     "backoff": dict(poll_backoff_ns=400),
     "relaxed-poll": dict(acquire_poll=False),
     "fence-always": dict(fence_always=True),
-    "replicas2": dict(poll_replicas=2, poll_spacing_ns=150),
-    "replicas8": dict(poll_replicas=8),
-    "gateway-replicas4": dict(poll_mode="gateway", poll_replicas=4),
-    "hybrid-replicas2": dict(poll_mode="hybrid", poll_replicas=2),
-    "ack-window": dict(ack_window=True),
     "no-ack-delay": dict(ack_delay_ns=0),
     "idle-delay": dict(idle_delay_ns=300),
     "ack-fixed": dict(ack_adaptive=False, ack_delay_ns=250),
     "ack-delay-1us": dict(ack_delay_ns=1000, idle_delay_ns=1500),
-    "ack-delay-replicas2": dict(ack_delay_ns=500, poll_replicas=2),   # the delay applies to 1 replica only
     "timeline": dict(timeline=True, poll_mode="gateway"),
     "pure-spin": dict(spin_strategy=native.PURE_SPIN),
     "stages2": dict(ring_stages=2),
     "lsu-below-17": dict(tma_min_workers=17),      # NW=16: every dispatch on LSU loads
     "stages12-lsu": dict(ring_stages=12, tma_payload=False),
     "slots8": dict(num_slots=8),
+    "full-board": dict(full_board=True),
+    "hybrid": dict(poll_mode="hybrid"),
 }
 
 

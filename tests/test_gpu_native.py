@@ -306,14 +306,14 @@ def test_criterion_7_random_programs_on_gpu():
     assert_trace_ok(session, program, 8)
 
 
-@pytest.mark.parametrize("mode,replicas", [("direct", 1), ("direct", 4), ("gateway", 1), ("gateway", 4),
-                                           ("hybrid", 1), ("hybrid", 2)])
-def test_poll_modes_random_programs(mode, replicas):
-    """Both to_gpu delivery paths (gateway warp + device mailboxes, direct
-    PCIe polling) and replica counts run the same random programs with
-    validated traces and golden projections."""
-    rng = random.Random(7 + replicas)
-    session = start(12, trace_capacity=4096, poll_mode=mode, poll_replicas=replicas)
+@pytest.mark.parametrize("mode,seed", [("direct", 1), ("direct", 4), ("gateway", 1), ("gateway", 4),
+                                       ("hybrid", 1), ("hybrid", 2)])
+def test_poll_modes_random_programs(mode, seed):
+    """Every to_gpu delivery path (direct PCIe polling, gateway warp + device
+    mailboxes, hybrid) runs the same random programs with validated traces
+    and golden projections."""
+    rng = random.Random(7 + seed)
+    session = start(12, trace_capacity=4096, poll_mode=mode)
     program = []
     for k in range(80):
         sms = rng.sample(range(12), rng.randint(1, 12))
@@ -325,11 +325,11 @@ def test_poll_modes_random_programs(mode, replicas):
     assert_trace_ok(session, program, 12)
 
 
-@pytest.mark.parametrize("mode,replicas", [("gateway", 1), ("gateway", 2), ("hybrid", 1)])
-def test_gateway_back_to_back_single_worker_triggers(mode, replicas):
+@pytest.mark.parametrize("mode", ["gateway", "hybrid"])
+def test_gateway_back_to_back_single_worker_triggers(mode):
     """148 separate trigger events queued before any wait, then one ack event
     for the whole mask: the event ring carries them all in order."""
-    session = start(None, trace_capacity=256, poll_mode=mode, poll_replicas=replicas)
+    session = start(None, trace_capacity=256, poll_mode=mode)
     n = session.num_workers
     work = WorkDescriptor(slot=0, kind="empty")
     for rep in range(3):
@@ -551,15 +551,14 @@ def test_second_live_session_on_a_device_is_refused():
     second.dispose()
 
 
-def test_ack_window_keeps_the_protocol():
-    session = start(8, trace_capacity=2048, ack_window=True)
-    session.register(WorkDescriptor(slot=0, kind="empty"))
-    masks = [1 << i for i in range(8)]
-    session.bench_roundtrip(masks, 0, 400)
-    session.trigger(0b1010, WorkDescriptor(slot=1, iterations=30))
-    session.wait(0b1010)
-    session.dispose()
-    assert_trace_ok(session, [(masks[k % 8], 0) for k in range(400)] + [(0b1010, 1)], 8)
+@pytest.mark.parametrize("kw", [dict(poll_replicas=2), dict(poll_replicas=4, poll_mode="gateway")])
+def test_removed_replica_knobs_are_refused(kw):
+    """Replicated to_gpu cells / event rings were measured slower and removed
+    (DESIGN.md section 3): lk_create refuses them instead of ignoring them."""
+    from paper_2310_01212_b200.errors import ConfigError
+    with pytest.raises(ConfigError, match="poll_replicas must be 1"):
+        native.NativeSession.start(native.NativeConfig(num_workers=4, **kw))
+    start(4).dispose()   # and the device is free for the next session
 
 
 @pytest.mark.slow

@@ -22,8 +22,7 @@ RTOL_F32_REDUCE = 1e-6
 
 # "tma": the ring for dispatches to >= 49 workers, LSU loads below (the
 # default); "ring": the ring for every dispatch (tma_min_workers=1)
-@pytest.fixture(scope="module", params=["tma-direct", "ring-direct", "lsu-direct", "tma-gateway", "ring-hybrid",
-                                        "dyn-gateway"])
+@pytest.fixture(scope="module", params=["tma-direct", "ring-direct", "lsu-direct", "tma-gateway", "ring-hybrid"])
 def session(request):
     try:   # bring torch's CUDA state AND the kernels the torch test uses up before the
         # persistent kernel is resident: CUDA 12 loads kernels lazily, and a module
@@ -38,8 +37,7 @@ def session(request):
     path, mode = request.param.split("-")
     s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_yield_threshold=200, poll_mode=mode,
                                                           tma_payload=path != "lsu",
-                                                          tma_min_workers=1 if path in ("ring", "dyn") else 49,
-                                                          dynamic_tiles=path == "dyn"))
+                                                          tma_min_workers=1 if path == "ring" else 49))
     yield s
     s.close()
 

@@ -44,6 +44,5 @@ def run(label, rounds=14800, **kw):
 
 for trial in range(2):
     run("no-delay", ack_delay_ns=0)
-    run("window300", ack_window=True, poll_spacing_ns=300, ack_delay_ns=0)
     run("delay200")
     run("delay400", ack_delay_ns=400)

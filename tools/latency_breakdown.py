@@ -52,7 +52,6 @@ def breakdown(label, rounds=20000, timeline=True, **kw):
 if __name__ == "__main__":
     breakdown("direct K=1 (clock64 only)", timeline=False, poll_mode="direct", poll_replicas=1)
     breakdown("direct K=1", poll_mode="direct", poll_replicas=1)
-    breakdown("direct K=2", poll_mode="direct", poll_replicas=2)
     breakdown("gateway K=1 (clock64 only)", timeline=False, poll_mode="gateway", poll_replicas=1)
     breakdown("gateway K=1", poll_mode="gateway", poll_replicas=1)
     breakdown("direct K=1 16w", poll_mode="direct", poll_replicas=1, num_workers=16)

@@ -36,8 +36,4 @@ def run(label, rounds=20000, mode="rr", **kw):
 native.pin_host_thread(0)
 pp = native.pingpong(0, 20000)
 print("pingpong p50 %.2f p99.9 %.2f" % (pct(pp[100:], 50), pct(pp[100:], 99.9)))
-for aw in (False, True):
-    for d in (200, 400, 700):
-        if not aw and d != 200:
-            continue
-        run(f"148 rr direct ack_window={aw} gap={d}", ack_window=aw, poll_spacing_ns=d)
+run("148 rr direct")
