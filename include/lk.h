@@ -163,8 +163,10 @@ typedef struct lk_config {
 #define LK_POLL_HYBRID  2u
 #define LK_HYBRID_DIRECT_MAX 8u
 
-#define LK_CF_ACQUIRE_POLL   1u  /* (the default; kept for ABI compatibility) every poll of a to_gpu cell or
-                                    event-ring entry is ld.acquire.sys, mailbox polls ld.acquire.gpu */
+#define LK_CF_ACQUIRE_POLL   1u  /* (the default; kept for ABI compatibility) DIRECT polls of a to_gpu
+                                    cell are ld.acquire.sys.  The gateway's ring and the mailboxes are
+                                    polled relaxed (acquire loads there cost 1.2 us per wide dispatch);
+                                    host-mapped payloads get explicit fences on that path */
 #define LK_CF_RELAXED_POLL 2048u /* polls with ld.relaxed.sys / .gpu instead; a host-mapped payload
                                     (LK_HINT_SYSMEM) then costs a fence.acq_rel.sys (~1.5 us) */
 #define LK_CF_FENCE_ALWAYS   2u  /* release fence before every FINISHED, even for no-write kinds */

@@ -73,11 +73,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu64(const unsigned lo
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint32_t ld_relaxed_gpu32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -789,25 +784,30 @@ __device__ __forceinline__ unsigned long long ld_cell(const unsigned long long* 
 }
 
 // The host wrote a host-mapped payload's inputs before the WORK value that
-// names it (release on the host side).  A poll with ld.acquire.sys
-// (LK_CF_ACQUIRE_POLL; LDG.STRONG.SYS + CCTL.IVALL, no membar) is already the
-// acquire the payload's loads are ordered behind.  A relaxed poll, or a value
-// forwarded through the gateway or a channel poller, gets a sys-scope fence
-// after it instead (LK_HINT_SYSMEM only: MEMBAR.SYS costs ~1.5 us).
+// names it (release on the host side).  A DIRECT poll with ld.acquire.sys
+// (LK_CF_ACQUIRE_POLL, the default; LDG.STRONG.SYS + CCTL.IVALL, no membar)
+// is already the acquire the payload's loads are ordered behind.  A relaxed
+// poll or a channel poller's value gets a sys-scope fence after it instead,
+// a value forwarded by the gateway (which fenced at sys scope) a gpu-scope
+// one (LK_HINT_SYSMEM only: MEMBAR.SYS costs ~1.5 us).
 __device__ __forceinline__ void acquire_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 // A to_gpu value is {word:32, seq:24, hint:8}; seq is the host's per-worker
 // write index mod 2^24 (serial-number compare: a worker is never 2^23 writes
 // behind, every write waits on its handshake) and is widened back to 32 bits
 // here, so trace records carry the host's full write index.
-__device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool timeline, bool acquired = false) {
+__device__ __forceinline__ bool accept(Elected& e, unsigned long long c, bool timeline, bool acquired = false,
+                                       bool via_gateway = false) {
   const uint32_t sq = uint32_t(c >> 32) & 0xFFFFFFu;
   const uint32_t delta = (sq - e.seq) & 0xFFFFFFu;
   if (delta == 0 || delta >= 0x800000u) return false;
   e.seq += delta;
   e.cur = uint32_t(c);
   e.hint = uint32_t(c >> 56);
-  if ((e.hint & LK_HINT_SYSMEM) && !acquired) acquire_sys();
+  if ((e.hint & LK_HINT_SYSMEM) && !acquired) {
+    if (via_gateway) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    else acquire_sys();
+  }
   e.dirty = true;
   e.c_seen = clock64();
   if (timeline) e.t_seen = globaltimer();
@@ -1091,12 +1091,11 @@ __device__ __forceinline__ uint32_t poll_k(const lk_dev_args& a, uint32_t wid, E
 __device__ __forceinline__ uint32_t poll_mailbox(const lk_dev_args& a, uint32_t wid, Elected& e) {
   const unsigned long long* mb = a.dmb + uint64_t(wid) * a.dmb_u64;
   const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
-  const bool acq = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
   for (;;) {
     const uint32_t act = settle(a, wid, e);
     if (act != LK_ACT_NONE) return act;
     for (;;) {
-      if (accept(e, acq ? ld_acquire_gpu64(mb) : ld_relaxed_gpu64(mb), timeline, acq)) {
+      if (accept(e, ld_relaxed_gpu64(mb), timeline, false, true)) {
         if (timeline) e.t_fwd = ld_relaxed_gpu64(mb + 1);
         const uint32_t f = fast_step(a, wid, e);
         if (f == kFastBegin) return LK_ACT_BEGIN;
@@ -1186,7 +1185,6 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = a.nw, N = a.ring_entries;
   const bool timeline = (a.flags & LK_CF_TIMELINE) != 0;
-  const bool acq = (a.flags & LK_CF_ACQUIRE_POLL) != 0;
   uint32_t wseq[6];                               // per-worker write counts, workers lane + 32q
 #pragma unroll
   for (int q = 0; q < 6; ++q) wseq[q] = 0;
@@ -1194,7 +1192,7 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
   unsigned long long v[K];
   auto issue = [&](int k) {
     if (lane < 6)
-      v[k] = ld_cell(a.ring + (uint64_t(k) * N + (expect - 1) % N) * 8 + lane, acq);
+      v[k] = ld_cell(a.ring + (uint64_t(k) * N + (expect - 1) % N) * 8 + lane, false);
   };
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -1213,13 +1211,12 @@ __device__ __forceinline__ void gateway_k(const lk_dev_args& a) {
       if (__all_sync(0xffffffffu, mine)) {
         const uint32_t word = uint32_t(w0 >> 32);
         const uint32_t hint = uint32_t(__shfl_sync(0xffffffffu, w, 5)) & 0xFFu;
-        // a host-mapped payload: the entry's acquire load synchronised with the
-        // host's release; a gpu-scope release fence before the forwarding
-        // stores passes it on to the workers' acquire polls of their mailboxes
-        if (hint & LK_HINT_SYSMEM) {
-          if (acq) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          else acquire_sys();
-        }
+        // a host-mapped payload: the sys-scope fence makes the entry's load
+        // the acquire of the host's release, and releases the forwarding
+        // stores after it; the worker's gpu-scope fence completes the chain
+        // (the ring is polled relaxed: acquire loads here and on the
+        // mailboxes cost 1.2 us per full-mask dispatch, tools/ab_wide.py)
+        if (hint & LK_HINT_SYSMEM) acquire_sys();
         // the four 48-bit mask words stay in registers: a runtime index into
         // an array would put it in local memory
         const unsigned long long mm = (1ull << kRingMaskBits) - 1;
