@@ -4,7 +4,7 @@ begin skew, begin -> first bulk copy issued, issue -> first data, the
 slowest worker's arrival, and the last worker's combine."""
 import sys
 
-sys.path.insert(0, ".")
+sys.path.insert(0, ".") if "paper_2310_01212_b200" not in sys.modules else None
 import numpy as np  # noqa: E402
 
 from paper_2310_01212_b200 import host, native  # noqa: E402
