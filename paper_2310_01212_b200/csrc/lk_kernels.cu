@@ -660,12 +660,35 @@ __device__ __forceinline__ void reduce_static(const lk_desc& d, uint32_t rank, u
 // copies were unrolled differently per site (2x apart in time per
 // iteration).
 __device__ __noinline__ uint32_t busy_loop(uint64_t iterations) {
+  // One PTX loop (a dependent 32-bit LCG step per iteration) so that ptxas
+  // emits the same SASS wherever it is compiled.  As C++ reading %clock, the
+  // two kernels' copies were unrolled and scheduled differently and an
+  // iteration cost 20 cycles in the persistent kernel against 26 in
+  // lk_work_kernel; S2UR's latency also varied with its neighbours
+  // (tools/busy_spans.py).  The caller stores the result, so the loop runs.
+  // The counter runs from the lane id to iterations + lane id (the same trip
+  // count), which keeps ptxas from moving the loop onto the uniform datapath
+  // in one kernel and not the other.
   uint32_t acc = 0;
-  for (uint64_t i = 0; i < iterations; ++i) {
-    uint32_t c;
-    asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
-    acc ^= c;
-  }
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      ".reg .u64 i, e;\n\t"
+      ".reg .u32 l;\n\t"
+      "mov.u32 l, %%laneid;\n\t"
+      "cvt.u64.u32 i, l;\n\t"
+      "add.u64 e, %1, i;\n"
+      "LK_BUSY_%=:\n\t"
+      "setp.ge.u64 p, i, e;\n\t"
+      "@p bra.uni LK_BUSY_DONE_%=;\n\t"
+      "mad.lo.u32 %0, %0, 1664525, 1013904223;\n\t"
+      "add.u64 i, i, 1;\n\t"
+      "bra.uni LK_BUSY_%=;\n"
+      "LK_BUSY_DONE_%=:\n\t"
+      "}"
+      : "+r"(acc)
+      : "l"(iterations)
+      : "memory");
   return acc;
 }
 
