@@ -124,7 +124,7 @@ typedef struct lk_config {
                                     and removed) */
   uint32_t poll_spacing_ns;      /* unused since replicas were removed (kept for the ABI) */
   uint32_t poll_mode;            /* LK_POLL_DIRECT (0, default), LK_POLL_GATEWAY or LK_POLL_HYBRID */
-  uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 64 */
+  uint32_t status_stride;        /* bytes between from_gpu status cells: 16..128 (power of 2); 0 = 32 */
   uint32_t ring_stages;          /* TMA payload ring depth in 16-KiB stages, 2..12; 0 = 6 */
   uint32_t sm_partition;         /* 0: the persistent kernel spans the GPU.  N: it runs in a green
                                     context of >= N SMs (driver granularity: multiples of 8), one

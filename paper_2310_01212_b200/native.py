@@ -60,7 +60,7 @@ class NativeConfig:
     threads_per_worker: int = 512
     poll_backoff_ns: int = 0
     cell_stride: int = 128          # bytes between to_gpu cells
-    status_stride: int = 64         # bytes between from_gpu status cells (64: one host cache line each)
+    status_stride: int = 32         # bytes between from_gpu status cells (32: two workers per host line)
     poll_mode: str = "direct"       # "direct": each worker polls its host cell; "gateway": one warp
                                     # polls all host cells and forwards through device memory
     poll_replicas: int = 1          # one to_gpu cell per worker (replicas were measured slower and removed)
