@@ -510,7 +510,8 @@ def run_threads_arm(args):
 
 METRIC = "trigger->done round trips per second (empty task, 148 persistent workers)"
 # extras printed at the end of the JSON line, next to the latency headline
-HEADLINE_EXTRAS = ("single_worker", "full_mask", "interference", "interference_green", "pingpong_floor",
+HEADLINE_EXTRAS = ("single_worker", "full_mask", "full_mask_gateway", "interference", "interference_green",
+                   "pingpong_floor",
                    "tail_attribution")
 
 
@@ -1133,6 +1134,14 @@ def run_lk_arm(args, world, rank, local):
         # the reduce's span; at 1 GiB they vanish
         payload["block_reduce_f32_steady"] = measure_payload(psession, "block_reduce_f32", [1024], 6,
                                                              2 * L2_BYTES)
+        # the empty full-mask dispatch on this GATEWAY session (one ring
+        # event per write), beside the DIRECT session's full_mask above
+        psession.register(WorkDescriptor(slot=0, kind="empty"))
+        pfull = host.full_mask(psession.num_workers)
+        psession.bench_roundtrip([pfull], 0, 2000)
+        _, gdone, gcyc = psession.bench_roundtrip([pfull], 0, args.full_rounds)
+        extras["full_mask_gateway"] = {"trigger_to_done": lat_summary(gdone), "round_trip": lat_summary(gcyc),
+                                       "tasks_per_s": round(args.full_rounds / (gcyc.sum() / 1e9), 1)}
         psession.dispose()
         psession.close()
 
