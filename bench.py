@@ -1093,6 +1093,14 @@ def run_lk_arm(args, world, rank, local):
     e2e_t, e2e_units = gather_max_sum(world, e2e_dt, e2e_rounds)
     e2e_value = e2e_units / e2e_t          # whole job: all ranks' tasks / slowest rank
 
+    # 64 MiB saxpy on this DIRECT session too: its per-worker early acks make
+    # the wide handshake cheaper end to end, the gateway's single ring event
+    # makes the start skew (and so the device span) smaller
+    if rank == 0 and not args.no_payload:
+        extras["payload_direct"] = {"saxpy_f32": measure_payload(session, "saxpy_f32", [64], args.payload_reps,
+                                                                 4 * L2_BYTES),
+                                    "poll_mode": "direct"}
+
     # configs[0] shape on the GPU: 4 workers round robin, int32 vector add of 64 Ki
     # elements per task (the CPU reference's workload), trigger->done per task
     if rank == 0 and not args.no_payload:
