@@ -510,7 +510,7 @@ def run_threads_arm(args):
 
 METRIC = "trigger->done round trips per second (empty task, 148 persistent workers)"
 # extras printed at the end of the JSON line, next to the latency headline
-HEADLINE_EXTRAS = ("single_worker", "full_mask", "full_mask_gateway", "interference", "interference_green",
+HEADLINE_EXTRAS = ("single_worker", "full_mask", "full_mask_payload_session", "interference", "interference_green",
                    "pingpong_floor",
                    "tail_attribution")
 
@@ -1124,10 +1124,11 @@ def run_lk_arm(args, world, rank, local):
     if rank == 0 and not args.no_lazy:
         extras["lazy_ack"] = measure_lazy(cfg, rr_masks, args.lazy_rounds)
 
-    # configs[2]: payload items dispatched to every worker.  Multi-worker
-    # dispatch runs on a GATEWAY-mode session (one ring event reaches all 148
-    # workers within ~0.5 us; direct polling spreads their start over ~2 us,
-    # which the span -- and so the GB/s -- would include at small sizes).
+    # configs[2]: payload items dispatched to every worker, on a HYBRID
+    # session: the trigger is one ring event (it reaches all 148 workers
+    # within ~0.5 us; direct polling spreads their start over ~2 us, which the
+    # span -- and so the GB/s -- would include at small sizes), and the acks
+    # go to the direct cells as each FINISHED is seen.
     payload = {}
     if not args.no_payload and rank == 0:
         pcfg = dataclasses.replace(cfg, poll_mode=args.payload_poll_mode)
@@ -1142,14 +1143,15 @@ def run_lk_arm(args, world, rank, local):
         # the reduce's span; at 1 GiB they vanish
         payload["block_reduce_f32_steady"] = measure_payload(psession, "block_reduce_f32", [1024], 6,
                                                              2 * L2_BYTES)
-        # the empty full-mask dispatch on this GATEWAY session (one ring
-        # event per write), beside the DIRECT session's full_mask above
+        # the empty full-mask dispatch on this session (triggers as one ring
+        # event), beside the DIRECT session's full_mask above
         psession.register(WorkDescriptor(slot=0, kind="empty"))
         pfull = host.full_mask(psession.num_workers)
         psession.bench_roundtrip([pfull], 0, 2000)
         _, gdone, gcyc = psession.bench_roundtrip([pfull], 0, args.full_rounds)
-        extras["full_mask_gateway"] = {"trigger_to_done": lat_summary(gdone), "round_trip": lat_summary(gcyc),
-                                       "tasks_per_s": round(args.full_rounds / (gcyc.sum() / 1e9), 1)}
+        extras["full_mask_payload_session"] = {"poll_mode": args.payload_poll_mode,
+                                               "trigger_to_done": lat_summary(gdone), "round_trip": lat_summary(gcyc),
+                                               "tasks_per_s": round(args.full_rounds / (gcyc.sum() / 1e9), 1)}
         psession.dispose()
         psession.close()
 
@@ -1340,7 +1342,7 @@ def main():
     ap.add_argument("--replicas", type=int, default=1)
     ap.add_argument("--spacing-ns", type=int, default=300)
     ap.add_argument("--lsu-payload", action="store_true", help="payload via 128-bit LSU loads, not the TMA ring")
-    ap.add_argument("--payload-poll-mode", choices=["gateway", "direct", "hybrid"], default="gateway")
+    ap.add_argument("--payload-poll-mode", choices=["gateway", "direct", "hybrid"], default="hybrid")
     ap.add_argument("--interference-poll-mode", choices=["gateway", "direct", "hybrid"], default="hybrid")
     ap.add_argument("--full-rounds", type=int, default=100_000)
     ap.add_argument("--e2e-rounds", type=int, default=100_000)

@@ -1302,10 +1302,12 @@ static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::
   // of them after the last.  Per worker this is the reference's order
   // (FINISHED seen, then NOP written: native.py:256-265); across workers the
   // acks overlap the rest of the scan.  Full-mask cycle 9.6 -> 7.9 us,
-  // trigger->done 5.3 -> 4.9 us (tools/ab_early_ack.py).  Ring-event acks
-  // (gateway, wide hybrid) stay one event for the whole mask.
-  const bool ack_each = ids.size() > 1 && !(s->cfg.flags & LK_CF_FULL_BOARD) &&
-                        (!s->gateway || (s->hybrid && ids.size() <= LK_HYBRID_DIRECT_MAX));
+  // trigger->done 5.3 -> 4.9 us (tools/ab_early_ack.py).  HYBRID sessions
+  // take every ack on the direct cells this way too, wide masks included
+  // (their triggers still travel as one ring event): full-mask cycle 10.4 ->
+  // 9.25 us, 64 MiB saxpy e2e +4% (profiles/r02_ab_hybrid_acks.txt).
+  // GATEWAY acks stay one ring event for the whole mask.
+  const bool ack_each = ids.size() > 1 && !(s->cfg.flags & LK_CF_FULL_BOARD) && (!s->gateway || s->hybrid);
   int rc = spin_words(s, ids, LK_FINISHED, "wait for FINISHED", ack_each);
   if (rc) return rc;
   const uint64_t finished_at = now_ns();
