@@ -1814,7 +1814,11 @@ extern "C" int lk_pingpong(int device, uint64_t rounds, uint64_t* rt_ns) {
   cudaStream_t st;
   LK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   cudaError_t ce = lk_launch_pingpong(flag, echo, rounds, st);
-  if (ce != cudaSuccess) return fail(LK_E_CUDA, "pingpong launch: %s", cudaGetErrorString(ce));
+  if (ce != cudaSuccess) {
+    cudaStreamDestroy(st);
+    free_pinned(cells);
+    return fail(LK_E_CUDA, "pingpong launch: %s", cudaGetErrorString(ce));
+  }
   int rc = LK_OK;
   for (uint64_t r = 1; r <= rounds; ++r) {
     const uint32_t want = uint32_t(r);
@@ -1828,11 +1832,21 @@ extern "C" int lk_pingpong(int device, uint64_t rounds, uint64_t* rt_ns) {
     if (rc) break;
     rt_ns[r - 1] = now_ns() - t0;
   }
-  if (rc == LK_OK) {
-    LK_CUDA(cudaStreamSynchronize(st));
+  if (rc != LK_OK) {
+    // release the kernel: it waits for flag >= round, so the largest value
+    // lets every remaining round through; reclaim everything once it exited
+    __atomic_store_n(flag, 0xFFFFFFFFu, __ATOMIC_RELEASE);
+    const uint64_t until = now_ns() + 1000000000ull;
+    cudaError_t q;
+    while ((q = cudaStreamQuery(st)) == cudaErrorNotReady && now_ns() < until) usleep(100);
+    if (q == cudaErrorNotReady) return rc;   // still resident: it may touch the cells, so they are leaked
     cudaStreamDestroy(st);
     free_pinned(cells);
+    return rc;
   }
+  LK_CUDA(cudaStreamSynchronize(st));
+  cudaStreamDestroy(st);
+  free_pinned(cells);
   return rc;
 }
 
