@@ -101,6 +101,16 @@ class DeviceBuffer:
             pass
 
 
+class _HostView:
+    """Array-interface holder for HostBuffer.array(): as the view's base it
+    keeps the HostBuffer (and so the pinned allocation) referenced."""
+
+    def __init__(self, buf: "HostBuffer", nbytes: int):
+        self.buf = buf
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (buf.ptr, False),
+                                    "version": 3}
+
+
 class HostBuffer:
     """Mapped pinned host memory (``lk_host_alloc``: cudaHostAlloc Mapped |
     Portable) that the persistent workers read and write over the link:
@@ -130,15 +140,15 @@ class HostBuffer:
         return buf
 
     def array(self, dtype, count: Optional[int] = None) -> np.ndarray:
-        """A numpy view of the buffer (no copy)."""
+        """A numpy view of the buffer (no copy).  The view keeps the buffer
+        alive; an explicit ``free()`` invalidates it."""
         if not self.ptr:
             raise UsageError("host buffer freed")
         dt = np.dtype(dtype)
         count = self.nbytes // dt.itemsize if count is None else count
         if count * dt.itemsize > self.nbytes:
             raise UsageError("view larger than the host buffer")
-        raw = (C.c_char * (count * dt.itemsize)).from_address(self.ptr)
-        return np.frombuffer(raw, dtype=dt, count=count)
+        return np.asarray(_HostView(self, count * dt.itemsize)).view(dt)
 
     def upload(self, arr: np.ndarray) -> None:
         a = np.ascontiguousarray(arr)
