@@ -116,7 +116,7 @@ typedef struct lk_config {
   uint32_t record_trace;         /* native.py:51 */
   uint32_t trace_capacity;       /* device records per worker; 0 = 65536 */
   uint32_t poll_backoff_ns;      /* device __nanosleep between idle polls (0 = none) */
-  uint32_t cell_stride;          /* bytes between to_gpu cells / replicas: 8..128 (power of 2); 0 = 128 */
+  uint32_t cell_stride;          /* bytes between to_gpu cells: 8..128 (power of 2); 0 = 128 */
   uint32_t num_slots;            /* descriptor table entries; 0 = 1024 */
   uint64_t wait_timeout_ns;      /* wait_timeout_s (native.py:52) */
   uint32_t flags;                /* LK_CF_* */
@@ -150,14 +150,16 @@ typedef struct lk_config {
 } lk_config;
 
 /* How to_gpu words reach the workers.  DIRECT: every worker polls its own
- * host cell (replicas) over PCIe.  GATEWAY: one warp polls a dense host
- * doorbell array for every worker and forwards new values to per-worker
- * mailboxes in device memory (fewer PCIe reads in flight, one extra L2 hop;
- * measured slower on the B200 hosts, kept as an option). */
+ * host cell over PCIe (lowest single-worker latency).  GATEWAY: one warp
+ * polls an event ring in host memory (one 64-B event per logical write,
+ * carrying the worker mask) and forwards new values to per-worker mailboxes
+ * in device memory: one host store per wide dispatch, one extra L2 hop per
+ * worker. */
 #define LK_POLL_DIRECT  0u
 #define LK_POLL_GATEWAY 1u
 /* HYBRID: writes to at most LK_HYBRID_DIRECT_MAX workers go to their direct
- * cells, wider ones (full-mask triggers, acks, EXIT) as one ring event; each
+ * cells, wider ones (full-mask triggers, EXIT) as one ring event, and every
+ * ack to the direct cells as each FINISHED is seen; each
  * CTA runs a host-cell poller warp and a mailbox poller warp that forward into
  * shared memory, where the protocol thread watches both. */
 #define LK_POLL_HYBRID  2u
