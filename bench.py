@@ -224,6 +224,17 @@ def gather_max_sum(world, t_s, units):
     return float(t.item()), float(u.item())
 
 
+def gather_rank_rows(world, row):
+    """Every rank's small summary dict, on every rank (gloo all_gather_object);
+    [row] at world size 1."""
+    if world == 1:
+        return [row]
+    import torch.distributed as dist
+    rows = [None] * world
+    dist.all_gather_object(rows, row)
+    return rows
+
+
 def aggregate(rank_times, rank_units):
     """Whole-job throughput: total units / slowest rank's time."""
     return sum(rank_units) / max(rank_times)
@@ -1020,6 +1031,11 @@ def run_lk_arm(args, world, rank, local):
     value = units / t_max
     done_all = np.concatenate(done_all)
     cyc_all = np.concatenate(cyc_all)
+    # configs[4]: every GPU's own p50/p99.9 beside the aggregate (rank = GPU)
+    mine = lat_summary(done_all)
+    per_rank = gather_rank_rows(world, {"rank": rank, "device": device, "rounds": int(done_all.size),
+                                        "elapsed_s": round(elapsed, 6), "tasks_per_s": round(rounds / elapsed, 1),
+                                        "p50_us": mine["p50_us"], "p99.9_us": mine["p99.9_us"]})
 
     tl = session.last_timeline().astype(np.int64)
     dev_cyc = (tl[:, 7] - tl[:, 5]).astype(np.float64)
@@ -1310,9 +1326,10 @@ def run_lk_arm(args, world, rank, local):
                 "note": "Python API session.trigger+session.wait per task (the _lkfast CPython path -> liblk.so), "
                         f"{e2e_rounds} tasks; host<->device traffic per task is the mailbox cells "
                         "themselves: WORK + ack down (8 B x replicas each), WORKING/FINISHED/NOP up (8 B each)"},
-        "gpu_launches": 1,
-        "gpu_launch_note": "one persistent kernel resident across the timed region; tasks are "
+        "gpu_launches": world,
+        "gpu_launch_note": "one persistent kernel per GPU resident across the timed region; tasks are "
                            "dispatched by mailbox words, not launches",
+        "per_rank": per_rank,
         "smid_distinct": len(set(smids)),
         "clocks": clk.summary(),
         # headline last: the driver keeps the tail of the line
@@ -1349,7 +1366,7 @@ def main():
     ap.add_argument("--base-rounds", type=int, default=100_000)
     ap.add_argument("--pp-rounds", type=int, default=100_000)
     ap.add_argument("--attrib-rounds", type=int, default=300_000, help="tail-attribution rounds (untimed)")
-    ap.add_argument("--payload-mib", type=int, nargs="+", default=[1, 4, 16, 64])
+    ap.add_argument("--payload-mib", type=int, nargs="+", default=[1, 2, 4, 8, 16, 32, 64])
     ap.add_argument("--payload-reps", type=int, default=30)
     ap.add_argument("--no-payload", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -31,8 +31,9 @@ def _worker(rank, world, port, q):
     import bench
     w, r, _ = bench.dist_setup()
     t, u = bench.gather_max_sum(w, 1.5 + r, 1000 * (r + 1))
+    rows = bench.gather_rank_rows(w, {"rank": r, "p50_us": 2.0 + r})
     bench.barrier(w)
-    q.put((r, t, u))
+    q.put((r, t, u, [row["p50_us"] for row in rows]))
     import torch.distributed as dist
     dist.destroy_process_group()
 
@@ -48,8 +49,9 @@ def test_gather_max_over_ranks_and_sum_of_units():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for _, t, u in out:
+    for _, t, u, p50s in out:
         assert t == 2.5 and u == 3000.0      # slowest rank's time, all ranks' units
+        assert p50s == [2.0, 3.0]            # every rank's row on every rank, in rank order
 
 
 def test_aggregate_is_units_over_slowest_rank():
