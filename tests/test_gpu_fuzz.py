@@ -1,6 +1,7 @@
 """Seeded randomized programs against the B200 session: random poll modes and
 payload paths, overlapping dispatches on disjoint worker sets, partial waits,
-every payload kind at random sizes and masks.  Each result is checked against
+every payload kind at random sizes and masks, about a third of the buffers in
+host-mapped memory (zero-copy).  Each result is checked against
 the oracle and each session's full trace is replayed by the oracle validator
 and checked against the golden per-worker projection."""
 from __future__ import annotations
@@ -14,7 +15,7 @@ from oracle import projection
 from oracle import protocol as O
 from oracle import work as W
 from paper_2310_01212_b200 import host, native
-from paper_2310_01212_b200.device import DeviceBuffer, WorkDescriptor, reduce_blocks
+from paper_2310_01212_b200.device import DeviceBuffer, HostBuffer, WorkDescriptor, reduce_blocks
 
 pytestmark = pytest.mark.gpu
 
@@ -60,6 +61,12 @@ def test_random_programs(seed):
                                    "hbm_stream"])
                 n = rng.choice([1, 5, 32, 1000, 65536 + rng.randrange(100), 300_001])
                 check = None
+                # about a third of the payload buffers are zero-copy host-mapped memory
+                host_side = rng.random() < 0.35
+
+                def mk(arr=None, nbytes=0, host_ok=True):
+                    cls = HostBuffer if (host_side and host_ok) else DeviceBuffer
+                    return cls.from_array(arr) if arr is not None else cls(nbytes)
                 if kind == "empty":
                     w = WorkDescriptor(slot=slot, kind="empty")
                 elif kind == "busy":
@@ -67,7 +74,7 @@ def test_random_programs(seed):
                 elif kind == "vector_add_i32":
                     a = nrng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
                     b = nrng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
-                    da, db, do = DeviceBuffer.from_array(a), DeviceBuffer.from_array(b), DeviceBuffer(4 * n)
+                    da, db, do = mk(a), DeviceBuffer.from_array(b), mk(nbytes=4 * n)
                     bufs += [da, db, do]
                     w = WorkDescriptor(slot=slot, kind=kind, data_in_ref=(da, db), data_out_ref=do)
                     check = lambda do=do, a=a, b=b, n=n: np.testing.assert_array_equal(  # noqa: E731
@@ -75,7 +82,7 @@ def test_random_programs(seed):
                 elif kind == "saxpy_f32":
                     x = nrng.uniform(-1, 1, n).astype(np.float32)
                     y = nrng.uniform(-1, 1, n).astype(np.float32)
-                    dx, dy = DeviceBuffer.from_array(x), DeviceBuffer.from_array(y)
+                    dx, dy = mk(x), mk(y)
                     bufs += [dx, dy]
                     alpha = float(rng.choice([1.5, -0.25, 3.0]))
                     w = WorkDescriptor(slot=slot, kind=kind, data_in_ref=(dx, dy), data_out_ref=dy, alpha=alpha)
@@ -84,7 +91,7 @@ def test_random_programs(seed):
                 elif kind == "block_reduce_f32":
                     x = nrng.integers(0, 8, n).astype(np.float32)
                     nbk = reduce_blocks(n)
-                    dx, dp, dt = DeviceBuffer.from_array(x), DeviceBuffer(8 * nbk), DeviceBuffer(8)
+                    dx, dp, dt = mk(x), DeviceBuffer(8 * nbk), mk(nbytes=8)   # partials: device memory
                     bufs += [dx, dp, dt]
                     w = WorkDescriptor(slot=slot, kind=kind, data_in_ref=dx, data_out_ref=dp, total_ref=dt)
 
@@ -93,7 +100,7 @@ def test_random_programs(seed):
                         assert dt.download(np.float64, 1)[0] == W.block_reduce_total(x)
                 else:
                     src = nrng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
-                    ds, dd = DeviceBuffer.from_array(src), DeviceBuffer(4 * n)
+                    ds, dd = mk(src), mk(nbytes=4 * n, host_ok=rng.random() < 0.5)
                     bufs += [ds, dd]
                     w = WorkDescriptor(slot=slot, kind=kind, data_in_ref=ds, data_out_ref=dd,
                                        iterations=rng.randint(1, 2))
