@@ -7,6 +7,11 @@
   187-223: 10,000 round-robin cycles on 4 workers, zero violations,
   exactly-once, median trigger < median spawn) with only persistkern.native
   replaced: the trace is validated by the REFERENCE's own protocol module.
+* test_bench.py::test_native_backend_scenario_smoke (T/test_bench.py:196-
+  203) on a fresh copy of the reference's own bench.py whose ``native`` is
+  this package: the reference harness's unmodified "native" backend
+  (_run_native_lk / _run_native_baseline, P/bench.py:218-241) drives the
+  B200 session and the launch+sync baseline.
 
 The modules are read from the reference tree when present (build container),
 else from the unmodified copies __graft_entry__.build() stages under
@@ -100,6 +105,46 @@ def test_reference_suite_is_covered(ref_native_tests):
 @pytest.mark.parametrize("name", _NATIVE_TESTS)
 def test_reference_test_native(ref_native_tests, name):
     getattr(ref_native_tests, name)()
+
+
+def _fresh_reference_module(name, aliases):
+    """A new instance of reference module ``persistkern.<name>`` executed with
+    ``aliases`` in sys.modules (so its ``from . import native`` binds this
+    package's native); sys.modules is restored afterwards."""
+    ref = reference_sys_path()
+    if ref is not None and str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import persistkern as real_pkg
+    path = Path(real_pkg.__path__[0]) / f"{name}.py"
+    dotted = f"persistkern.{name}"
+    saved = {k: sys.modules.get(k) for k in [dotted, *aliases]}
+    try:
+        for k, mod in aliases.items():
+            sys.modules[k] = mod
+        spec = importlib.util.spec_from_file_location(dotted, path)
+        module = importlib.util.module_from_spec(spec)
+        module.__package__ = "persistkern"
+        sys.modules[dotted] = module   # dataclasses resolve their module while the class is built
+        spec.loader.exec_module(module)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                sys.modules.pop(k, None)
+            else:
+                sys.modules[k] = v
+    return module
+
+
+def test_reference_bench_native_backend_runs_on_b200():
+    """The reference harness's own native backend, unmodified, on this
+    package: Scenario(backend="native") -> run_scenario -> _run_native_lk /
+    _run_native_baseline; the reference test asserts 5 samples per row and
+    spawn (here: launch+sync) slower than trigger."""
+    ours = _ours()
+    bench = _fresh_reference_module("bench", {"persistkern.native": ours["persistkern.native"]})
+    assert bench.native is ours["persistkern.native"]
+    mod = _load("test_bench.py", {"persistkern.bench": bench})
+    mod.test_native_backend_scenario_smoke()
 
 
 def test_reference_criterion_8_with_reference_validator():
