@@ -19,6 +19,7 @@ oracle/_ref/tests/ (git-ignored; they travel to the GPU box with the repo).
 """
 from __future__ import annotations
 
+import dataclasses
 import importlib.util
 import sys
 import types
@@ -145,6 +146,27 @@ def test_reference_bench_native_backend_runs_on_b200():
     assert bench.native is ours["persistkern.native"]
     mod = _load("test_bench.py", {"persistkern.bench": bench})
     mod.test_native_backend_scenario_smoke()
+
+
+def test_reference_cli_native_backend_on_b200_keeps_the_reference_behaviour():
+    """`persistkern run --scenario table2-single-sm --backend native` through
+    fresh copies of the reference's cli.py and bench.py bound to this
+    package.  The scenario runs on the B200 (both models, 100 reps), then the
+    reference's own compare step fails exactly as it does on the CPU: its
+    native baseline emits no Dispose row (P/bench.py:233-241 vs 306), a
+    reference defect SURVEY.md section 8(f) notes.  The drop-in reproduces
+    it; the b200 backend (refharness, tests/test_gpu_refharness.py) adds
+    the row and completes."""
+    ours = _ours()
+    bench = _fresh_reference_module("bench", {"persistkern.native": ours["persistkern.native"]})
+    cli = _fresh_reference_module("cli", {"persistkern.bench": bench})
+    assert cli.bench is bench and bench.native is ours["persistkern.native"]
+    scenario = bench.builtin_scenarios()["table2-single-sm"]
+    stats = bench.run_scenario(dataclasses.replace(scenario, backend="native"))
+    assert stats.get("LK", "Wait").samples == scenario.reps
+    assert stats.get("BASE", "Launch").samples == scenario.reps
+    with pytest.raises(KeyError, match="BASE/Dispose"):
+        cli.main(["run", "--scenario", "table2-single-sm", "--backend", "native"])
 
 
 def test_reference_criterion_8_with_reference_validator():
