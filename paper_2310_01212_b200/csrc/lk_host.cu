@@ -230,6 +230,7 @@ struct lk_session {
   volatile unsigned long long* gw_tail = nullptr;   // GATEWAY: events consumed (device-written)
   uint32_t ring_entries = 256;
   uint32_t ev_head = 0;                       // GATEWAY: events appended
+  uint32_t tail_seen = 0;                     // GATEWAY: the consumed count as last read
   std::vector<uint32_t> last_word;            // GATEWAY: shadow of each worker's to_gpu value
   std::mutex post_mu;
   std::vector<uint32_t> all_ids;
@@ -268,6 +269,11 @@ struct lk_session {
   // LK_CF_LAZY_ACK: workers whose NOP ack was written but whose republished
   // NOP has not been seen yet; the next trigger/dispose touching them waits
   std::vector<uint64_t> ack_pending;                      // nwords, under mu
+  // Workers whose NOP the host has observed since its last write to them: a
+  // worker only changes its cell in answer to a host write (a failing one
+  // raises err_any, which every call checks first), so trigger's idle check
+  // need not re-read their cells (native.py:219-220).  Under mu.
+  std::vector<uint64_t> idle_known;
   std::vector<uint8_t> registered;                        // per slot
   std::vector<lk_desc> reg_desc;                          // host copy per slot (as staged)
   std::vector<lk_desc> reg_in;                            // ... and as the caller passed it
@@ -353,10 +359,14 @@ struct lk_session {
       return true;
     }
     std::lock_guard<std::mutex> g(post_mu);   // trigger and wait may run on different host threads
-    const uint64_t deadline = now_ns() + cfg.wait_timeout_ns;
-    while (ev_head - uint32_t(*gw_tail) >= ring_entries - 1) {   // flow control
-      LK_PAUSE();
-      if (now_ns() > deadline) return false;
+    // flow control: the consumed count is re-read (a cache miss: the device
+    // writes that line) only when the count seen last says the ring is full
+    if (ev_head - tail_seen >= ring_entries - 1) {
+      const uint64_t deadline = now_ns() + cfg.wait_timeout_ns;
+      while (ev_head - (tail_seen = uint32_t(*gw_tail)) >= ring_entries - 1) {
+        LK_PAUSE();
+        if (now_ns() > deadline) return false;
+      }
     }
     const uint32_t seq = ++ev_head;
     const uint64_t tag = uint64_t(seq & 0xFFFFu) << 48;
@@ -778,6 +788,7 @@ extern "C" int lk_create(const lk_config* cfg_in, lk_session** out, uint64_t* in
   s->inflight.reserve(64);
   s->scratch.assign(s->nwords, 0);
   s->ack_pending.assign(s->nwords, 0);
+  s->idle_known.assign(s->nwords, 0);
   s->reg_desc.resize(cfg.num_slots);
   s->reg_in.resize(cfg.num_slots);
   s->slot_ver.assign(cfg.num_slots, 0);
@@ -1199,7 +1210,10 @@ static int settle_acks(lk_session* s, const std::vector<uint32_t>& ids) {
   if (due.empty()) return LK_OK;
   int rc = spin_words(s, due, LK_NOP, "wait for ack consumption");
   if (rc) return rc;
-  for (uint32_t i : due) s->ack_pending[i >> 6] &= ~(1ull << (i & 63));
+  for (uint32_t i : due) {
+    s->ack_pending[i >> 6] &= ~(1ull << (i & 63));
+    s->idle_known[i >> 6] |= 1ull << (i & 63);
+  }
   return LK_OK;
 }
 
@@ -1220,6 +1234,7 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   rc = settle_acks(s, ids);
   if (rc) return rc;
   for (uint32_t i : ids) {
+    if (s->idle_known[i >> 6] >> (i & 63) & 1) continue;
     const uint32_t w = s->word(i);
     if (w != LK_NOP) return fail(LK_E_BUSY, "worker %u not idle (from_gpu=%u)", i, w);
   }
@@ -1272,6 +1287,7 @@ static int trigger_locked(lk_session* s, const uint64_t* mask, uint32_t nwords, 
   for (uint32_t i : ids) {
     s->pending[i >> 6] |= 1ull << (i & 63);
     sp[i >> 6] |= 1ull << (i & 63);
+    s->idle_known[i >> 6] &= ~(1ull << (i & 63));
   }
   s->slot_busy[slot] = 1;
   s->inflight.push_back(slot);
@@ -1326,6 +1342,8 @@ static int wait_impl(lk_session* s, const uint64_t* mask, uint32_t nwords, std::
     for (uint32_t k = 0; k < s->nwords; ++k) s->pending[k] &= ~m[k];
     if (lazy)
       for (uint32_t k = 0; k < s->nwords; ++k) s->ack_pending[k] |= m[k];
+    else
+      for (uint32_t k = 0; k < s->nwords; ++k) s->idle_known[k] |= m[k];   // NOP observed above
     // a slot is freed only once every worker it was triggered on was waited (native.py:266-272)
     for (size_t j = 0; j < s->inflight.size();) {
       const uint32_t slot = s->inflight[j];
@@ -1513,6 +1531,7 @@ extern "C" int lk_debug_poke(lk_session* s, uint32_t worker, uint32_t word) {
   if (!s || worker >= s->nw) return fail(LK_E_USAGE, "bad worker");
   std::lock_guard<std::mutex> g(s->mu);
   s->wslot[worker] = 0xFFFFFFFFu;   // a poked WORK may refill the worker's descriptor cache
+  s->idle_known[worker >> 6] &= ~(1ull << (worker & 63));   // its cell may change now
   s->post(std::vector<uint32_t>{worker}, word);
   return LK_OK;
 }
