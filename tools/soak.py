@@ -14,8 +14,11 @@ from paper_2310_01212_b200 import host, native  # noqa: E402
 from paper_2310_01212_b200.device import DeviceBuffer, HostBuffer, WorkDescriptor, reduce_blocks  # noqa: E402
 
 minutes = float(sys.argv[1]) if len(sys.argv) > 1 else 5.0
+mode = sys.argv[2] if len(sys.argv) > 2 else "direct"
+lazy = len(sys.argv) > 3 and sys.argv[3] == "lazy"
 native.pin_host_thread(0)
-s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN))
+s, _ = native.NativeSession.start(native.NativeConfig(num_workers=None, spin_strategy=native.PURE_SPIN,
+                                                      poll_mode=mode, lazy_ack=lazy))
 n = s.num_workers
 empty = WorkDescriptor(slot=0, kind="empty")
 s.register(empty)
@@ -74,6 +77,6 @@ s.dispose()
 s.close()
 dx.free()
 dy.free()
-print(f"soak {minutes:.1f} min: {rounds} handshakes, {payloads} checked saxpy dispatches, {zero_copy} checked "
+print(f"soak {minutes:.1f} min ({mode}{', lazy ack' if lazy else ''}): {rounds} handshakes, {payloads} checked saxpy dispatches, {zero_copy} checked "
       f"zero-copy vector adds, {reduces} bit-exact 16 MiB reduces, no error; "
       f"worst round-robin cycle {worst / 1e3:.1f} us", flush=True)
