@@ -112,6 +112,28 @@ class TimingLog:
     def __repr__(self) -> str:
         return repr(list(self))
 
+    # the rest of list's mutable-sequence surface, for callers that edit the log
+    def insert(self, i: int, t: PhaseTiming) -> None:
+        self._rows.insert(i, (t.phase, t.cycles, t.sm_mask))
+
+    def __setitem__(self, i, t) -> None:
+        if isinstance(i, slice):
+            self._rows[i] = [(x.phase, x.cycles, x.sm_mask) for x in t]
+        else:
+            self._rows[i] = (t.phase, t.cycles, t.sm_mask)
+
+    def __delitem__(self, i) -> None:
+        del self._rows[i]
+
+    def index(self, t, *args) -> int:
+        return self._rows.index((t.phase, t.cycles, t.sm_mask), *args)
+
+    def count(self, t) -> int:
+        return self._rows.count((t.phase, t.cycles, t.sm_mask)) if isinstance(t, PhaseTiming) else 0
+
+    def copy(self) -> list:
+        return list(self)
+
 
 def full_mask(num_sms: int) -> int:
     return (1 << num_sms) - 1
@@ -152,3 +174,8 @@ def timings_csv(rows, backend: Optional[str] = None) -> str:
             cols.append(backend)
         lines.append(",".join(cols))
     return "\n".join(lines) + "\n"
+
+
+import collections.abc as _abc  # noqa: E402
+
+_abc.MutableSequence.register(TimingLog)   # isinstance(session.timings, MutableSequence)

@@ -433,3 +433,21 @@ def test_committed_bench_line_keeps_the_contract():
     r = json.loads((ROOT / "profiles" / "r01_bench_reference_line.json").read_text())
     assert r["impl"] == "reference" and r["metric"] == d["metric"] and r["unit"] == d["unit"]
     assert set(r["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
+
+
+def test_timing_log_mutable_sequence_surface_matches_list():
+    """Every list operation a caller of the reference's ``timings: list``
+    (P/native.py:99) could use gives what the same operation on a list gives."""
+    import collections.abc as abc
+    ts = [host.PhaseTiming(host.PHASE_TRIGGER, k, 0b1) for k in range(1, 6)]
+    log, ref = host.TimingLog(ts), list(ts)
+    assert isinstance(log, abc.MutableSequence)
+    extra = host.PhaseTiming(host.PHASE_WAIT, 99, 0b10)
+    for op in (lambda x: x.insert(1, extra), lambda x: x.__setitem__(0, extra),
+               lambda x: x.__delitem__(2), lambda x: x.__setitem__(slice(0, 2), [ts[4], ts[3]])):
+        op(log)
+        op(ref)
+        assert log == ref and list(log) == ref
+    assert log.index(ts[3]) == ref.index(ts[3]) and log.count(ts[3]) == ref.count(ts[3]) == 2
+    assert log.count(extra) == ref.count(extra) == 0
+    assert log.copy() == ref and isinstance(log.copy(), list)
