@@ -16,14 +16,21 @@ torch.cuda.synchronize) would never return.  The C loop is itself synchronous
 barrier (gloo, CPU-only) on both sides.
 
 Extra objects on the JSON line: latency percentiles and jitter, the
-cudaLaunchKernel+cudaStreamSynchronize baseline, the raw PCIe ping-pong
-floor, the full-148-worker variant, payload HBM GB/s (SAXPY / block reduce
-1-64 MiB, L2-cold by buffer rotation, device globaltimer spans), the roofline
-of the dominant payload kernel and the CPU baseline (oracle port of the
-reference executor, timed on this host).
+cudaLaunchKernel+cudaStreamSynchronize baseline and the cheapest
+conventional flows (empty kernel, stream query, CUDA graph, spin scheduling),
+the raw PCIe ping-pong floor, the full-148-worker variant, payload HBM GB/s
+(SAXPY / block reduce 1-64 MiB, L2-cold by buffer rotation, device
+globaltimer spans) on the payload session and on the DIRECT one, the roofline
+of the dominant payload kernel, zero-copy small transfers against cudaMemcpy
+(and the paper's full-board mailbox workaround), the interference tests,
+Table II through the reference's scenarios, the tail attribution, and the CPU
+baseline (the unmodified reference executor, timed on this host).  The
+latency headline and the speed-up ratios are the last keys of the line.
 
 Multi-GPU (torchrun): one independent LK instance per GPU, host thread pinned
-to the GPU's NUMA-local cores; "replicas only", no collective on the path.
+to the GPU's NUMA-local cores; "replicas only", no collective on the path;
+every rank's p50/p99.9 in `per_rank`.  `--threads`: the same in one process,
+one NUMA-pinned host thread per visible GPU.
 """
 from __future__ import annotations
 
