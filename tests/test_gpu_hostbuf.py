@@ -153,3 +153,19 @@ def test_alloc_and_free_while_resident(session):
         b.array(np.int32)[:] = 7
         b.free()
     run(session, 1, WorkDescriptor(slot=49, kind="empty"))
+
+
+@pytest.mark.parametrize("kind", ["vector_add_i32", "saxpy_f32", "hbm_stream"])
+@pytest.mark.parametrize("where", ["device", "host"])
+def test_empty_payloads_complete_and_touch_nothing(session, kind, where):
+    """n = 0 on every worker (an empty input is legal in the reference's
+    descriptors): the handshake completes, the output guard words are left
+    alone, and the session keeps working."""
+    cls = HostBuffer if where == "host" else DeviceBuffer
+    guard = np.full(4, 0x5A5A5A5A, np.int32)
+    a, b, o = cls.from_array(guard), cls.from_array(guard), cls.from_array(guard)
+    ins = (a,) if kind == "hbm_stream" else (a, b)
+    run(session, host.full_mask(session.num_workers),
+        WorkDescriptor(slot=50, kind=kind, data_in_ref=ins if len(ins) > 1 else ins[0], data_out_ref=o, n=0))
+    np.testing.assert_array_equal(o.download(np.int32, 4), guard)
+    run(session, 1, WorkDescriptor(slot=51, kind="empty"))
