@@ -180,7 +180,10 @@ def _addr(ref) -> int:
         return ref.ptr
     if hasattr(ref, "data_ptr"):
         if hasattr(ref, "is_cuda") and not ref.is_cuda:
-            raise UsageError("payload tensors must live on the GPU")
+            # a pinned CPU tensor is mapped host memory under UVA: zero-copy,
+            # like a HostBuffer (the runtime checks the mapping at staging)
+            if not (hasattr(ref, "is_pinned") and ref.is_pinned()):
+                raise UsageError("payload tensors must live on the GPU or in pinned host memory")
         return int(ref.data_ptr())
     cai = getattr(ref, "__cuda_array_interface__", None)
     if cai is not None:

@@ -169,3 +169,19 @@ def test_empty_payloads_complete_and_touch_nothing(session, kind, where):
         WorkDescriptor(slot=50, kind=kind, data_in_ref=ins if len(ins) > 1 else ins[0], data_out_ref=o, n=0))
     np.testing.assert_array_equal(o.download(np.int32, 4), guard)
     run(session, 1, WorkDescriptor(slot=51, kind="empty"))
+
+
+def test_pinned_torch_tensors_are_zero_copy_payloads(session):
+    """torch CPU tensors in pinned memory (cudaHostAlloc under UVA: mapped,
+    device address = host address) are accepted as zero-copy payload refs
+    like HostBuffers; pageable CPU tensors are refused."""
+    torch = pytest.importorskip("torch")
+    n = 10_001
+    a = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32).pin_memory()
+    b = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32).pin_memory()
+    o = torch.empty(n, dtype=torch.int32).pin_memory()
+    run(session, 0b111, WorkDescriptor(slot=52, kind="vector_add_i32", data_in_ref=(a, b), data_out_ref=o))
+    np.testing.assert_array_equal(o.numpy(), W.vector_add_i32(a.numpy(), b.numpy()))
+    with pytest.raises(UsageError, match="pinned host memory"):
+        WorkDescriptor(slot=53, kind="vector_add_i32", data_in_ref=(torch.zeros(4, dtype=torch.int32),) * 2,
+                       data_out_ref=o).to_c()
