@@ -21,8 +21,8 @@ hbm_stream          src (any, 4-B elements)       dst
 =================== ============================= ===========================
 
 A buffer is a torch CUDA tensor, a :class:`DeviceBuffer`, a
-:class:`HostBuffer` (mapped pinned host memory, zero-copy), or a raw address
-(int) of either kind; the runtime classifies every pointer when it stages the
+:class:`HostBuffer` or a pinned torch CPU tensor (mapped pinned host memory,
+zero-copy), or a raw address (int) of either kind; the runtime classifies every pointer when it stages the
 descriptor and refuses anything else.  ``n`` defaults to the element count of
 the first input.
 """
