@@ -249,6 +249,18 @@ def aggregate(rank_times, rank_units):
 
 # ----------------------------------------------------------------------------- CPU baseline
 
+MIN_TIMED_ROUNDS = 20
+
+
+def _over_budget(t_start, budget_s, k, warmup, timed):
+    """Stop a bounded CPU sample once its time budget is spent, but never
+    before MIN_TIMED_ROUNDS timed rounds (a small budget may be spent in the
+    warm-up alone)."""
+    if timed >= MIN_TIMED_ROUNDS and time.perf_counter() - t_start > budget_s:
+        return True
+    return False
+
+
 def cpu_baseline_config0(num_workers=4, rounds=1000, warmup=50, n=65536, threshold=10_000, budget_s=30.0):
     """BASELINE config 0 on this host's cores: 4 workers, int32 vector add of
     64 Ki elements run on the worker thread, round-robin masks, the given
@@ -304,7 +316,7 @@ def cpu_baseline_config0(num_workers=4, rounds=1000, warmup=50, n=65536, thresho
         s.wait(m)
         if k >= warmup:
             lat.append(time.perf_counter_ns() - t0)
-        if time.perf_counter() - t_start > budget_s:
+        if _over_budget(t_start, budget_s, k, warmup, len(lat)):
             break
     s.dispose()
     assert np.array_equal(out, W.vector_add_i32(a, b))
@@ -344,7 +356,7 @@ def cpu_spawn_baseline_config0(rounds=1000, warmup=50, n=65536, budget_s=10.0):
             base.wait()
             if k >= warmup:
                 lat.append(time.perf_counter_ns() - t0)
-            if time.perf_counter() - t_start > budget_s:
+            if _over_budget(t_start, budget_s, k, warmup, len(lat)):
                 break
     finally:
         ref_native._busy_loop = orig
