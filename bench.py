@@ -1020,10 +1020,20 @@ def run_lk_arm(args, world, rank, local):
         os.sched_setaffinity(0, {pinned_core})
     except Exception:
         pinned = 0
+    # under ncu (which serialises launches) the same command still runs: the
+    # descriptors live in mapped host memory and the legs that make CUDA
+    # calls while a session is resident (payload buffers, cudaMemcpy probes,
+    # the payload/interference/zero-copy sessions) are skipped. The line is
+    # then a launch-list run, not a bench value.
+    prof = native.under_profiler()
+    if prof:
+        args.no_payload = args.no_interference = args.no_lazy = args.no_green = True
+        args.no_zero_copy = args.no_table2 = True
     cfg = native.NativeConfig(num_workers=args.workers, device=device, spin_strategy=native.PURE_SPIN,
                               poll_backoff_ns=args.backoff_ns, cell_stride=args.cell_stride,
                               poll_replicas=args.replicas, poll_spacing_ns=args.spacing_ns,
-                              poll_mode=args.poll_mode, tma_payload=not args.lsu_payload)
+                              poll_mode=args.poll_mode, tma_payload=not args.lsu_payload,
+                              host_descriptors=prof)
     session, init = native.NativeSession.start(cfg)
     n = session.num_workers
     empty = WorkDescriptor(slot=0, kind="empty")
@@ -1056,12 +1066,14 @@ def run_lk_arm(args, world, rank, local):
                                         "elapsed_s": round(elapsed, 6), "tasks_per_s": round(rounds / elapsed, 1),
                                         "p50_us": mine["p50_us"], "p99.9_us": mine["p99.9_us"]})
 
-    tl = session.last_timeline().astype(np.int64)
-    dev_cyc = (tl[:, 7] - tl[:, 5]).astype(np.float64)
-    extras = {"device_handling": {
-        "what": "clock64 cycles, each worker's last timed dispatch: to_gpu value seen -> FINISHED store issued",
-        "p50_cycles": float(np.median(dev_cyc)), "max_cycles": float(dev_cyc.max()),
-        "p50_us_at_max_clock": round(float(np.median(dev_cyc)) / SM_MAX_GHZ / 1e3, 4)}}
+    extras = {}
+    if not prof:   # a device->host copy of the timeline words
+        tl = session.last_timeline().astype(np.int64)
+        dev_cyc = (tl[:, 7] - tl[:, 5]).astype(np.float64)
+        extras["device_handling"] = {
+            "what": "clock64 cycles, each worker's last timed dispatch: to_gpu value seen -> FINISHED store issued",
+            "p50_cycles": float(np.median(dev_cyc)), "max_cycles": float(dev_cyc.max()),
+            "p50_us_at_max_clock": round(float(np.median(dev_cyc)) / SM_MAX_GHZ / 1e3, 4)}
     # tail attribution (untimed): the same loop with the host thread's own
     # spin gaps recorded per round; a round slower than p50 + 2 us whose host
     # thread stalled >= 1 us was slowed on the host side, not on the link/GPU
@@ -1107,7 +1119,7 @@ def run_lk_arm(args, world, rank, local):
     # the small-transfer case the paper's pathology is about (PAPER:160-162,
     # P/link.py:84-122): a 4-byte cudaMemcpy each way (stream-synchronous)
     # next to the mailbox word round trip above
-    if rank == 0:
+    if rank == 0 and not prof:
         extras["small_transfer"] = measure_small_transfer(device, 2000)
 
     # several host threads, each a closed loop over its own worker group (one
@@ -1245,8 +1257,9 @@ def run_lk_arm(args, world, rank, local):
         except Exception as exc:  # pragma: no cover
             floor[name] = {"error": str(exc)}
     base["floor"] = floor
-    pp = native.pingpong(device, args.pp_rounds)
-    extras["pingpong_floor"] = lat_summary(pp[100:])
+    if not prof:   # the ping-pong kernel waits on the host: a serialised launch would never return
+        pp = native.pingpong(device, args.pp_rounds)
+        extras["pingpong_floor"] = lat_summary(pp[100:])
 
     if rank != 0:
         return
@@ -1350,6 +1363,8 @@ def run_lk_arm(args, world, rank, local):
                            "dispatched by mailbox words, not launches",
         "per_rank": per_rank,
         "smid_distinct": len(set(smids)),
+        **({"profiled": "run under a profiler: launch list only, not a bench value; session legs that "
+                        "call CUDA while resident were skipped"} if prof else {}),
         "clocks": clk.summary(),
         # headline last: the driver keeps the tail of the line
         **{k: extras[k] for k in HEADLINE_EXTRAS if k in extras},
