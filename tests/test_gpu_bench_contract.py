@@ -42,3 +42,22 @@ def test_bench_line_keeps_the_contract():
     assert d["gpu_launches"] >= 1
     keys = list(d)
     assert keys[-1] == "speedup_vs_launch_sync_p999" and "latency_us" in keys[-6:]
+
+
+def test_bench_profiler_mode_skips_live_session_cuda_legs():
+    """Under a profiler (detected from ncu's environment, faked here without
+    any injection) bench.py keeps host descriptors and skips the legs that
+    call CUDA while a session is resident; the line says it is not a bench
+    value. profiles/r02_bench_launches_ncu.csv is this mode under real ncu."""
+    import os
+    env = dict(os.environ, NV_TPS_LAUNCH_TOKEN="test")
+    cmd = [sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--rounds", "2000",
+           "--full-rounds", "2000", "--e2e-rounds", "2000", "--base-rounds", "2000", "--attrib-rounds", "2000",
+           "--driver-rounds", "2000", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=280, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert "profiled" in d and d["roofline"] is None and d["payload"] == {}
+    for k in ("device_handling", "small_transfer", "pingpong_floor", "zero_copy", "lazy_ack", "interference"):
+        assert k not in d, k
+    assert d["value"] > 10_000 and d["gpu_launches"] >= 1
