@@ -130,12 +130,20 @@ __device__ __forceinline__ void st4(uint4* p, uint4 v) {
 // kStageBytes are in flight per SM (6 x 16 KiB = 96 KiB by default: at
 // ~44 GB/s per SM and a loaded HBM latency of ~1.5 us Little's law asks for
 // ~66 KiB per SM; 6 measured best of 4/6/8/12, tools/ab_stages.py), issued
-// by one elected thread while the other warps consume.  The ring persists across dispatches: `g` counts tiles consumed
-// since the barriers were initialised (identical in every thread), so
-// stage = g % stages and the mbarrier phase parity = (g / stages) & 1.
+// by one elected thread while the other warps consume.  The ring persists
+// across dispatches: `g` is the ring position (identical in every thread),
+// kept modulo 2 x stages, so stage = g mod stages and the mbarrier phase
+// parity = g / stages come from one compare (rp_* below).  A tile count
+// would need two u32 divisions by the run-time stage count per tile (~100
+// cycles each on the producer's path to the first copy) and would break
+// the stage/phase mapping when it wrapped at 2^32 (2^32 mod 6 != 0).
 constexpr uint32_t kStageBytes = 16384;
 constexpr uint32_t kMaxStages = 12;
 constexpr uint32_t kDefaultStages = 6;
+
+__device__ __forceinline__ uint32_t rp_stage(uint32_t pos, uint32_t S) { return pos >= S ? pos - S : pos; }
+__device__ __forceinline__ uint32_t rp_parity(uint32_t pos, uint32_t S) { return pos >= S ? 1u : 0u; }
+__device__ __forceinline__ uint32_t rp_next(uint32_t pos, uint32_t S) { return pos + 1 == 2 * S ? 0u : pos + 1; }
 
 struct Ring {
   uint8_t* buf;       // stages x kStageBytes, 128-B aligned, dynamic shared memory
@@ -220,29 +228,34 @@ template <class Load, class Use>
 __device__ __forceinline__ void ring_stream(Ring& r, uint32_t& g, uint32_t ntiles, uint32_t T, const Load& load,
                                             const Use& use) {
   const uint32_t c0 = g, S = r.stages;
+  uint32_t f = c0;                                  // the producer's position (tiles are filled in order)
   auto fill = [&](uint32_t i) {
-    const uint32_t f = c0 + i, st = f % S;
-    mbar_wait(r.empty + st, ((f / S) & 1u) ^ 1u);   // previous use of this stage released
+    const uint32_t st = rp_stage(f, S);
+    mbar_wait(r.empty + st, rp_parity(f, S) ^ 1u);  // previous use of this stage released
     load(i, r.buf + st * kStageBytes, r.full + st);
+    f = rp_next(f, S);
   };
   const bool split = T >= 64;
   const uint32_t ci = split ? threadIdx.x - 32 : threadIdx.x, nc = split ? T - 32 : T;
   if (split && threadIdx.x < 32) {
     if (threadIdx.x == 0)
       for (uint32_t i = 0; i < ntiles; ++i) fill(i);
+    g = __shfl_sync(0xffffffffu, f, 0);             // the producer's position after its last fill
   } else {
     if (!split && threadIdx.x == 0)
       for (uint32_t i = 0; i < ntiles && i < S - 1; ++i) fill(i);
+    uint32_t c = c0;
     for (uint32_t i = 0; i < ntiles; ++i) {
       if (!split && threadIdx.x == 0 && i + S - 1 < ntiles) fill(i + S - 1);
-      const uint32_t c = c0 + i, st = c % S;
-      mbar_wait(r.full + st, (c / S) & 1u);
+      const uint32_t st = rp_stage(c, S);
+      mbar_wait(r.full + st, rp_parity(c, S));
       use(i, r.buf + st * kStageBytes, ci, nc);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(r.empty + st);
+      c = rp_next(c, S);
     }
+    g = c;
   }
-  g = c0 + ntiles;
 }
 
 // ---------------------------------------------------------------- work items
@@ -573,10 +586,10 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
   uint64_t* const emptyr = r.empty + kMaxStages;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    uint32_t f = *r.gred;
+    uint32_t f = *r.gred;                                          // ring position, modulo 2S
     auto fill = [&](uint32_t b) {                                  // b = block or kTileEnd
-      const uint32_t st = f % S;
-      mbar_wait(emptyr + st, ((f / S) & 1u) ^ 1u);
+      const uint32_t st = rp_stage(f, S);
+      mbar_wait(emptyr + st, rp_parity(f, S) ^ 1u);
       r.tile[st] = b;
       if (b == kTileEnd) {
         mbar_arrive(fullr + st);                                   // wake the owner, no bytes
@@ -586,7 +599,7 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
         mbar_expect_tx(fullr + st, bytes);                         // 0 bytes: a tail-only block
         if (bytes) bulk_g2s(r.buf + st * kStageBytes, x4 + v0, bytes, fullr + st);
       }
-      ++f;
+      f = rp_next(f, S);
     };
     // the first claim goes out right after the first static copy (before it
     // when there is no static share): its L2 round trip overlaps the copies,
@@ -610,11 +623,13 @@ __device__ __forceinline__ void reduce_dyn(const lk_desc& d, uint32_t rank, uint
     *r.gred = f;                                                   // read by all after the closing barrier
   } else if (warp >= 1 && warp <= S) {
     const uint32_t st = warp - 1;
-    const uint32_t c0 = *r.gred;
-    uint32_t p = c0 + (st + S - c0 % S) % S;                       // this stage's first position
-    for (;; p += S) {
-      mbar_wait(fullr + st, (p / S) & 1u);
-      if (tl && p == c0 && lane == 0) tl[14] = globaltimer();      // the dispatch's first stage landed
+    const uint32_t c0 = *r.gred, s0 = rp_stage(c0, S);
+    // parity of this stage's first position at or after c0 (the next lap
+    // when the stage precedes c0's); every later use is S positions on
+    uint32_t par = rp_parity(c0, S) ^ (st < s0 ? 1u : 0u);
+    for (bool first = st == s0;; par ^= 1u, first = false) {
+      mbar_wait(fullr + st, par);
+      if (tl && first && lane == 0) tl[14] = globaltimer();        // the dispatch's first stage landed
       const uint32_t b = r.tile[st];
       if (b == kTileEnd) {
         __syncwarp();
