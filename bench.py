@@ -31,6 +31,11 @@ Multi-GPU (torchrun): one independent LK instance per GPU, host thread pinned
 to the GPU's NUMA-local cores; "replicas only", no collective on the path;
 every rank's p50/p99.9 in `per_rank`.  `--threads`: the same in one process,
 one NUMA-pinned host thread per visible GPU.
+
+Under ncu (`ncu --metrics gpu__time_duration.sum python bench.py ...`) the
+same command runs for its launch list: the session keeps its descriptors in
+mapped host memory and the legs that make CUDA calls while a session is
+resident are skipped; the line is marked "profiled" and is not a bench value.
 """
 from __future__ import annotations
 
