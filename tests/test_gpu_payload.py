@@ -89,7 +89,7 @@ def test_misaligned_pointers_take_scalar_path(session):
     np.testing.assert_array_equal(do.download(np.int32, n + 1)[1:], W.vector_add_i32(a[1:], b[1:]))
 
 
-@pytest.mark.parametrize("n", [1 << 18, 12345, 4 << 20])
+@pytest.mark.parametrize("n", [1, 33, 1 << 18, 12345, 4 << 20])
 def test_saxpy_f32_bit_exact_in_place(session, n):
     x, y = _f32(n, 2), _f32(n, 3)
     dx, dy = DeviceBuffer.from_array(x), DeviceBuffer.from_array(y)
@@ -103,6 +103,35 @@ def test_saxpy_f32_bit_exact_in_place(session, n):
                                       alpha=1.5))
     want2 = W.saxpy_f32(1.5, x, want)
     np.testing.assert_array_equal(dy.download(np.float32, n).view(np.uint32), want2.view(np.uint32))
+
+
+@pytest.mark.parametrize("kind", ["vector_add_i32", "saxpy_f32", "hbm_stream"])
+@pytest.mark.parametrize("mask_name", ["one", "odd", "full"])
+@pytest.mark.parametrize("n", [31, 4097, 300_007])
+def test_map_writes_stop_at_n(session, kind, mask_name, n):
+    """The last worker's shard ends at n: the output's guard words past n
+    (inside the same allocation) are never written, whatever the shard
+    boundaries and the path (ring tiles, LSU tails)."""
+    pad = 64
+    guard = np.int32(0x5A5A5A5A)
+    if kind == "saxpy_f32":   # finite floats: NaN payloads differ between numpy and the device
+        a, b = _f32(n + pad, 7).view(np.int32), _f32(n + pad, 8).view(np.int32)
+    else:
+        a, b = _i32(n + pad, 7), _i32(n + pad, 8)
+    out = np.full(n + pad, guard, np.int32)
+    da, db, do = DeviceBuffer.from_array(a), DeviceBuffer.from_array(b), DeviceBuffer.from_array(out)
+    ins = da if kind == "hbm_stream" else (da, db)
+    run(session, MASKS[mask_name](session.num_workers),
+        WorkDescriptor(slot=48, kind=kind, data_in_ref=ins, data_out_ref=do, n=n, alpha=1.5))
+    got = do.download(np.int32, n + pad)
+    np.testing.assert_array_equal(got[n:], out[n:])
+    if kind == "vector_add_i32":
+        want = W.vector_add_i32(a[:n], b[:n])
+    elif kind == "saxpy_f32":
+        want = W.saxpy_f32(1.5, a[:n].view(np.float32), b[:n].view(np.float32)).view(np.int32)
+    else:
+        want = a[:n]
+    np.testing.assert_array_equal(got[:n], want)
 
 
 def test_saxpy_after_host_rewrite_is_coherent(session):
