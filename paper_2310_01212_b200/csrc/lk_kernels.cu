@@ -152,8 +152,7 @@ struct Ring {
   uint64_t* empty;    // same layout: one arrival per consumer warp (maps) / the stage's owner warp (reduce)
   uint32_t stages;    // <= kMaxStages
   uint32_t* tile;     // stages: global tile index a stage holds (dynamic schedule), shared memory
-  uint32_t* gshared;  // the ring count after a dynamic stream, for threads that did not count it
-  uint32_t* gred;     // shared memory: positions the owner-warp ring has used (persists across dispatches)
+  uint32_t* gred;     // shared memory: the owner-warp ring's position, modulo 2 x stages (persists across dispatches)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1310,7 +1309,7 @@ struct PersistSmem {
   uint32_t cmd, rank, count, slot;
   ReduceSmem red;
   uint64_t full[2 * kMaxStages], empty[2 * kMaxStages];
-  uint32_t tile[kMaxStages], ring_g, ring_gr;
+  uint32_t tile[kMaxStages], ring_gr;
   unsigned long long chan[2];      // HYBRID: latest direct-cell value, latest mailbox value
   lk_desc cdesc;                   // this worker's last fetched descriptor (LK_HINT_CACHED)
   unsigned long long cmask[4];     // ... and its slot's trigger mask
@@ -1341,7 +1340,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
     return;
   }
   extern __shared__ __align__(128) uint8_t dyn_smem[];
-  Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages, sm.tile, &sm.ring_g, &sm.ring_gr};
+  Ring ring{dyn_smem, sm.full, sm.empty, a.ring_stages, sm.tile, &sm.ring_gr};
   const bool ring_ok = a.use_tma != 0;
   uint32_t g = 0;
   if (ring_ok) ring_init(ring, T);
@@ -1489,7 +1488,7 @@ __global__ void __launch_bounds__(kPersistMaxThreads, 1) lk_persistent_kernel(co
 __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, uint32_t* ctr, int use_tma) {
   __shared__ ReduceSmem rs;
   __shared__ uint64_t full[2 * kMaxStages], empty[2 * kMaxStages];
-  __shared__ uint32_t tile[kMaxStages], gsh, gred;
+  __shared__ uint32_t tile[kMaxStages], gred;
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   if (single_thread_kind(d.kind)) {
     // the result goes to global memory (the counter line's spare word), which
@@ -1497,7 +1496,7 @@ __global__ void __launch_bounds__(kMaxThreads) lk_work_kernel(const lk_desc d, u
     if (threadIdx.x == 0 && d.kind == LK_KIND_BUSY_LOOP) ctr[3] = busy_loop(d.iterations);
     return;
   }
-  Ring ring{dyn_smem, full, empty, kDefaultStages, tile, &gsh, &gred};
+  Ring ring{dyn_smem, full, empty, kDefaultStages, tile, &gred};
   uint32_t g = 0;
   if (use_tma) ring_init(ring, blockDim.x);
   run_multi(d, blockIdx.x, gridDim.x, ctr, rs, blockDim.x, ring, use_tma != 0, g);
